@@ -1,0 +1,138 @@
+/*
+ * pint_b200.h -- C ABI of the B200-native batched fine propagator for
+ * Parareal ALE fluid-structure interaction (arXiv:1907.01252).
+ *
+ * The reference (pintbench, pure Python) has no FFI: its plug-in point for
+ * this hot path is the duck-typed Propagator protocol
+ * `{step, cost_hint, advance(state, t_end)}` (reference
+ * pkg/src/pintbench/integrators.py:105-112) implemented by ThetaPropagator
+ * (integrators.py:126-166), plus the Parareal correction helpers
+ * `parareal_update` / `theta_weight` (parareal.py:154-197) and the correction
+ * norm (parareal.py:429-431).  Every entry point below replaces one of those
+ * call sites; the Python host layer (paper_1907_01252_b200/propagator.py)
+ * binds them with ctypes and keeps the reference's Python API.  See
+ * INTEGRATION.md for the binding a maintainer would add to pintbench.
+ *
+ * Conventions
+ *  - plain pointers and sizes; device pointers are CUDA global memory
+ *    addresses owned by the caller (PyTorch tensors in this repo);
+ *  - a batch of S slices is one contiguous buffer [S][C][np]: C = 2*dim+1
+ *    field components (vx, vy[, vz], ux, uy[, uz], p), each padded from
+ *    nn nodes to np (pint_sizes) doubles; padding entries must be zero;
+ *  - every call is enqueued on `stream` (cudaStream_t, NULL = legacy default);
+ *    calls that return host results synchronise that stream;
+ *  - return value: PINT_OK or an error code; pint_last_error() explains;
+ *  - all arithmetic is fp64 and bitwise deterministic, and a slice's result
+ *    does not depend on which other slices share the launch.
+ */
+#ifndef PINT_B200_H
+#define PINT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PINT_OK = 0,
+  PINT_NUMERIC_BREAKDOWN = 1, /* linalg.py:17 NumericBreakdown            */
+  PINT_NEWTON_MAX_ITERS = 2,  /* linalg.py:21 MaxItersExceeded            */
+  PINT_MESH_DEGENERATE = 3,   /* problems.py:36 MeshDegenerate            */
+  PINT_INVALID_ARG = 4,
+  PINT_CUDA_ERROR = 5
+};
+
+typedef struct pint_ctx pint_ctx;
+
+/* Problem description: the FSIProblem dataclass
+ * (paper_1907_01252_b200/problem.py); replaces ProblemSpec
+ * (problems.py:136-151) for the FSI path. */
+typedef struct pint_problem_desc {
+  int32_t dim;          /* 2 or 3 */
+  int32_t cells[3];     /* cells per direction (cells[2] ignored in 2-d) */
+  double extent[3];
+  double bar_lo[3], bar_hi[3];
+  double rho_f, nu_f, rho_s, mu_s, lambda_s;
+  double u_peak, ramp_time, delta_p;
+} pint_problem_desc;
+
+/* NewtonSettings (linalg.py:129-149) minus the FD epsilon (exact Jacobian). */
+typedef struct pint_newton_opts {
+  double abs_tol, rel_tol;
+  int32_t max_iters;
+  double damping_min;
+} pint_newton_opts;
+
+/* GMRES(restart) right-preconditioned by a geometric V-cycle. */
+typedef struct pint_krylov_opts {
+  double rtol, atol;
+  int32_t restart, max_iters;
+  int32_t pre_smooth, post_smooth;
+  double omega;
+  int32_t max_levels;    /* 0 = as many as the mesh allows */
+  int32_t coarse_sweeps; /* block-Jacobi sweeps when the coarsest level is too big for a dense inverse */
+} pint_krylov_opts;
+
+/* ---- lifetime -------------------------------------------------------- */
+int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out);
+int pint_destroy(pint_ctx* ctx);
+const char* pint_last_error(const pint_ctx* ctx);
+/* nn nodes, np padded stride, C dofs/node, number of multigrid levels */
+int pint_sizes(const pint_ctx* ctx, int32_t* nn, int32_t* np, int32_t* C, int32_t* levels);
+/* node flags (uint8 per node: 1 solid-touch, 2 fluid-touch, 4 Dirichlet v, 8 Dirichlet u)
+ * and cell flags (1 solid, 2 outflow) into host buffers, for cross-checks */
+int pint_flags(const pint_ctx* ctx, uint8_t* node_flags, uint8_t* cell_flags);
+
+/* ---- fine propagation: replaces ThetaPropagator.advance, batched --------
+ * Advances each slice s from t0[s] to t_end[s] in nsteps[s] shifted-CN
+ * steps of size k (the last one absorbs the rounding slack exactly as
+ * integrators.py:154-162), theta = 1/2 + theta0*k_step clamped to [1/2, 1]
+ * (integrators.py:73), Newton guess = previous state (integrators.py:93).
+ * y_in / y_out: device [S][C][np].  Host outputs per slice: Newton
+ * iterations, Krylov iterations, status (PINT_*), failing t_n. */
+int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, const double* t0,
+                   const double* t_end, const int32_t* nsteps, double k, double theta0,
+                   const pint_newton_opts* newton, const pint_krylov_opts* krylov, int32_t* newton_iters,
+                   int32_t* krylov_iters, int32_t* status, double* fail_t, void* stream);
+
+/* ---- kernel-level entry points (parity ladder + c5 roofline sweep) ----
+ * Per-slice step data: k[s], theta[s], t1[s] (host arrays).
+ * residual: r = R(y; y_old) with Dirichlet/identity rows (integrators.py:83-88
+ * analogue); norms (host, may be NULL) = ||r_s||_2, +inf on a degenerate mesh. */
+int pint_residual(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                  const double* theta, const double* t1, double* r, double* norms, void* stream);
+/* matrix-free Jacobian-vector product J(y) w */
+int pint_jvp(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* w, const double* k,
+             const double* theta, const double* t1, double* Jw, void* stream);
+/* assemble the block-stencil Jacobian into the context (level 0) */
+int pint_assemble(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                  const double* theta, const double* t1, void* stream);
+/* copy the assembled block-stencil Jacobian [S][noff][C][C][np] out (device) */
+int pint_jacobian_blocks(pint_ctx* ctx, int32_t S, double* out, void* stream);
+/* y = J x with the assembled Jacobian */
+int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream);
+/* multigrid setup on the assembled Jacobian and one V-cycle x = M^{-1} b */
+int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov, void* stream);
+int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, void* stream);
+/* GMRES solve J x = b with the current preconditioner; its/resid per slice (host) */
+int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, const pint_krylov_opts* krylov,
+                      int32_t* its, double* resid, void* stream);
+
+/* ---- Parareal correction (parareal.py:154-197, 422-431) ---------------
+ * K8a, batched over S slices: delta = f_old - c_old. */
+int pint_parareal_precorrect(int32_t S, int32_t C, int32_t nn, int32_t np, const double* f_old,
+                             const double* c_old, double* delta, void* stream);
+/* K8b, one slice inside the sequential sweep: theta (host out) =
+ * theta_weight(f_old, c_new, variant, clamp) with variant 0 classic,
+ * 1 least_squares, 2 angle_penalized; x_new = theta c_new + f_old - theta c_old;
+ * corr (host out) = ||x_new - x_prev|| / ||x_new|| (0 if equal, inf if ||x_new|| = 0). */
+int pint_parareal_correct_one(int32_t C, int32_t nn, int32_t np, const double* c_new, const double* f_old,
+                              const double* c_old, const double* x_prev, double* x_new, int32_t variant,
+                              double clamp_lo, double clamp_hi, double* theta_out, double* corr_out,
+                              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINT_B200_H */

@@ -1,0 +1,635 @@
+// K3 block-stencil SpMV, K4 geometric-multigrid preconditioner (Galerkin RAP,
+// node-block Jacobi smoother, dense coarsest solve), K5 deterministic
+// per-slice reductions and K6 Krylov vector updates.  All kernels are batched
+// over slices (grid.y) and honour a per-slice active mask so diverging Newton /
+// Krylov iteration counts never change a slice's arithmetic (batch
+// invariance, SURVEY.md §8b Determinism row).
+#pragma once
+
+#include "pint_common.cuh"
+
+namespace pint {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedChunk = 4096;  // elements per reduction block (fixed => batch invariant)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order block reduction; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double out = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int w = 0; w < nw; ++w) out += sh[w];
+  }
+  __syncthreads();
+  return out;
+}
+
+// ---------------------------------------------------------------- generic vector kernels
+__global__ void k_zero_active(double* __restrict__ x, size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  double* xs = x + s * per_slice;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    xs[i] = 0.0;
+}
+
+__global__ void k_copy_active(double* __restrict__ dst, const double* __restrict__ src, size_t per_slice,
+                              const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    dst[s * per_slice + i] = src[s * per_slice + i];
+}
+
+// y = a_s * x + y  (a per slice)
+__global__ void k_axpy_slice(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ a,
+                             double sign, size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double al = sign * a[s];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    y[s * per_slice + i] += al * x[s * per_slice + i];
+}
+
+// out = x + lam_s * d
+__global__ void k_trial(double* __restrict__ out, const double* __restrict__ x, const double* __restrict__ d,
+                        const double* __restrict__ lam, size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double l = lam[s];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    out[s * per_slice + i] = x[s * per_slice + i] + l * d[s * per_slice + i];
+}
+
+// out = -x
+__global__ void k_negate(double* __restrict__ out, const double* __restrict__ x, size_t per_slice,
+                         const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    out[s * per_slice + i] = -x[s * per_slice + i];
+}
+
+// out = x / a_s  (a_s == 0 -> out = 0)
+__global__ void k_scale_inv(double* __restrict__ out, const double* __restrict__ x, const double* __restrict__ a,
+                            size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double al = a[s];
+  const double inv = al != 0.0 ? 1.0 / al : 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    out[s * per_slice + i] = x[s * per_slice + i] * inv;
+}
+
+// ---------------------------------------------------------------- K5 reductions
+// partial[s][blk] = sum over the block's chunk of x*y (x == y for norms)
+__global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __restrict__ x, const double* __restrict__ y,
+                                                            size_t per_slice, double* __restrict__ partial, int nblk,
+                                                            const int* __restrict__ active) {
+  __shared__ double sh[kRedThreads / 32];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const size_t base = (size_t)blockIdx.x * kRedChunk;
+  const double* xs = x + s * per_slice;
+  const double* ys = y + s * per_slice;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+    const size_t e = base + i;
+    if (e < per_slice) acc += xs[e] * ys[e];
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partial[(size_t)s * nblk + blockIdx.x] = acc;
+}
+
+// out[s] = sum_b partial[s][b] (sequential fixed order); sqrt if requested;
+// +inf if the slice flagged a degenerate mesh
+__global__ void k_dot_final(const double* __restrict__ partial, int nblk, double* __restrict__ out, int S, int take_sqrt,
+                            const int* __restrict__ degen, const int* __restrict__ active) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (active && !active[s]) return;
+  double acc = 0.0;
+  for (int b = 0; b < nblk; ++b) acc += partial[(size_t)s * nblk + b];
+  if (take_sqrt) acc = sqrt(acc);
+  if (degen && degen[s]) acc = __longlong_as_double(0x7ff0000000000000LL);
+  out[s] = acc;
+}
+
+// multi-dot: partial[s][i][blk] = <V_i, w> over the chunk, i = 0..nv-1
+__global__ void __launch_bounds__(kRedThreads) k_mdot_partial(const double* __restrict__ V, size_t vstride,
+                                                             const double* __restrict__ w, int nv, size_t per_slice,
+                                                             double* __restrict__ partial, int nblk, int maxv,
+                                                             const int* __restrict__ active) {
+  __shared__ double sh[kRedThreads / 32];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const size_t base = (size_t)blockIdx.x * kRedChunk;
+  const double* ws = w + s * per_slice;
+  for (int v = 0; v < nv; ++v) {
+    const double* vs = V + v * vstride + s * per_slice;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+      const size_t e = base + i;
+      if (e < per_slice) acc += vs[e] * ws[e];
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
+  }
+}
+
+// h[s][i] (+)= sum_b partial[s][i][b]
+__global__ void k_mdot_final(const double* __restrict__ partial, int nblk, int nv, int maxv, double* __restrict__ h,
+                             int hstride, int accumulate, int S, const int* __restrict__ active) {
+  const int s = blockIdx.x;
+  if (s >= S) return;
+  if (active && !active[s]) return;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += partial[((size_t)s * maxv + v) * nblk + b];
+    if (accumulate) h[(size_t)s * hstride + v] += acc;
+    else h[(size_t)s * hstride + v] = acc;
+  }
+}
+
+// w -= sum_i coef[s][i] V_i   (fixed order in i)
+__global__ void k_mupdate(double* __restrict__ w, const double* __restrict__ V, size_t vstride,
+                          const double* __restrict__ coef, int cstride, int nv, size_t per_slice,
+                          const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double* cs = coef + (size_t)s * cstride;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < per_slice; e += (size_t)gridDim.x * blockDim.x) {
+    double acc = w[s * per_slice + e];
+    for (int v = 0; v < nv; ++v) acc -= cs[v] * V[v * vstride + s * per_slice + e];
+    w[s * per_slice + e] = acc;
+  }
+}
+
+// out = sum_i coef[s][i] V_i (nv per slice from nvs[s])
+__global__ void k_mcombine(double* __restrict__ out, const double* __restrict__ V, size_t vstride,
+                           const double* __restrict__ coef, int cstride, const int* __restrict__ nvs,
+                           size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double* cs = coef + (size_t)s * cstride;
+  const int nv = nvs[s];
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < per_slice; e += (size_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int v = 0; v < nv; ++v) acc += cs[v] * V[v * vstride + s * per_slice + e];
+    out[s * per_slice + e] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- K3 block-stencil SpMV
+// y = A x  or  y = b - A x (residual form)
+template <int D, bool RESID>
+__global__ void __launch_bounds__(128) k_spmv(Grid g, const double* __restrict__ A, const double* __restrict__ x,
+                                             const double* __restrict__ b, double* __restrict__ y,
+                                             const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.nn) return;
+  const int np = g.np;
+  const size_t vs = (size_t)C * np;
+  const double* As = A + (size_t)s * NOFF * C * C * np + n;
+  const double* xs = x + s * vs;
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+#pragma unroll
+  for (int off = 0; off < NOFF; ++off) {
+    const int nb = neighbour(g, i, j, k, off);
+    if (nb < 0) continue;
+    double xv[C];
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) xv[cb] = __ldg(xs + cb * np + nb);
+#pragma unroll
+    for (int ca = 0; ca < C; ++ca)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) acc[ca] += __ldg(As + ((size_t)(off * C + ca) * C + cb) * np) * xv[cb];
+  }
+  double* ys = y + s * vs;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (RESID) ys[c * np + n] = b[s * vs + c * np + n] - acc[c];
+    else ys[c * np + n] = acc[c];
+  }
+}
+
+// ---------------------------------------------------------------- K4 node-block Jacobi
+// Dinv[s][ca][cb][n] = inverse of the centre block (Gauss-Jordan, partial pivoting)
+template <int D>
+__global__ void k_block_inverse(Grid g, const double* __restrict__ A, double* __restrict__ Dinv,
+                                const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.nn) return;
+  const int np = g.np;
+  const int ctr = center_offset(D);
+  const double* As = A + (size_t)s * NOFF * C * C * np;
+  double a[C][2 * C];
+  for (int r = 0; r < C; ++r)
+    for (int c = 0; c < 2 * C; ++c)
+      a[r][c] = c < C ? As[(((size_t)ctr * C + r) * C + c) * np + n] : (c - C == r ? 1.0 : 0.0);
+  for (int p = 0; p < C; ++p) {
+    int piv = p;
+    double best = fabs(a[p][p]);
+    for (int r = p + 1; r < C; ++r)
+      if (fabs(a[r][p]) > best) { best = fabs(a[r][p]); piv = r; }
+    if (piv != p)
+      for (int c = 0; c < 2 * C; ++c) { double t = a[p][c]; a[p][c] = a[piv][c]; a[piv][c] = t; }
+    const double d = a[p][p];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+    for (int c = 0; c < 2 * C; ++c) a[p][c] *= inv;
+    for (int r = 0; r < C; ++r) {
+      if (r == p) continue;
+      const double f = a[r][p];
+      if (f != 0.0)
+        for (int c = 0; c < 2 * C; ++c) a[r][c] -= f * a[p][c];
+    }
+  }
+  double* Ds = Dinv + (size_t)s * C * C * np;
+  for (int r = 0; r < C; ++r)
+    for (int c = 0; c < C; ++c) Ds[((size_t)r * C + c) * np + n] = a[r][C + c];
+}
+
+// x_out = (x_in ? x_in : 0) + omega Dinv (b - A x_in)
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(128) k_smooth(Grid g, const double* __restrict__ A, const double* __restrict__ Dinv,
+                                               const double* __restrict__ b, const double* __restrict__ xin,
+                                               double* __restrict__ xout, double omega,
+                                               const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.nn) return;
+  const int np = g.np;
+  const size_t vs = (size_t)C * np;
+  double res[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) res[c] = __ldg(b + s * vs + c * np + n);
+  if (!FIRST) {
+    const double* As = A + (size_t)s * NOFF * C * C * np + n;
+    const double* xs = xin + s * vs;
+    int i, j, k;
+    node_coords(g, n, i, j, k);
+#pragma unroll
+    for (int off = 0; off < NOFF; ++off) {
+      const int nb = neighbour(g, i, j, k, off);
+      if (nb < 0) continue;
+      double xv[C];
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) xv[cb] = __ldg(xs + cb * np + nb);
+#pragma unroll
+      for (int ca = 0; ca < C; ++ca)
+#pragma unroll
+        for (int cb = 0; cb < C; ++cb) res[ca] -= __ldg(As + ((size_t)(off * C + ca) * C + cb) * np) * xv[cb];
+    }
+  }
+  const double* Ds = Dinv + (size_t)s * C * C * np + n;
+#pragma unroll
+  for (int ca = 0; ca < C; ++ca) {
+    double z = 0.0;
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) z += __ldg(Ds + (size_t)(ca * C + cb) * np) * res[cb];
+    const double base = FIRST ? 0.0 : xin[s * vs + ca * np + n];
+    xout[s * vs + ca * np + n] = base + omega * z;
+  }
+}
+
+// ---------------------------------------------------------------- grid transfer (Q1 bilinear / trilinear)
+__device__ __forceinline__ double pweight(int fine, int coarse) {
+  const int d = fine - 2 * coarse;
+  return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0);
+}
+
+// bc[c][I] = sum_i P(i, I) rf[c][i]
+template <int D>
+__global__ void k_restrict(Grid gf, Grid gc, const double* __restrict__ rf, double* __restrict__ bc,
+                           const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= gc.nn) return;
+  int ci, cj, ck;
+  node_coords(gc, I, ci, cj, ck);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  const double* rs = rf + (size_t)s * C * gf.np;
+  for (int dk = (D == 3 ? -1 : 0); dk <= (D == 3 ? 1 : 0); ++dk)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int di = -1; di <= 1; ++di) {
+        const int fi = 2 * ci + di, fj = 2 * cj + dj, fk = 2 * ck + dk;
+        if (fi < 0 || fi >= gf.n[0] || fj < 0 || fj >= gf.n[1] || fk < 0 || fk >= gf.n[2]) continue;
+        const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
+        const int f = node_index(gf, fi, fj, fk);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += w * rs[c * gf.np + f];
+      }
+  double* bs = bc + (size_t)s * C * gc.np;
+#pragma unroll
+  for (int c = 0; c < C; ++c) bs[c * gc.np + I] = acc[c];
+}
+
+// xf[c][i] += sum_I P(i, I) ec[c][I]
+template <int D>
+__global__ void k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec, double* __restrict__ xf,
+                              const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= gf.nn) return;
+  int fi, fj, fk;
+  node_coords(gf, f, fi, fj, fk);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  const double* es = ec + (size_t)s * C * gc.np;
+  const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
+  for (int ck = k0; ck <= (D == 3 ? k0 + (fk & 1) : k0); ++ck)
+    for (int cj = j0; cj <= j0 + (fj & 1); ++cj)
+      for (int ci = i0; ci <= i0 + (fi & 1); ++ci) {
+        const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
+        const int I = node_index(gc, ci, cj, ck);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += w * es[c * gc.np + I];
+      }
+  double* xs = xf + (size_t)s * C * gf.np;
+#pragma unroll
+  for (int c = 0; c < C; ++c) xs[c * gf.np + f] += acc[c];
+}
+
+// Galerkin coarse operator Ac = P^T Af P; thread = (coarse node, coarse offset, row comp)
+template <int D>
+__global__ void k_rap(Grid gf, Grid gc, const double* __restrict__ Af, double* __restrict__ Ac,
+                      const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.z;
+  if (active && !active[s]) return;
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= gc.nn) return;
+  const int oc = blockIdx.y / C, ca = blockIdx.y % C;
+  int ci, cj, ck;
+  node_coords(gc, I, ci, cj, ck);
+  int odi, odj, odk;
+  offset_delta(oc, D, odi, odj, odk);
+  const int Ji = ci + odi, Jj = cj + odj, Jk = ck + odk;
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  const bool valid = !(Ji < 0 || Ji >= gc.n[0] || Jj < 0 || Jj >= gc.n[1] || Jk < 0 || Jk >= gc.n[2]);
+  if (valid) {
+    const double* As = Af + (size_t)s * NOFF * C * C * gf.np;
+    for (int dk = (D == 3 ? -1 : 0); dk <= (D == 3 ? 1 : 0); ++dk)
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int fi = 2 * ci + di, fj = 2 * cj + dj, fk = 2 * ck + dk;
+          if (fi < 0 || fi >= gf.n[0] || fj < 0 || fj >= gf.n[1] || fk < 0 || fk >= gf.n[2]) continue;
+          const double rw = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
+          const int f = node_index(gf, fi, fj, fk);
+          for (int off = 0; off < NOFF; ++off) {
+            int ddi, ddj, ddk;
+            offset_delta(off, D, ddi, ddj, ddk);
+            const int gi = fi + ddi, gj = fj + ddj, gk = fk + ddk;
+            if (gi < 0 || gi >= gf.n[0] || gj < 0 || gj >= gf.n[1] || gk < 0 || gk >= gf.n[2]) continue;
+            const double pw = pweight(gi, Ji) * pweight(gj, Jj) * (D == 3 ? pweight(gk, Jk) : 1.0);
+            if (pw == 0.0) continue;
+            const double w = rw * pw;
+            const double* blk = As + (((size_t)off * C + ca) * C) * gf.np + f;
+#pragma unroll
+            for (int cb = 0; cb < C; ++cb) acc[cb] += w * blk[(size_t)cb * gf.np];
+          }
+        }
+  }
+  double* Cs = Ac + (size_t)s * NOFF * C * C * gc.np;
+#pragma unroll
+  for (int cb = 0; cb < C; ++cb) Cs[(((size_t)oc * C + ca) * C + cb) * gc.np + I] = acc[cb];
+}
+
+// ---------------------------------------------------------------- dense coarsest level
+// M[s] (n x 2n, row-major) = [A | I] with dense index c*nn + node
+template <int D>
+__global__ void k_dense_build(Grid g, const double* __restrict__ A, double* __restrict__ M,
+                              const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = C * g.nn;
+  double* Ms = M + (size_t)s * n * 2 * n;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * 2 * n; idx += gridDim.x * blockDim.x)
+    Ms[idx] = 0.0;
+  __syncthreads();
+  // one thread per (row node, row comp)
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n; row += gridDim.x * blockDim.x) {
+    const int ca = row / g.nn, node = row % g.nn;
+    int i, j, k;
+    node_coords(g, node, i, j, k);
+    const double* As = A + (size_t)s * NOFF * C * C * g.np;
+    for (int off = 0; off < NOFF; ++off) {
+      const int nb = neighbour(g, i, j, k, off);
+      if (nb < 0) continue;
+      for (int cb = 0; cb < C; ++cb)
+        Ms[(size_t)row * 2 * n + cb * g.nn + nb] = As[(((size_t)off * C + ca) * C + cb) * g.np + node];
+    }
+    Ms[(size_t)row * 2 * n + n + row] = 1.0;
+  }
+}
+
+// in-place Gauss-Jordan with partial pivoting, one CTA per slice (grid.x = S)
+__global__ void k_gauss_jordan(double* __restrict__ M, int n, const int* __restrict__ active) {
+  const int s = blockIdx.x;
+  if (active && !active[s]) return;
+  double* Ms = M + (size_t)s * n * 2 * n;
+  __shared__ double sval[32];
+  __shared__ int sidx[32];
+  __shared__ int piv_sh;
+  const int w2 = 2 * n;
+  for (int p = 0; p < n; ++p) {
+    // pivot search (deterministic: largest |a|, lowest row on ties)
+    double best = -1.0;
+    int bi = p;
+    for (int r = p + threadIdx.x; r < n; r += blockDim.x) {
+      const double v = fabs(Ms[(size_t)r * w2 + p]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, best, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { sval[threadIdx.x >> 5] = best; sidx[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int ii = p;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (sval[w] > b || (sval[w] == b && sidx[w] < ii)) { b = sval[w]; ii = sidx[w]; }
+      piv_sh = ii;
+    }
+    __syncthreads();
+    const int piv = piv_sh;
+    if (piv != p)
+      for (int c = threadIdx.x; c < w2; c += blockDim.x) {
+        const double t = Ms[(size_t)p * w2 + c];
+        Ms[(size_t)p * w2 + c] = Ms[(size_t)piv * w2 + c];
+        Ms[(size_t)piv * w2 + c] = t;
+      }
+    __syncthreads();
+    const double d = Ms[(size_t)p * w2 + p];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < w2; c += blockDim.x) Ms[(size_t)p * w2 + c] *= inv;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * w2; idx += blockDim.x) {
+      const int r = idx / w2, c = idx % w2;
+      if (r == p || c == p) continue;
+      Ms[(size_t)r * w2 + c] -= Ms[(size_t)r * w2 + p] * Ms[(size_t)p * w2 + c];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      if (r != p) Ms[(size_t)r * w2 + p] = 0.0;
+    __syncthreads();
+  }
+}
+
+// x = Ainv b on the coarsest level (grid.x = S)
+template <int D>
+__global__ void k_dense_apply(Grid g, const double* __restrict__ M, const double* __restrict__ b,
+                              double* __restrict__ x, const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  const int s = blockIdx.x;
+  if (active && !active[s]) return;
+  const int n = C * g.nn;
+  const double* Ms = M + (size_t)s * n * 2 * n;
+  const double* bs = b + (size_t)s * C * g.np;
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < n; ++c) acc += Ms[(size_t)row * 2 * n + n + c] * bs[(c / g.nn) * g.np + (c % g.nn)];
+    x[(size_t)s * C * g.np + (row / g.nn) * g.np + (row % g.nn)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- GMRES scalar work (one thread per slice)
+// Arnoldi column j of H is in h[s][0..j+1]; applies previous Givens
+// rotations, builds rotation j, updates g and the convergence state.
+__global__ void k_gmres_givens(int j, int m, double* __restrict__ H, double* __restrict__ cs,
+                               double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
+                               int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its,
+                               double* __restrict__ resid, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (!gm_active[s]) return;
+  double* h = H + (size_t)s * (m + 1) * m + (size_t)j * (m + 1);  // column-major column j
+  double* c = cs + (size_t)s * m;
+  double* sv = sn + (size_t)s * m;
+  double* g = gv + (size_t)s * (m + 1);
+  for (int i = 0; i < j; ++i) {
+    const double t = c[i] * h[i] + sv[i] * h[i + 1];
+    h[i + 1] = -sv[i] * h[i] + c[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double a = h[j], b = h[j + 1];
+  const double r = hypot(a, b);
+  double cj = 1.0, sj = 0.0;
+  if (r != 0.0) { cj = a / r; sj = b / r; }
+  c[j] = cj;
+  sv[j] = sj;
+  h[j] = r;
+  h[j + 1] = 0.0;
+  g[j + 1] = -sj * g[j];
+  g[j] = cj * g[j];
+  gm_steps[s] = j + 1;
+  its[s] += 1;
+  const double res = fabs(g[j + 1]);
+  resid[s] = res;
+  if (res <= tol[s] || b == 0.0 || j + 1 == m) gm_active[s] = 0;
+}
+
+// back substitution H y = g for the steps taken this cycle
+__global__ void k_gmres_solve(int m, const double* __restrict__ H, const double* __restrict__ gv,
+                              const int* __restrict__ gm_steps, double* __restrict__ y, const int* __restrict__ active,
+                              int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (active && !active[s]) return;
+  const int k = gm_steps[s];
+  const double* Hs = H + (size_t)s * (m + 1) * m;
+  const double* g = gv + (size_t)s * (m + 1);
+  double* ys = y + (size_t)s * (m + 1);
+  for (int i = k - 1; i >= 0; --i) {
+    double acc = g[i];
+    for (int c = i + 1; c < k; ++c) acc -= Hs[(size_t)c * (m + 1) + i] * ys[c];
+    const double d = Hs[(size_t)i * (m + 1) + i];
+    ys[i] = d != 0.0 ? acc / d : 0.0;
+  }
+  for (int i = k; i <= m; ++i) ys[i] = 0.0;
+}
+
+}  // namespace pint
+
+namespace pint {
+
+// hcol[s][i] += add[s][i], i < nv
+__global__ void k_add_cols(double* __restrict__ hcol, int hstride, const double* __restrict__ add, int astride, int nv,
+                           int S, const int* __restrict__ active) {
+  const int s = blockIdx.x;
+  if (s >= S || (active && !active[s])) return;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[(size_t)s * hstride + i] += add[(size_t)s * astride + i];
+}
+
+// hcol[s][row] = sqrt(sum_b partial[s][b])
+__global__ void k_norm_to_h(const double* __restrict__ partial, int nblk, double* __restrict__ hcol, int hstride,
+                            int row, int S, const int* __restrict__ active) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || (active && !active[s])) return;
+  double acc = 0.0;
+  for (int b = 0; b < nblk; ++b) acc += partial[(size_t)s * nblk + b];
+  hcol[(size_t)s * hstride + row] = sqrt(acc);
+}
+
+// vout = w / hcol[s][row]  (0 when the norm vanished: lucky breakdown)
+__global__ void k_scale_col(double* __restrict__ vout, const double* __restrict__ w, const double* __restrict__ hcol,
+                            int hstride, int row, size_t per_slice, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double h = hcol[(size_t)s * hstride + row];
+  const double inv = h != 0.0 ? 1.0 / h : 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    vout[s * per_slice + i] = w[s * per_slice + i] * inv;
+}
+
+// x += z
+__global__ void k_axpy_one(double* __restrict__ x, const double* __restrict__ z, size_t per_slice,
+                           const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    x[s * per_slice + i] += z[s * per_slice + i];
+}
+
+}  // namespace pint

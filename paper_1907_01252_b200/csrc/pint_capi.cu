@@ -1,0 +1,934 @@
+// Host runtime of the batched fine propagator: context (mesh tables, multigrid
+// hierarchy, Krylov / Newton workspace), the Newton + GMRES + V-cycle control
+// flow, and the C ABI declared in include/pint_b200.h.
+//
+// Control flow mirrors the reference hot path (SURVEY.md §3 stack A):
+//   ThetaPropagator.advance (integrators.py:144-166)   -> pint_propagate
+//   _theta_step (integrators.py:70-96)                  -> Impl::newton_step
+//   newton_solve (linalg.py:167-248)                    -> Impl::newton_step
+//   _fd_jacobian + np.linalg.solve (linalg.py:152-164, 224)
+//                      -> Jacobian assembly + V-cycle-preconditioned GMRES
+// Every slice carries its own Newton / line-search / Krylov state; kernels
+// skip inactive slices, so a slice's arithmetic is independent of the batch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pint_b200.h"
+#include "kernels_assembly.cuh"
+#include "kernels_linalg.cuh"
+#include "kernels_parareal.cuh"
+
+using namespace pint;
+
+namespace {
+
+constexpr int kDenseMax = 1024;
+
+struct Level {
+  Grid g;
+  double* A = nullptr;     // [S][noff][C][C][np]
+  double* Dinv = nullptr;  // [S][C][C][np]
+  double* rhs = nullptr;
+  double* xa = nullptr;
+  double* xb = nullptr;
+  double* res = nullptr;
+  double* sol = nullptr;   // coarse-level V-cycle output (l > 0)
+};
+
+size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+struct pint_ctx {
+  pint_problem_desc desc{};
+  int D = 2, C = 5, maxS = 0, restart = 30;
+  Grid g{};
+  Phys ph{};
+  int cells[3] = {1, 1, 1};
+  std::vector<uint8_t> h_node_flags, h_cell_flags;
+  std::vector<double> h_profile;
+  uint8_t* d_node_flags = nullptr;
+  uint8_t* d_cell_flags = nullptr;
+  double* d_profile = nullptr;
+  std::vector<Level> lv;
+  bool dense = false;
+  int dense_n = 0;
+  double* d_dense = nullptr;
+  // Newton
+  double *ystate = nullptr, *ynew = nullptr, *r = nullptr, *dx = nullptr, *ytrial = nullptr, *rtrial = nullptr,
+         *b = nullptr;
+  // GMRES
+  double *V = nullptr, *H = nullptr, *gv = nullptr, *cs = nullptr, *sn = nullptr, *ybuf = nullptr, *z = nullptr,
+         *w = nullptr, *u = nullptr, *gm_res = nullptr, *gm_tol = nullptr, *gm_beta = nullptr;
+  int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
+  // reductions / per-slice scalars
+  double* partial = nullptr;
+  int nblk = 0;
+  double* d_norms = nullptr;
+  int* d_degen = nullptr;
+  int* d_active = nullptr;
+  int* d_mask2 = nullptr;
+  double* d_lam = nullptr;
+  StepScalars* d_st = nullptr;
+  double* h_dbl = nullptr;  // pinned
+  int* h_int = nullptr;     // pinned
+  size_t bytes = 0;
+  std::vector<void*> allocs;
+  std::mutex mu;
+  std::string err;
+  int prec_levels = 0;  // levels set up by the last precond_setup
+  pint_krylov_opts kopt{};
+};
+
+namespace {
+
+#define PINT_CHECK(call)                                                       \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+      return PINT_CUDA_ERROR;                                                  \
+    }                                                                          \
+  } while (0)
+
+#define PINT_LAUNCHED()                                                        \
+  do {                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                       \
+    if (e_ != cudaSuccess) {                                                   \
+      ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);      \
+      return PINT_CUDA_ERROR;                                                  \
+    }                                                                          \
+  } while (0)
+
+template <typename T>
+int dalloc(pint_ctx* ctx, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + " B): " + cudaGetErrorString(e);
+    return PINT_CUDA_ERROR;
+  }
+  cudaMemset(q, 0, std::max<size_t>(count, 1) * sizeof(T));
+  ctx->allocs.push_back(q);
+  ctx->bytes += count * sizeof(T);
+  *p = static_cast<T*>(q);
+  return PINT_OK;
+}
+
+#define PINT_TRY(x)          \
+  do {                       \
+    int rc_ = (x);           \
+    if (rc_ != PINT_OK) return rc_; \
+  } while (0)
+
+Grid make_grid(int dim, const int* cells) {
+  Grid g{};
+  g.dim = dim;
+  g.n[0] = cells[0] + 1;
+  g.n[1] = cells[1] + 1;
+  g.n[2] = dim == 3 ? cells[2] + 1 : 1;
+  g.nn = g.n[0] * g.n[1] * g.n[2];
+  g.np = (int)round_up((size_t)g.nn, 32);
+  g.C = 2 * dim + 1;
+  g.noff = ipow3(dim);
+  return g;
+}
+
+double ramp_value(double t, double T) {
+  const double tt = std::min(t, T);
+  return 0.5 * (1.0 - std::cos(M_PI * tt / T));
+}
+
+StepScalars make_step(double k, double theta, double t1, double ramp_time) {
+  StepScalars s;
+  s.k = k;
+  s.kt = k * theta;
+  s.ko = k * (1.0 - theta);
+  s.ramp = ramp_value(t1, ramp_time);
+  return s;
+}
+
+inline dim3 node_grid(int nn, int S, int bs = 128) { return dim3((nn + bs - 1) / bs, S); }
+inline dim3 vec_grid(size_t n, int S) {
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  return dim3((unsigned)blocks, S);
+}
+
+// ---------------------------------------------------------------- mesh tables (host)
+void build_tables(pint_ctx* ctx) {
+  const auto& d = ctx->desc;
+  const int D = ctx->D;
+  const Grid& g = ctx->g;
+  const int ncell = ctx->cells[0] * ctx->cells[1] * ctx->cells[2];
+  ctx->h_cell_flags.assign(ncell, 0);
+  ctx->h_node_flags.assign(g.nn, 0);
+  ctx->h_profile.assign(g.nn, 0.0);
+  double h[3];
+  for (int m = 0; m < 3; ++m) h[m] = m < D ? d.extent[m] / d.cells[m] : 1.0;
+  for (int ck = 0; ck < ctx->cells[2]; ++ck)
+    for (int cj = 0; cj < ctx->cells[1]; ++cj)
+      for (int ci = 0; ci < ctx->cells[0]; ++ci) {
+        const int idx[3] = {ci, cj, ck};
+        bool solid = true;
+        for (int m = 0; m < D; ++m) {
+          const double c = (idx[m] + 0.5) * h[m];
+          solid = solid && (c >= d.bar_lo[m]) && (c <= d.bar_hi[m]);
+        }
+        uint8_t f = solid ? kCellSolid : 0;
+        if (!solid && ci == ctx->cells[0] - 1) f |= kCellOutflow;
+        const int cell = (ck * ctx->cells[1] + cj) * ctx->cells[0] + ci;
+        ctx->h_cell_flags[cell] = f;
+        for (int a = 0; a < (1 << D); ++a) {
+          const int n = node_index(g, ci + (a & 1), cj + ((a >> 1) & 1), D == 3 ? ck + ((a >> 2) & 1) : 0);
+          ctx->h_node_flags[n] |= solid ? kSolidTouch : kFluidTouch;
+        }
+      }
+  for (int n = 0; n < g.nn; ++n) {
+    int i, j, k;
+    node_coords(g, n, i, j, k);
+    const int idx[3] = {i, j, k};
+    bool wall = false;
+    for (int m = 1; m < D; ++m) wall = wall || idx[m] == 0 || idx[m] == d.cells[m];
+    const bool in_lo = i == 0, out_hi = i == d.cells[0];
+    uint8_t f = ctx->h_node_flags[n];
+    if (in_lo || wall) f |= kDirV;
+    if (in_lo || out_hi || wall) f |= kDirU;
+    ctx->h_node_flags[n] = f;
+    double prof = d.u_peak;
+    for (int m = 1; m < D; ++m) {
+      const double y = idx[m] * h[m];
+      const double H = d.extent[m];
+      prof = prof * 4.0 * y * (H - y) / (H * H);
+    }
+    ctx->h_profile[n] = (in_lo && !wall) ? prof : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- dimension-specific implementation
+template <int D>
+struct Impl {
+  static constexpr int C = 2 * D + 1;
+
+  static MeshDev mesh(pint_ctx* ctx) {
+    MeshDev m;
+    m.g = ctx->g;
+    m.cells[0] = ctx->cells[0];
+    m.cells[1] = ctx->cells[1];
+    m.cells[2] = ctx->cells[2];
+    m.cell_flags = ctx->d_cell_flags;
+    m.node_flags = ctx->d_node_flags;
+    m.profile = ctx->d_profile;
+    return m;
+  }
+
+  static int colour_count(pint_ctx* ctx, int colour) {
+    int n = 1;
+    for (int m = 0; m < D; ++m) n *= (ctx->cells[m] - ((colour >> m) & 1) + 1) >> 1;
+    return n;
+  }
+
+  static size_t vs(pint_ctx* ctx) { return (size_t)C * ctx->g.np; }
+
+  // ---- residual r = R(y; yo); norms into ctx->d_norms (and host if h != nullptr)
+  static int residual(pint_ctx* ctx, int S, const double* y, const double* yo, double* r, const int* mask,
+                      double* h_norms, cudaStream_t st) {
+    MeshDev m = mesh(ctx);
+    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, st>>>(r, vs(ctx), mask);
+    cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
+    for (int c = 0; c < (1 << D); ++c) {
+      const int ne = colour_count(ctx, c);
+      if (ne == 0) continue;
+      k_residual_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
+                                                                      mask, c);
+    }
+    k_fix_residual<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, ctx->d_st, y, r, mask);
+    PINT_LAUNCHED();
+    return norms(ctx, S, r, r, mask, true, ctx->d_degen, h_norms, st);
+  }
+
+  static int norms(pint_ctx* ctx, int S, const double* x, const double* y, const int* mask, bool take_sqrt,
+                   const int* degen, double* h_out, cudaStream_t st) {
+    const int nblk = ctx->nblk;
+    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(x, y, vs(ctx), ctx->partial, nblk, mask);
+    k_dot_final<<<(S + 127) / 128, 128, 0, st>>>(ctx->partial, nblk, ctx->d_norms, S, take_sqrt ? 1 : 0, degen,
+                                                mask);
+    PINT_LAUNCHED();
+    if (h_out) {
+      PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+      PINT_CHECK(cudaStreamSynchronize(st));
+      std::memcpy(h_out, ctx->h_dbl, sizeof(double) * S);
+    }
+    return PINT_OK;
+  }
+
+  // ---- Jacobian assembly into level 0
+  static int assemble(pint_ctx* ctx, int S, const double* y, const double* yo, const int* mask, cudaStream_t st) {
+    MeshDev m = mesh(ctx);
+    Level& L0 = ctx->lv[0];
+    const size_t ms = (size_t)ctx->g.noff * C * C * ctx->g.np;
+    k_zero_active<<<vec_grid(ms, S), 256, 0, st>>>(L0.A, ms, mask);
+    constexpr int A = 1 << D;
+    for (int c = 0; c < A; ++c) {
+      const int ne = colour_count(ctx, c);
+      if (ne == 0) continue;
+      k_jacobian_colour<D><<<dim3((ne + 63) / 64, A * C, S), 64, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
+                                                                         c);
+    }
+    k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, L0.A, mask);
+    PINT_LAUNCHED();
+    return PINT_OK;
+  }
+
+  static int jvp(pint_ctx* ctx, int S, const double* y, const double* yo, const double* w, double* out,
+                 cudaStream_t st) {
+    MeshDev m = mesh(ctx);
+    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, st>>>(out, vs(ctx), nullptr);
+    for (int c = 0; c < (1 << D); ++c) {
+      const int ne = colour_count(ctx, c);
+      if (ne == 0) continue;
+      k_jvp_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
+    }
+    k_fix_jvp<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, w, out, nullptr);
+    PINT_LAUNCHED();
+    return PINT_OK;
+  }
+
+  static void spmv(pint_ctx* ctx, int lvl, int S, const double* x, double* y, const int* mask, cudaStream_t st) {
+    Level& L = ctx->lv[lvl];
+    k_spmv<D, false><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, x, nullptr, y, mask);
+  }
+
+  // ---- multigrid setup: RAP on all levels, block inverses, dense coarsest
+  static int precond_setup(pint_ctx* ctx, int S, const pint_krylov_opts* ko, const int* mask, cudaStream_t st) {
+    int nl = (int)ctx->lv.size();
+    if (ko->max_levels > 0) nl = std::min(nl, (int)ko->max_levels);
+    ctx->prec_levels = nl;
+    ctx->kopt = *ko;
+    for (int l = 0; l < nl; ++l) {
+      Level& L = ctx->lv[l];
+      if (l > 0) {
+        Level& F = ctx->lv[l - 1];
+        k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, st>>>(F.g, L.g, F.A, L.A, mask);
+      }
+      k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, mask);
+    }
+    if (ctx->dense && nl == (int)ctx->lv.size()) {
+      Level& L = ctx->lv[nl - 1];
+      k_dense_build<D><<<dim3(1, S), 512, 0, st>>>(L.g, L.A, ctx->d_dense, mask);
+      k_gauss_jordan<<<S, 512, 0, st>>>(ctx->d_dense, ctx->dense_n, mask);
+    }
+    PINT_LAUNCHED();
+    return PINT_OK;
+  }
+
+  static void smooth(pint_ctx* ctx, const Level& L, int S, const double* b, const double* xin, double* xout,
+                     const int* mask, cudaStream_t st, bool first) {
+    const double om = ctx->kopt.omega;
+    if (first)
+      k_smooth<D, true><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, b, nullptr, xout, om, mask);
+    else
+      k_smooth<D, false><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, b, xin, xout, om, mask);
+  }
+
+  // x = V-cycle(b) on level l; b and x must not alias level scratch of l
+  static void vcycle(pint_ctx* ctx, int l, int S, const double* b, double* x, const int* mask, cudaStream_t st) {
+    Level& L = ctx->lv[l];
+    const int nl = ctx->prec_levels;
+    const pint_krylov_opts& ko = ctx->kopt;
+    if (l == nl - 1) {
+      if (ctx->dense && nl == (int)ctx->lv.size()) {
+        k_dense_apply<D><<<S, 256, 0, st>>>(L.g, ctx->d_dense, b, x, mask);
+      } else {
+        const int sweeps = std::max(1, (int)ko.coarse_sweeps);
+        double* cur = L.xa;
+        double* nxt = L.xb;
+        smooth(ctx, L, S, b, nullptr, sweeps == 1 ? x : cur, mask, st, true);
+        for (int i = 1; i < sweeps; ++i) {
+          double* out = (i == sweeps - 1) ? x : nxt;
+          smooth(ctx, L, S, b, cur, out, mask, st, false);
+          std::swap(cur, nxt);
+        }
+      }
+      return;
+    }
+    Level& Lc = ctx->lv[l + 1];
+    const int pre = std::max(1, (int)ko.pre_smooth);
+    const int post = std::max(1, (int)ko.post_smooth);
+    double* cur = L.xa;
+    double* nxt = L.xb;
+    smooth(ctx, L, S, b, nullptr, cur, mask, st, true);
+    for (int i = 1; i < pre; ++i) {
+      smooth(ctx, L, S, b, cur, nxt, mask, st, false);
+      std::swap(cur, nxt);
+    }
+    k_spmv<D, true><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, cur, b, L.res, mask);
+    k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, st>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
+    double* xc = Lc.sol;
+    vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
+    k_prolong_add<D><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, Lc.g, xc, cur, mask);
+    for (int i = 0; i < post; ++i) {
+      double* out = (i == post - 1) ? x : nxt;
+      smooth(ctx, L, S, b, cur, out, mask, st, false);
+      std::swap(cur, nxt);
+    }
+  }
+
+  // ---- GMRES(m), right preconditioned:  J x = b  for slices in mask
+  static int gmres(pint_ctx* ctx, int S, const double* b, double* x, const int* mask, const pint_krylov_opts* ko,
+                   int* h_its, double* h_res, cudaStream_t st) {
+    const int m = ctx->restart;
+    const size_t n = vs(ctx);
+    const size_t vstride = (size_t)ctx->maxS * n;
+    const int nblk = ctx->nblk;
+    std::vector<int> host_mask(S, 1);
+    if (mask) {
+      PINT_CHECK(cudaMemcpyAsync(ctx->h_int, mask, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+      PINT_CHECK(cudaStreamSynchronize(st));
+      for (int s = 0; s < S; ++s) host_mask[s] = ctx->h_int[s];
+    }
+    // x = 0, r = b, beta = ||b||, tol = max(rtol beta0, atol)
+    k_zero_active<<<vec_grid(n, S), 256, 0, st>>>(x, n, mask);
+    PINT_TRY(norms(ctx, S, b, b, mask, true, nullptr, nullptr, st));
+    std::vector<double> beta(S, 0.0), tol(S, 0.0);
+    PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+    PINT_CHECK(cudaStreamSynchronize(st));
+    for (int s = 0; s < S; ++s) {
+      beta[s] = ctx->h_dbl[s];
+      tol[s] = std::max(ko->rtol * beta[s], ko->atol);
+    }
+    PINT_CHECK(cudaMemcpyAsync(ctx->gm_tol, tol.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    std::vector<int> its(S, 0);
+    std::vector<double> res(beta);
+    const double* rvec = b;  // residual of the current cycle start
+    PINT_CHECK(cudaMemsetAsync(ctx->gm_its, 0, sizeof(int) * S, st));
+    for (int cycle = 0;; ++cycle) {
+      // slices that run this cycle
+      std::vector<int> cyc(S, 0);
+      int ncyc = 0;
+      for (int s = 0; s < S; ++s) {
+        cyc[s] = host_mask[s] && res[s] > tol[s] && its[s] < ko->max_iters && std::isfinite(res[s]);
+        ncyc += cyc[s];
+      }
+      if (ncyc == 0) break;
+      PINT_CHECK(cudaMemcpyAsync(ctx->cyc_active, cyc.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->gm_active, cyc.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+      PINT_CHECK(cudaMemsetAsync(ctx->gm_steps, 0, sizeof(int) * S, st));
+      // v0 = r / beta ; g = (beta, 0, ...)
+      std::vector<double> g0((size_t)S * (m + 1), 0.0);
+      for (int s = 0; s < S; ++s) g0[(size_t)s * (m + 1)] = res[s];
+      PINT_CHECK(cudaMemcpyAsync(ctx->gv, g0.data(), sizeof(double) * g0.size(), cudaMemcpyHostToDevice, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->gm_beta, res.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+      k_scale_inv<<<vec_grid(n, S), 256, 0, st>>>(ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
+      int remaining_cap = m;
+      for (int s = 0; s < S; ++s)
+        if (cyc[s]) remaining_cap = std::min(remaining_cap, std::max(1, ko->max_iters - its[s]));
+      for (int j = 0; j < m; ++j) {
+        double* vj = ctx->V + j * vstride;
+        double* vj1 = ctx->V + (j + 1) * vstride;
+        // z = M^{-1} v_j ; w = J z
+        vcycle(ctx, 0, S, vj, ctx->z, ctx->gm_active, st);
+        spmv(ctx, 0, S, ctx->z, ctx->w, ctx->gm_active, st);
+        // CGS2 against v_0..v_j
+        double* hcol = ctx->H + (size_t)j * (m + 1);
+        const int hstride = (m + 1) * m;
+        for (int pass = 0; pass < 2; ++pass) {
+          k_mdot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
+                                                               m + 1, ctx->gm_active);
+          k_mdot_final<<<S, 32, 0, st>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
+                                         pass == 0 ? hstride : (m + 1), 0, S, ctx->gm_active);
+          k_mupdate<<<vec_grid(n, S), 256, 0, st>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
+                                                    pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
+          if (pass == 1) {
+            // h += h2
+            k_add_cols<<<S, 32, 0, st>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
+          }
+        }
+        // h_{j+1,j} = ||w|| ; v_{j+1} = w / h_{j+1,j}
+        k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
+        k_norm_to_h<<<(S + 127) / 128, 128, 0, st>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
+        k_scale_col<<<vec_grid(n, S), 256, 0, st>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
+        k_gmres_givens<<<(S + 127) / 128, 128, 0, st>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
+                                                       ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, S);
+        PINT_LAUNCHED();
+        if (j + 1 >= remaining_cap) break;
+        // poll: any slice still iterating?
+        if ((j & 3) == 3 || j + 1 == m) {
+          PINT_CHECK(cudaMemcpyAsync(ctx->h_int, ctx->gm_active, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+          PINT_CHECK(cudaStreamSynchronize(st));
+          bool any = false;
+          for (int s = 0; s < S; ++s) any = any || ctx->h_int[s];
+          if (!any) break;
+        }
+      }
+      // x += M^{-1} (V y)
+      k_gmres_solve<<<(S + 127) / 128, 128, 0, st>>>(m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
+                                                    S);
+      k_mcombine<<<vec_grid(n, S), 256, 0, st>>>(ctx->u, ctx->V, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
+                                                 ctx->cyc_active);
+      vcycle(ctx, 0, S, ctx->u, ctx->z, ctx->cyc_active, st);
+      k_axpy_one<<<vec_grid(n, S), 256, 0, st>>>(x, ctx->z, n, ctx->cyc_active);
+      // true residual r = b - J x into ctx->u (reused as cycle start)
+      k_spmv<D, true><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+      rvec = ctx->u;
+      PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->h_int, ctx->gm_its, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+      PINT_CHECK(cudaStreamSynchronize(st));
+      for (int s = 0; s < S; ++s)
+        if (cyc[s]) {
+          res[s] = ctx->h_dbl[s];
+          its[s] = ctx->h_int[s];
+        }
+    }
+    for (int s = 0; s < S; ++s) {
+      if (h_its) h_its[s] = its[s];
+      if (h_res) h_res[s] = res[s];
+    }
+    return PINT_OK;
+  }
+
+  // ---- one shifted-CN step for the slices in `act` (host), Newton per slice
+  //      (control flow of linalg.py:207-248)
+  static int newton_step(pint_ctx* ctx, int S, const double* yo, double* y, const std::vector<int>& act,
+                         const pint_newton_opts* no, const pint_krylov_opts* ko, std::vector<int>& nit,
+                         std::vector<int>& kit, std::vector<int>& status, cudaStream_t st) {
+    const size_t n = vs(ctx);
+    std::vector<double> rnorm(S), target(S), tnorm(S), lam(S, 1.0);
+    std::vector<int> running(S, 0), its(S, 0), ls(S, 0), accept(S, 0);
+    PINT_CHECK(cudaMemcpyAsync(ctx->d_active, act.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+    k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(y, yo, n, ctx->d_active);  // Newton guess = previous state
+    PINT_TRY(residual(ctx, S, y, yo, ctx->r, ctx->d_active, rnorm.data(), st));
+    for (int s = 0; s < S; ++s) {
+      if (!act[s]) continue;
+      if (!std::isfinite(rnorm[s])) { status[s] = PINT_NUMERIC_BREAKDOWN; continue; }
+      target[s] = no->abs_tol + no->rel_tol * rnorm[s];
+      running[s] = rnorm[s] > target[s];
+    }
+    std::vector<int> klin(S, 0);
+    std::vector<double> kres(S, 0.0);
+    for (int it = 0; it < no->max_iters; ++it) {
+      int nrun = 0;
+      for (int s = 0; s < S; ++s) nrun += running[s];
+      if (nrun == 0) break;
+      PINT_CHECK(cudaMemcpyAsync(ctx->d_active, running.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+      PINT_TRY(assemble(ctx, S, y, yo, ctx->d_active, st));
+      PINT_TRY(precond_setup(ctx, S, ko, ctx->d_active, st));
+      k_negate<<<vec_grid(n, S), 256, 0, st>>>(ctx->b, ctx->r, n, ctx->d_active);
+      PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, klin.data(), kres.data(), st));
+      for (int s = 0; s < S; ++s)
+        if (running[s]) kit[s] += klin[s];
+      // line search: lambda = 1, halve until decrease or damping_min (accept anyway)
+      for (int s = 0; s < S; ++s) { lam[s] = 1.0; ls[s] = running[s]; }
+      for (;;) {
+        int nls = 0;
+        for (int s = 0; s < S; ++s) nls += ls[s];
+        if (nls == 0) break;
+        PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ls.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+        PINT_CHECK(cudaMemcpyAsync(ctx->d_lam, lam.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+        k_trial<<<vec_grid(n, S), 256, 0, st>>>(ctx->ytrial, y, ctx->dx, ctx->d_lam, n, ctx->d_mask2);
+        std::vector<double> tn(S, 0.0);
+        PINT_TRY(residual(ctx, S, ctx->ytrial, yo, ctx->rtrial, ctx->d_mask2, tn.data(), st));
+        for (int s = 0; s < S; ++s) {
+          if (!ls[s]) continue;
+          tnorm[s] = std::isfinite(tn[s]) ? tn[s] : INFINITY;
+          if (tnorm[s] < rnorm[s] || lam[s] <= no->damping_min) ls[s] = 0;
+          else lam[s] = std::max(lam[s] / 2.0, no->damping_min);
+        }
+      }
+      for (int s = 0; s < S; ++s) {
+        accept[s] = 0;
+        if (!running[s]) continue;
+        if (!std::isfinite(tnorm[s])) {
+          status[s] = PINT_NUMERIC_BREAKDOWN;
+          running[s] = 0;
+          continue;
+        }
+        accept[s] = 1;
+      }
+      PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, accept.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(y, ctx->ytrial, n, ctx->d_mask2);
+      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(ctx->r, ctx->rtrial, n, ctx->d_mask2);
+      PINT_LAUNCHED();
+      for (int s = 0; s < S; ++s) {
+        if (!accept[s]) continue;
+        rnorm[s] = tnorm[s];
+        its[s] += 1;
+        running[s] = rnorm[s] > target[s];
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      if (!act[s] || status[s] != PINT_OK) continue;
+      nit[s] += its[s];
+      if (rnorm[s] > target[s]) status[s] = PINT_NEWTON_MAX_ITERS;
+    }
+    return PINT_OK;
+  }
+
+  static int propagate(pint_ctx* ctx, int S, const double* y_in, double* y_out, const double* t0,
+                       const double* t_end, const int* nsteps, double k, double theta0, const pint_newton_opts* no,
+                       const pint_krylov_opts* ko, int* newton_iters, int* krylov_iters, int* status_out,
+                       double* fail_t, cudaStream_t st) {
+    const size_t n = vs(ctx);
+    PINT_CHECK(cudaMemcpyAsync(ctx->ystate, y_in, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
+    std::vector<double> t(t0, t0 + S);
+    std::vector<int> nit(S, 0), kit(S, 0), status(S, PINT_OK);
+    std::vector<double> ft(S, 0.0);
+    int nmax = 0;
+    for (int s = 0; s < S; ++s) nmax = std::max(nmax, nsteps[s]);
+    std::vector<StepScalars> sts(S);
+    for (int j = 0; j < nmax; ++j) {
+      std::vector<int> act(S, 0);
+      std::vector<double> t1(S, 0.0);
+      for (int s = 0; s < S; ++s) {
+        if (j >= nsteps[s] || status[s] != PINT_OK) continue;
+        const double kk = (j == nsteps[s] - 1) ? (t_end[s] - t[s]) : k;
+        const double theta = std::min(std::max(0.5 + theta0 * kk, 0.5), 1.0);
+        t1[s] = t[s] + kk;
+        sts[s] = make_step(kk, theta, t1[s], ctx->desc.ramp_time);
+        act[s] = 1;
+      }
+      PINT_CHECK(cudaMemcpyAsync(ctx->d_st, sts.data(), sizeof(StepScalars) * S, cudaMemcpyHostToDevice, st));
+      PINT_TRY(newton_step(ctx, S, ctx->ystate, ctx->ynew, act, no, ko, nit, kit, status, st));
+      std::vector<int> ok(S, 0);
+      for (int s = 0; s < S; ++s) {
+        if (!act[s]) continue;
+        if (status[s] != PINT_OK) { ft[s] = t1[s]; continue; }
+        ok[s] = 1;
+        t[s] = t1[s];
+      }
+      PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ok.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(ctx->ystate, ctx->ynew, n, ctx->d_mask2);
+      PINT_LAUNCHED();
+    }
+    PINT_CHECK(cudaMemcpyAsync(y_out, ctx->ystate, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
+    PINT_CHECK(cudaStreamSynchronize(st));
+    for (int s = 0; s < S; ++s) {
+      if (newton_iters) newton_iters[s] = nit[s];
+      if (krylov_iters) krylov_iters[s] = kit[s];
+      if (status_out) status_out[s] = status[s];
+      if (fail_t) fail_t[s] = ft[s];
+    }
+    return PINT_OK;
+  }
+};
+
+int upload_steps(pint_ctx* ctx, int S, const double* k, const double* theta, const double* t1, cudaStream_t st) {
+  std::vector<StepScalars> sts(S);
+  for (int s = 0; s < S; ++s) sts[s] = make_step(k[s], theta[s], t1[s], ctx->desc.ramp_time);
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_st, sts.data(), sizeof(StepScalars) * S, cudaMemcpyHostToDevice, st));
+  return PINT_OK;
+}
+
+int check_S(pint_ctx* ctx, int S) {
+  if (!ctx) return PINT_INVALID_ARG;
+  if (S < 1 || S > ctx->maxS) {
+    ctx->err = "batch size " + std::to_string(S) + " outside [1, " + std::to_string(ctx->maxS) + "]";
+    return PINT_INVALID_ARG;
+  }
+  return PINT_OK;
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+
+extern "C" {
+
+int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out) {
+  if (!desc || !out || max_slices < 1 || restart < 1) return PINT_INVALID_ARG;
+  if (desc->dim != 2 && desc->dim != 3) return PINT_INVALID_ARG;
+  for (int m = 0; m < desc->dim; ++m)
+    if (desc->cells[m] < 1) return PINT_INVALID_ARG;
+  pint_ctx* ctx = new pint_ctx();
+  *out = ctx;
+  ctx->desc = *desc;
+  ctx->D = desc->dim;
+  ctx->C = 2 * desc->dim + 1;
+  ctx->maxS = max_slices;
+  ctx->restart = restart;
+  ctx->cells[0] = desc->cells[0];
+  ctx->cells[1] = desc->cells[1];
+  ctx->cells[2] = desc->dim == 3 ? desc->cells[2] : 1;
+  ctx->g = make_grid(ctx->D, ctx->cells);
+  Phys& ph = ctx->ph;
+  ph.rho_f = desc->rho_f;
+  ph.rnu = desc->rho_f * desc->nu_f;
+  ph.rho_s = desc->rho_s;
+  ph.mu = desc->mu_s;
+  ph.lam = desc->lambda_s;
+  ph.delta = desc->delta_p;
+  double wq = 1.0, wf = 1.0;
+  for (int m = 0; m < 3; ++m) {
+    ph.h[m] = m < ctx->D ? desc->extent[m] / desc->cells[m] : 1.0;
+    if (m < ctx->D) wq *= 0.5 * ph.h[m];
+    if (m >= 1 && m < ctx->D) wf *= 0.5 * ph.h[m];
+  }
+  ph.wq = wq;
+  ph.wf = wf;
+  build_tables(ctx);
+
+  const int C = ctx->C;
+  const int S = max_slices;
+  const size_t vsz = (size_t)C * ctx->g.np;
+  int rc;
+#define ALLOC(p, cnt)                   \
+  if ((rc = dalloc(ctx, &(p), (cnt))) != PINT_OK) return rc;
+  ALLOC(ctx->d_node_flags, (size_t)ctx->g.nn);
+  ALLOC(ctx->d_cell_flags, ctx->h_cell_flags.size());
+  ALLOC(ctx->d_profile, (size_t)ctx->g.nn);
+  cudaMemcpy(ctx->d_node_flags, ctx->h_node_flags.data(), ctx->h_node_flags.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_cell_flags, ctx->h_cell_flags.data(), ctx->h_cell_flags.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_profile, ctx->h_profile.data(), sizeof(double) * ctx->h_profile.size(), cudaMemcpyHostToDevice);
+
+  // multigrid hierarchy: coarsen while every cell count is even
+  int cl[3] = {ctx->cells[0], ctx->cells[1], ctx->cells[2]};
+  for (;;) {
+    Level L;
+    L.g = make_grid(ctx->D, cl);
+    ctx->lv.push_back(L);
+    bool even = true;
+    for (int m = 0; m < ctx->D; ++m) even = even && (cl[m] % 2 == 0) && cl[m] >= 2;
+    if (!even) break;
+    for (int m = 0; m < ctx->D; ++m) cl[m] /= 2;
+  }
+  for (size_t l = 0; l < ctx->lv.size(); ++l) {
+    Level& L = ctx->lv[l];
+    const size_t np = L.g.np;
+    ALLOC(L.A, (size_t)S * L.g.noff * C * C * np);
+    ALLOC(L.Dinv, (size_t)S * C * C * np);
+    ALLOC(L.xa, (size_t)S * C * np);
+    ALLOC(L.xb, (size_t)S * C * np);
+    ALLOC(L.res, (size_t)S * C * np);
+    if (l > 0) ALLOC(L.rhs, (size_t)S * C * np);
+    if (l > 0) ALLOC(L.sol, (size_t)S * C * np);
+  }
+  const Level& Lc = ctx->lv.back();
+  ctx->dense_n = C * Lc.g.nn;
+  ctx->dense = ctx->dense_n <= kDenseMax;
+  if (ctx->dense) ALLOC(ctx->d_dense, (size_t)S * ctx->dense_n * 2 * ctx->dense_n);
+
+  ALLOC(ctx->ystate, S * vsz);
+  ALLOC(ctx->ynew, S * vsz);
+  ALLOC(ctx->r, S * vsz);
+  ALLOC(ctx->dx, S * vsz);
+  ALLOC(ctx->ytrial, S * vsz);
+  ALLOC(ctx->rtrial, S * vsz);
+  ALLOC(ctx->b, S * vsz);
+  const int m = restart;
+  ALLOC(ctx->V, (size_t)(m + 1) * S * vsz);
+  ALLOC(ctx->z, S * vsz);
+  ALLOC(ctx->w, S * vsz);
+  ALLOC(ctx->u, S * vsz);
+  ALLOC(ctx->H, (size_t)S * (m + 1) * m);
+  ALLOC(ctx->gv, (size_t)S * (m + 1));
+  ALLOC(ctx->cs, (size_t)S * m);
+  ALLOC(ctx->sn, (size_t)S * m);
+  ALLOC(ctx->ybuf, (size_t)S * (m + 1));
+  ALLOC(ctx->gm_res, (size_t)S);
+  ALLOC(ctx->gm_tol, (size_t)S);
+  ALLOC(ctx->gm_beta, (size_t)S);
+  ALLOC(ctx->gm_active, (size_t)S);
+  ALLOC(ctx->gm_steps, (size_t)S);
+  ALLOC(ctx->gm_its, (size_t)S);
+  ALLOC(ctx->cyc_active, (size_t)S);
+  ctx->nblk = (int)((vsz + kRedChunk - 1) / kRedChunk);
+  ALLOC(ctx->partial, (size_t)S * (m + 1) * ctx->nblk);
+  ALLOC(ctx->d_norms, (size_t)S);
+  ALLOC(ctx->d_degen, (size_t)S);
+  ALLOC(ctx->d_active, (size_t)S);
+  ALLOC(ctx->d_mask2, (size_t)S);
+  ALLOC(ctx->d_lam, (size_t)S);
+  ALLOC(ctx->d_st, (size_t)S);
+#undef ALLOC
+  if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess) {
+    ctx->err = "cudaMallocHost failed";
+    return PINT_CUDA_ERROR;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    ctx->err = std::string("create: ") + cudaGetErrorString(e);
+    return PINT_CUDA_ERROR;
+  }
+  return PINT_OK;
+}
+
+int pint_destroy(pint_ctx* ctx) {
+  if (!ctx) return PINT_OK;
+  cudaDeviceSynchronize();
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->h_dbl) cudaFreeHost(ctx->h_dbl);
+  if (ctx->h_int) cudaFreeHost(ctx->h_int);
+  delete ctx;
+  return PINT_OK;
+}
+
+const char* pint_last_error(const pint_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int pint_sizes(const pint_ctx* ctx, int32_t* nn, int32_t* np, int32_t* C, int32_t* levels) {
+  if (!ctx) return PINT_INVALID_ARG;
+  if (nn) *nn = ctx->g.nn;
+  if (np) *np = ctx->g.np;
+  if (C) *C = ctx->C;
+  if (levels) *levels = (int32_t)ctx->lv.size();
+  return PINT_OK;
+}
+
+int pint_flags(const pint_ctx* ctx, uint8_t* node_flags, uint8_t* cell_flags) {
+  if (!ctx) return PINT_INVALID_ARG;
+  if (node_flags) std::memcpy(node_flags, ctx->h_node_flags.data(), ctx->h_node_flags.size());
+  if (cell_flags) std::memcpy(cell_flags, ctx->h_cell_flags.data(), ctx->h_cell_flags.size());
+  return PINT_OK;
+}
+
+#define DISPATCH(call) (ctx->D == 2 ? Impl<2>::call : Impl<3>::call)
+
+int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, const double* t0,
+                   const double* t_end, const int32_t* nsteps, double k, double theta0,
+                   const pint_newton_opts* newton, const pint_krylov_opts* krylov, int32_t* newton_iters,
+                   int32_t* krylov_iters, int32_t* status, double* fail_t, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  if (!y_in || !y_out || !t0 || !t_end || !nsteps || !newton || !krylov || k <= 0.0) {
+    ctx->err = "invalid argument to pint_propagate";
+    return PINT_INVALID_ARG;
+  }
+  if (krylov->restart > ctx->restart) {
+    ctx->err = "krylov restart exceeds the context's restart length";
+    return PINT_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  return DISPATCH(propagate(ctx, S, y_in, y_out, t0, t_end, nsteps, k, theta0, newton, krylov, newton_iters,
+                            krylov_iters, status, fail_t, st));
+}
+
+int pint_residual(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                  const double* theta, const double* t1, double* r, double* norms, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
+  std::vector<double> tmp(S);
+  rc = DISPATCH(residual(ctx, S, y, y_old, r, nullptr, tmp.data(), st));
+  if (rc == PINT_OK && norms) std::memcpy(norms, tmp.data(), sizeof(double) * S);
+  return rc;
+}
+
+int pint_jvp(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* w, const double* k,
+             const double* theta, const double* t1, double* Jw, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
+  return DISPATCH(jvp(ctx, S, y, y_old, w, Jw, st));
+}
+
+int pint_assemble(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                  const double* theta, const double* t1, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
+  return DISPATCH(assemble(ctx, S, y, y_old, nullptr, st));
+}
+
+int pint_jacobian_blocks(pint_ctx* ctx, int32_t S, double* out, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const size_t ms = (size_t)ctx->g.noff * ctx->C * ctx->C * ctx->g.np;
+  PINT_CHECK(cudaMemcpyAsync(out, ctx->lv[0].A, sizeof(double) * ms * S, cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+  return PINT_OK;
+}
+
+int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  DISPATCH(spmv(ctx, 0, S, x, y, nullptr, (cudaStream_t)stream));
+  PINT_LAUNCHED();
+  return PINT_OK;
+}
+
+int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return DISPATCH(precond_setup(ctx, S, krylov, nullptr, (cudaStream_t)stream));
+}
+
+int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (ctx->prec_levels == 0) {
+    ctx->err = "pint_precond_apply before pint_precond_setup";
+    return PINT_INVALID_ARG;
+  }
+  DISPATCH(vcycle(ctx, 0, S, b, x, nullptr, (cudaStream_t)stream));
+  PINT_LAUNCHED();
+  return PINT_OK;
+}
+
+int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, const pint_krylov_opts* krylov,
+                      int32_t* its, double* resid, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  if (krylov->restart > ctx->restart) {
+    ctx->err = "krylov restart exceeds the context's restart length";
+    return PINT_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, its, resid, (cudaStream_t)stream));
+}
+
+int pint_parareal_precorrect(int32_t S, int32_t C, int32_t nn, int32_t np, const double* f_old,
+                             const double* c_old, double* delta, void* stream) {
+  if (S < 1 || C < 1 || nn < 1 || np < nn) return PINT_INVALID_ARG;
+  const size_t total = (size_t)S * C * np;
+  size_t blocks = std::min<size_t>((total + 255) / 256, 4096);
+  k_precorrect<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(f_old, c_old, delta, total);
+  return cudaGetLastError() == cudaSuccess ? PINT_OK : PINT_CUDA_ERROR;
+}
+
+int pint_parareal_correct_one(int32_t C, int32_t nn, int32_t np, const double* c_new, const double* f_old,
+                              const double* c_old, const double* x_prev, double* x_new, int32_t variant,
+                              double clamp_lo, double clamp_hi, double* theta_out, double* corr_out,
+                              void* stream) {
+  if (C < 1 || nn < 1 || np < nn || variant < 0 || variant > 2 || clamp_lo > clamp_hi) return PINT_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblk = (nn + kRedChunk - 1) / kRedChunk;
+  double* scratch = nullptr;
+  const size_t cnt = (size_t)C * 3 * nblk + (size_t)C * 2 * nblk + 2;
+  if (cudaMallocAsync((void**)&scratch, sizeof(double) * cnt, st) != cudaSuccess) return PINT_CUDA_ERROR;
+  double* part3 = scratch;
+  double* part2 = scratch + (size_t)C * 3 * nblk;
+  double* d_theta = part2 + (size_t)C * 2 * nblk;
+  double* d_corr = d_theta + 1;
+  k_block_dots<<<dim3(nblk, C), kRedThreads, 0, st>>>(f_old, c_new, nn, np, part3, nblk);
+  k_theta<<<1, 32, 0, st>>>(part3, nblk, C, variant, clamp_lo, clamp_hi, d_theta);
+  k_update_norms<<<dim3(nblk, C), kRedThreads, 0, st>>>(c_new, f_old, c_old, x_prev, x_new, d_theta, nn, np, part2,
+                                                        nblk);
+  k_corr<<<1, 32, 0, st>>>(part2, nblk, C, d_corr);
+  double hres[2];
+  cudaMemcpyAsync(hres, d_theta, sizeof(double) * 2, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(scratch, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PINT_CUDA_ERROR;
+  if (theta_out) *theta_out = hres[0];
+  if (corr_out) *corr_out = hres[1];
+  return cudaGetLastError() == cudaSuccess ? PINT_OK : PINT_CUDA_ERROR;
+}
+
+}  // extern "C"
