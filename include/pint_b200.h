@@ -54,7 +54,8 @@ typedef struct pint_problem_desc {
   double extent[3];
   double bar_lo[3], bar_hi[3];
   double rho_f, nu_f, rho_s, mu_s, lambda_s;
-  double u_peak, ramp_time, delta_p;
+  double u_peak, ramp_time;
+  double alpha_p;       /* pressure stabilization: delta = alpha_p / (rho_f (1/k + U/h + nu_f/h^2)) */
 } pint_problem_desc;
 
 /* NewtonSettings (linalg.py:129-149) minus the FD epsilon (exact Jacobian). */
@@ -118,6 +119,15 @@ int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, voi
 /* GMRES solve J x = b with the current preconditioner; its/resid per slice (host) */
 int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, const pint_krylov_opts* krylov,
                       int32_t* its, double* resid, void* stream);
+
+/* ---- profiling (bench.py) --------------------------------------------
+ * enable != 0: count launches and bracket every level-0 smoother sweep (the
+ * dominant kernel of the fine step) with CUDA events on its stream.
+ * read: launches issued, profiled-kernel launches, active slice-launches of it,
+ * its summed event time (ms) and its algorithmic bytes per slice-launch. */
+int pint_profile(pint_ctx* ctx, int32_t enable);
+int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches, int64_t* slice_launches,
+                      double* kernel_ms, int64_t* bytes_per_slice_launch);
 
 /* ---- Parareal correction (parareal.py:154-197, 422-431) ---------------
  * K8a, batched over S slices: delta = f_old - c_old. */

@@ -249,7 +249,7 @@ def element_residual(mesh: Mesh, Yn, Yo, k: float, theta: float):
     rho_f, rho_s = P.rho_f, P.rho_s
     rnu = P.rho_f * P.nu_f
     mu, lam = P.mu_s, P.lambda_s
-    delta = P.delta_p
+    delta = P.delta_p(k)
     solid = mesh.solid
 
     def fields(Y, N, dN):

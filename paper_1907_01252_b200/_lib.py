@@ -35,7 +35,7 @@ EXPORTS = (
     "pint_create", "pint_destroy", "pint_last_error", "pint_sizes", "pint_flags",
     "pint_propagate", "pint_residual", "pint_jvp", "pint_assemble", "pint_jacobian_blocks",
     "pint_spmv", "pint_precond_setup", "pint_precond_apply", "pint_linear_solve",
-    "pint_parareal_precorrect", "pint_parareal_correct_one",
+    "pint_parareal_precorrect", "pint_parareal_correct_one", "pint_profile", "pint_profile_read",
 )
 
 
@@ -53,7 +53,7 @@ class ProblemDesc(ctypes.Structure):
         ("lambda_s", ctypes.c_double),
         ("u_peak", ctypes.c_double),
         ("ramp_time", ctypes.c_double),
-        ("delta_p", ctypes.c_double),
+        ("alpha_p", ctypes.c_double),
     ]
 
 
@@ -104,6 +104,9 @@ _SIGNATURES = {
     "pint_linear_solve": (_I, [_P, _I, _P, _P, ctypes.POINTER(KrylovOpts), _IP, _DP, _P]),
     "pint_parareal_precorrect": (_I, [_I, _I, _I, _I, _P, _P, _P, _P]),
     "pint_parareal_correct_one": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _DP, _DP, _P]),
+    "pint_profile": (_I, [_P, _I]),
+    "pint_profile_read": (_I, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                               ctypes.POINTER(ctypes.c_int64), _DP, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 _lib = None

@@ -240,7 +240,7 @@ __device__ __forceinline__ void fsi_element(const Phys& ph, const StepScalars& s
         T gdot = gpn[0] * dN[a][0];
 #pragma unroll
         for (int j = 1; j < D; ++j) gdot = gdot + gpn[j] * dN[a][j];
-        R[a][2 * D] += (W * k) * (div * N[a] + ph.delta * gdot);
+        R[a][2 * D] += (W * k) * (div * N[a] + st.delta * gdot);
         if ((ext_mask >> a) & 1) {
 #pragma unroll
           for (int i = 0; i < D; ++i) {

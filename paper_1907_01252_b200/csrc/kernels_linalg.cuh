@@ -276,11 +276,13 @@ template <int D, bool FIRST>
 __global__ void __launch_bounds__(128) k_smooth(Grid g, const double* __restrict__ A, const double* __restrict__ Dinv,
                                                const double* __restrict__ b, const double* __restrict__ xin,
                                                double* __restrict__ xout, double omega,
-                                               const int* __restrict__ active) {
+                                               const int* __restrict__ active,
+                                               unsigned long long* __restrict__ work) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.y;
   if (active && !active[s]) return;
+  if (work && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(work, 1ULL);  // profiling: active slice-launches
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= g.nn) return;
   const int np = g.np;

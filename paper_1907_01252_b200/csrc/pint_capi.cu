@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -44,6 +46,9 @@ struct Level {
 size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
 }  // namespace
+
+struct pint_ctx;
+static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st);
 
 struct pint_ctx {
   pint_problem_desc desc{};
@@ -83,10 +88,33 @@ struct pint_ctx {
   std::mutex mu;
   std::string err;
   int prec_levels = 0;  // levels set up by the last precond_setup
+  bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
+  // profiling (bench.py roofline): launch count and CUDA-event timing of the
+  // level-0 smoother sweeps, the dominant kernel of the fine step
+  long long launches = 0;
+  bool prof = false;
+  unsigned long long* d_work = nullptr;  // active-slice launches of the profiled kernel
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
   pint_krylov_opts kopt{};
 };
 
+static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st) {
+  ++ctx->launches;
+  return st;
+}
+
 namespace {
+
+cudaEvent_t next_event(pint_ctx* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
 
 #define PINT_CHECK(call)                                                       \
   do {                                                                         \
@@ -145,12 +173,24 @@ double ramp_value(double t, double T) {
   return 0.5 * (1.0 - std::cos(M_PI * tt / T));
 }
 
-StepScalars make_step(double k, double theta, double t1, double ramp_time) {
+// pressure stabilization delta_K(k); same expression order as FSIProblem.delta_p
+double delta_value(const pint_problem_desc& d, double k) {
+  double h2 = 0.0;
+  for (int m = 0; m < d.dim; ++m) {
+    const double h = d.extent[m] / d.cells[m];
+    h2 += h * h;
+  }
+  const double hk = std::sqrt(h2 / d.dim);
+  return d.alpha_p / (d.rho_f * (1.0 / k + d.u_peak / hk + d.nu_f / (hk * hk)));
+}
+
+StepScalars make_step(const pint_problem_desc& d, double k, double theta, double t1) {
   StepScalars s;
   s.k = k;
   s.kt = k * theta;
   s.ko = k * (1.0 - theta);
-  s.ramp = ramp_value(t1, ramp_time);
+  s.ramp = ramp_value(t1, d.ramp_time);
+  s.delta = delta_value(d, k);
   return s;
 }
 
@@ -240,15 +280,15 @@ struct Impl {
   static int residual(pint_ctx* ctx, int S, const double* y, const double* yo, double* r, const int* mask,
                       double* h_norms, cudaStream_t st) {
     MeshDev m = mesh(ctx);
-    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, st>>>(r, vs(ctx), mask);
+    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, counted(ctx, st)>>>(r, vs(ctx), mask);
     cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_residual_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
+      k_residual_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
                                                                       mask, c);
     }
-    k_fix_residual<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, ctx->d_st, y, r, mask);
+    k_fix_residual<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, ctx->d_st, y, r, mask);
     PINT_LAUNCHED();
     return norms(ctx, S, r, r, mask, true, ctx->d_degen, h_norms, st);
   }
@@ -256,8 +296,8 @@ struct Impl {
   static int norms(pint_ctx* ctx, int S, const double* x, const double* y, const int* mask, bool take_sqrt,
                    const int* degen, double* h_out, cudaStream_t st) {
     const int nblk = ctx->nblk;
-    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(x, y, vs(ctx), ctx->partial, nblk, mask);
-    k_dot_final<<<(S + 127) / 128, 128, 0, st>>>(ctx->partial, nblk, ctx->d_norms, S, take_sqrt ? 1 : 0, degen,
+    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(x, y, vs(ctx), ctx->partial, nblk, mask);
+    k_dot_final<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, ctx->d_norms, S, take_sqrt ? 1 : 0, degen,
                                                 mask);
     PINT_LAUNCHED();
     if (h_out) {
@@ -273,15 +313,15 @@ struct Impl {
     MeshDev m = mesh(ctx);
     Level& L0 = ctx->lv[0];
     const size_t ms = (size_t)ctx->g.noff * C * C * ctx->g.np;
-    k_zero_active<<<vec_grid(ms, S), 256, 0, st>>>(L0.A, ms, mask);
+    k_zero_active<<<vec_grid(ms, S), 256, 0, counted(ctx, st)>>>(L0.A, ms, mask);
     constexpr int A = 1 << D;
     for (int c = 0; c < A; ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_jacobian_colour<D><<<dim3((ne + 63) / 64, A * C, S), 64, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
+      k_jacobian_colour<D><<<dim3((ne + 63) / 64, A * C, S), 64, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
                                                                          c);
     }
-    k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, L0.A, mask);
+    k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, L0.A, mask);
     PINT_LAUNCHED();
     return PINT_OK;
   }
@@ -289,20 +329,20 @@ struct Impl {
   static int jvp(pint_ctx* ctx, int S, const double* y, const double* yo, const double* w, double* out,
                  cudaStream_t st) {
     MeshDev m = mesh(ctx);
-    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, st>>>(out, vs(ctx), nullptr);
+    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, counted(ctx, st)>>>(out, vs(ctx), nullptr);
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_jvp_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, st>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
+      k_jvp_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
     }
-    k_fix_jvp<D><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(m, w, out, nullptr);
+    k_fix_jvp<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, w, out, nullptr);
     PINT_LAUNCHED();
     return PINT_OK;
   }
 
   static void spmv(pint_ctx* ctx, int lvl, int S, const double* x, double* y, const int* mask, cudaStream_t st) {
     Level& L = ctx->lv[lvl];
-    k_spmv<D, false><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, x, nullptr, y, mask);
+    k_spmv<D, false><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
   }
 
   // ---- multigrid setup: RAP on all levels, block inverses, dense coarsest
@@ -315,14 +355,14 @@ struct Impl {
       Level& L = ctx->lv[l];
       if (l > 0) {
         Level& F = ctx->lv[l - 1];
-        k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, st>>>(F.g, L.g, F.A, L.A, mask);
+        k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, counted(ctx, st)>>>(F.g, L.g, F.A, L.A, mask);
       }
-      k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, mask);
+      k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, mask);
     }
     if (ctx->dense && nl == (int)ctx->lv.size()) {
       Level& L = ctx->lv[nl - 1];
-      k_dense_build<D><<<dim3(1, S), 512, 0, st>>>(L.g, L.A, ctx->d_dense, mask);
-      k_gauss_jordan<<<S, 512, 0, st>>>(ctx->d_dense, ctx->dense_n, mask);
+      k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
+      k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->dense_n, mask);
     }
     PINT_LAUNCHED();
     return PINT_OK;
@@ -331,10 +371,24 @@ struct Impl {
   static void smooth(pint_ctx* ctx, const Level& L, int S, const double* b, const double* xin, double* xout,
                      const int* mask, cudaStream_t st, bool first) {
     const double om = ctx->kopt.omega;
-    if (first)
-      k_smooth<D, true><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, b, nullptr, xout, om, mask);
-    else
-      k_smooth<D, false><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, L.Dinv, b, xin, xout, om, mask);
+    if (first) {
+      k_smooth<D, true><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, nullptr, xout, om,
+                                                                           mask, nullptr);
+      return;
+    }
+    const bool prof = ctx->prof && &L == &ctx->lv[0];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+      e0 = next_event(ctx);
+      e1 = next_event(ctx);
+      cudaEventRecord(e0, st);
+    }
+    k_smooth<D, false><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, xin, xout, om, mask,
+                                                                          prof ? ctx->d_work : nullptr);
+    if (prof) {
+      cudaEventRecord(e1, st);
+      ctx->ev_pairs.emplace_back(e0, e1);
+    }
   }
 
   // x = V-cycle(b) on level l; b and x must not alias level scratch of l
@@ -344,7 +398,7 @@ struct Impl {
     const pint_krylov_opts& ko = ctx->kopt;
     if (l == nl - 1) {
       if (ctx->dense && nl == (int)ctx->lv.size()) {
-        k_dense_apply<D><<<S, 256, 0, st>>>(L.g, ctx->d_dense, b, x, mask);
+        k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense, b, x, mask);
       } else {
         const int sweeps = std::max(1, (int)ko.coarse_sweeps);
         double* cur = L.xa;
@@ -368,11 +422,11 @@ struct Impl {
       smooth(ctx, L, S, b, cur, nxt, mask, st, false);
       std::swap(cur, nxt);
     }
-    k_spmv<D, true><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, L.A, cur, b, L.res, mask);
-    k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, st>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
+    k_spmv<D, true><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
+    k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
-    k_prolong_add<D><<<node_grid(L.g.nn, S), 128, 0, st>>>(L.g, Lc.g, xc, cur, mask);
+    k_prolong_add<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, xc, cur, mask);
     for (int i = 0; i < post; ++i) {
       double* out = (i == post - 1) ? x : nxt;
       smooth(ctx, L, S, b, cur, out, mask, st, false);
@@ -394,7 +448,7 @@ struct Impl {
       for (int s = 0; s < S; ++s) host_mask[s] = ctx->h_int[s];
     }
     // x = 0, r = b, beta = ||b||, tol = max(rtol beta0, atol)
-    k_zero_active<<<vec_grid(n, S), 256, 0, st>>>(x, n, mask);
+    k_zero_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, n, mask);
     PINT_TRY(norms(ctx, S, b, b, mask, true, nullptr, nullptr, st));
     std::vector<double> beta(S, 0.0), tol(S, 0.0);
     PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
@@ -425,7 +479,7 @@ struct Impl {
       for (int s = 0; s < S; ++s) g0[(size_t)s * (m + 1)] = res[s];
       PINT_CHECK(cudaMemcpyAsync(ctx->gv, g0.data(), sizeof(double) * g0.size(), cudaMemcpyHostToDevice, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->gm_beta, res.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
-      k_scale_inv<<<vec_grid(n, S), 256, 0, st>>>(ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
+      k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
       int remaining_cap = m;
       for (int s = 0; s < S; ++s)
         if (cyc[s]) remaining_cap = std::min(remaining_cap, std::max(1, ko->max_iters - its[s]));
@@ -439,22 +493,22 @@ struct Impl {
         double* hcol = ctx->H + (size_t)j * (m + 1);
         const int hstride = (m + 1) * m;
         for (int pass = 0; pass < 2; ++pass) {
-          k_mdot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
+          k_mdot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
                                                                m + 1, ctx->gm_active);
-          k_mdot_final<<<S, 32, 0, st>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
+          k_mdot_final<<<S, 32, 0, counted(ctx, st)>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
                                          pass == 0 ? hstride : (m + 1), 0, S, ctx->gm_active);
-          k_mupdate<<<vec_grid(n, S), 256, 0, st>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
+          k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
                                                     pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
           if (pass == 1) {
             // h += h2
-            k_add_cols<<<S, 32, 0, st>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
+            k_add_cols<<<S, 32, 0, counted(ctx, st)>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
           }
         }
         // h_{j+1,j} = ||w|| ; v_{j+1} = w / h_{j+1,j}
-        k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, st>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
-        k_norm_to_h<<<(S + 127) / 128, 128, 0, st>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
-        k_scale_col<<<vec_grid(n, S), 256, 0, st>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
-        k_gmres_givens<<<(S + 127) / 128, 128, 0, st>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
+        k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
+        k_norm_to_h<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
+        k_scale_col<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
+        k_gmres_givens<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
                                                        ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, S);
         PINT_LAUNCHED();
         if (j + 1 >= remaining_cap) break;
@@ -468,14 +522,14 @@ struct Impl {
         }
       }
       // x += M^{-1} (V y)
-      k_gmres_solve<<<(S + 127) / 128, 128, 0, st>>>(m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
+      k_gmres_solve<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
                                                     S);
-      k_mcombine<<<vec_grid(n, S), 256, 0, st>>>(ctx->u, ctx->V, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
+      k_mcombine<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->u, ctx->V, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
                                                  ctx->cyc_active);
       vcycle(ctx, 0, S, ctx->u, ctx->z, ctx->cyc_active, st);
-      k_axpy_one<<<vec_grid(n, S), 256, 0, st>>>(x, ctx->z, n, ctx->cyc_active);
+      k_axpy_one<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, ctx->z, n, ctx->cyc_active);
       // true residual r = b - J x into ctx->u (reused as cycle start)
-      k_spmv<D, true><<<node_grid(ctx->g.nn, S), 128, 0, st>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+      k_spmv<D, true><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
       rvec = ctx->u;
       PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
@@ -503,7 +557,7 @@ struct Impl {
     std::vector<double> rnorm(S), target(S), tnorm(S), lam(S, 1.0);
     std::vector<int> running(S, 0), its(S, 0), ls(S, 0), accept(S, 0);
     PINT_CHECK(cudaMemcpyAsync(ctx->d_active, act.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-    k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(y, yo, n, ctx->d_active);  // Newton guess = previous state
+    k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(y, yo, n, ctx->d_active);  // Newton guess = previous state
     PINT_TRY(residual(ctx, S, y, yo, ctx->r, ctx->d_active, rnorm.data(), st));
     for (int s = 0; s < S; ++s) {
       if (!act[s]) continue;
@@ -520,10 +574,15 @@ struct Impl {
       PINT_CHECK(cudaMemcpyAsync(ctx->d_active, running.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
       PINT_TRY(assemble(ctx, S, y, yo, ctx->d_active, st));
       PINT_TRY(precond_setup(ctx, S, ko, ctx->d_active, st));
-      k_negate<<<vec_grid(n, S), 256, 0, st>>>(ctx->b, ctx->r, n, ctx->d_active);
+      k_negate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->b, ctx->r, n, ctx->d_active);
       PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, klin.data(), kres.data(), st));
       for (int s = 0; s < S; ++s)
         if (running[s]) kit[s] += klin[s];
+      if (ctx->verbose)
+        for (int s = 0; s < S; ++s)
+          if (running[s])
+            fprintf(stderr, "[pint] newton it %d slice %d |r| %.3e gmres its %d res %.3e\n", it, s, rnorm[s], klin[s],
+                    kres[s]);
       // line search: lambda = 1, halve until decrease or damping_min (accept anyway)
       for (int s = 0; s < S; ++s) { lam[s] = 1.0; ls[s] = running[s]; }
       for (;;) {
@@ -532,7 +591,7 @@ struct Impl {
         if (nls == 0) break;
         PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ls.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
         PINT_CHECK(cudaMemcpyAsync(ctx->d_lam, lam.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
-        k_trial<<<vec_grid(n, S), 256, 0, st>>>(ctx->ytrial, y, ctx->dx, ctx->d_lam, n, ctx->d_mask2);
+        k_trial<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->ytrial, y, ctx->dx, ctx->d_lam, n, ctx->d_mask2);
         std::vector<double> tn(S, 0.0);
         PINT_TRY(residual(ctx, S, ctx->ytrial, yo, ctx->rtrial, ctx->d_mask2, tn.data(), st));
         for (int s = 0; s < S; ++s) {
@@ -553,8 +612,8 @@ struct Impl {
         accept[s] = 1;
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, accept.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(y, ctx->ytrial, n, ctx->d_mask2);
-      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(ctx->r, ctx->rtrial, n, ctx->d_mask2);
+      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(y, ctx->ytrial, n, ctx->d_mask2);
+      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->r, ctx->rtrial, n, ctx->d_mask2);
       PINT_LAUNCHED();
       for (int s = 0; s < S; ++s) {
         if (!accept[s]) continue;
@@ -591,7 +650,7 @@ struct Impl {
         const double kk = (j == nsteps[s] - 1) ? (t_end[s] - t[s]) : k;
         const double theta = std::min(std::max(0.5 + theta0 * kk, 0.5), 1.0);
         t1[s] = t[s] + kk;
-        sts[s] = make_step(kk, theta, t1[s], ctx->desc.ramp_time);
+        sts[s] = make_step(ctx->desc, kk, theta, t1[s]);
         act[s] = 1;
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_st, sts.data(), sizeof(StepScalars) * S, cudaMemcpyHostToDevice, st));
@@ -604,7 +663,7 @@ struct Impl {
         t[s] = t1[s];
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ok.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-      k_copy_active<<<vec_grid(n, S), 256, 0, st>>>(ctx->ystate, ctx->ynew, n, ctx->d_mask2);
+      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->ystate, ctx->ynew, n, ctx->d_mask2);
       PINT_LAUNCHED();
     }
     PINT_CHECK(cudaMemcpyAsync(y_out, ctx->ystate, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
@@ -621,7 +680,7 @@ struct Impl {
 
 int upload_steps(pint_ctx* ctx, int S, const double* k, const double* theta, const double* t1, cudaStream_t st) {
   std::vector<StepScalars> sts(S);
-  for (int s = 0; s < S; ++s) sts[s] = make_step(k[s], theta[s], t1[s], ctx->desc.ramp_time);
+  for (int s = 0; s < S; ++s) sts[s] = make_step(ctx->desc, k[s], theta[s], t1[s]);
   PINT_CHECK(cudaMemcpyAsync(ctx->d_st, sts.data(), sizeof(StepScalars) * S, cudaMemcpyHostToDevice, st));
   return PINT_OK;
 }
@@ -653,6 +712,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->C = 2 * desc->dim + 1;
   ctx->maxS = max_slices;
   ctx->restart = restart;
+  ctx->verbose = std::getenv("PINT_VERBOSE") && std::getenv("PINT_VERBOSE")[0] == '1';
   ctx->cells[0] = desc->cells[0];
   ctx->cells[1] = desc->cells[1];
   ctx->cells[2] = desc->dim == 3 ? desc->cells[2] : 1;
@@ -663,7 +723,6 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ph.rho_s = desc->rho_s;
   ph.mu = desc->mu_s;
   ph.lam = desc->lambda_s;
-  ph.delta = desc->delta_p;
   double wq = 1.0, wf = 1.0;
   for (int m = 0; m < 3; ++m) {
     ph.h[m] = m < ctx->D ? desc->extent[m] / desc->cells[m] : 1.0;
@@ -746,6 +805,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->d_mask2, (size_t)S);
   ALLOC(ctx->d_lam, (size_t)S);
   ALLOC(ctx->d_st, (size_t)S);
+  ALLOC(ctx->d_work, (size_t)1);
 #undef ALLOC
   if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
       cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess) {
@@ -764,6 +824,7 @@ int pint_destroy(pint_ctx* ctx) {
   if (!ctx) return PINT_OK;
   cudaDeviceSynchronize();
   for (void* p : ctx->allocs) cudaFree(p);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->h_dbl) cudaFreeHost(ctx->h_dbl);
   if (ctx->h_int) cudaFreeHost(ctx->h_int);
   delete ctx;
@@ -785,6 +846,44 @@ int pint_flags(const pint_ctx* ctx, uint8_t* node_flags, uint8_t* cell_flags) {
   if (!ctx) return PINT_INVALID_ARG;
   if (node_flags) std::memcpy(node_flags, ctx->h_node_flags.data(), ctx->h_node_flags.size());
   if (cell_flags) std::memcpy(cell_flags, ctx->h_cell_flags.data(), ctx->h_cell_flags.size());
+  return PINT_OK;
+}
+
+int pint_profile(pint_ctx* ctx, int32_t enable) {
+  if (!ctx) return PINT_INVALID_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaDeviceSynchronize();
+  ctx->prof = enable != 0;
+  ctx->launches = 0;
+  ctx->ev_pairs.clear();
+  ctx->ev_used = 0;
+  cudaMemset(ctx->d_work, 0, sizeof(unsigned long long));
+  return PINT_OK;
+}
+
+int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches, int64_t* slice_launches,
+                      double* kernel_ms, int64_t* bytes_per_slice_launch) {
+  if (!ctx) return PINT_INVALID_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  PINT_CHECK(cudaDeviceSynchronize());
+  double ms = 0.0;
+  for (auto& pr : ctx->ev_pairs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, pr.first, pr.second);
+    ms += t;
+  }
+  unsigned long long work = 0;
+  PINT_CHECK(cudaMemcpy(&work, ctx->d_work, sizeof(work), cudaMemcpyDeviceToHost));
+  if (launches) *launches = ctx->launches;
+  if (kernel_launches) *kernel_launches = (int64_t)ctx->ev_pairs.size();
+  if (slice_launches) *slice_launches = (int64_t)work;
+  if (kernel_ms) *kernel_ms = ms;
+  if (bytes_per_slice_launch) {
+    const Grid& g = ctx->lv[0].g;
+    const int64_t C = ctx->C;
+    // A (noff C^2) + Dinv (C^2) + b + x_in + x_out (3 C), fp64, per node
+    *bytes_per_slice_launch = (int64_t)g.nn * 8 * ((int64_t)g.noff * C * C + C * C + 3 * C);
+  }
   return PINT_OK;
 }
 

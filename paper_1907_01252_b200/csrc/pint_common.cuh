@@ -82,11 +82,12 @@ struct StepScalars {
   double kt;     // k * theta
   double ko;     // k * (1 - theta)
   double ramp;   // inflow ramp s(t1)
+  double delta;  // pressure stabilization delta_K(k)
 };
 
 // physical parameters of the element kernel
 struct Phys {
-  double rho_f, rnu, rho_s, mu, lam, delta;
+  double rho_f, rnu, rho_s, mu, lam;
   double h[3];
   double wq;     // volume quadrature weight per point
   double wf;     // outflow face quadrature weight per point

@@ -24,8 +24,11 @@ Shared decisions (DESIGN.md §2 restates them):
   and, in 3-d, z = 0, z = H); u = 0 on the whole outer boundary; the outlet
   x = Lx is do-nothing with the paper's boundary correction term;
 * inflow ramp s(t) = forcing_s(min(t, 0.5), 0.5) (reference problems.py:214-221);
-* pressure stabilization: Brezzi-Pitkaranta delta_K (ref. coordinates),
-  delta = alpha_p h^2 / (rho_f (nu_f + U h));
+* pressure stabilization: PSPG-type Brezzi-Pitkaranta term
+  k delta (grad p, grad xi) in reference coordinates with the transient
+  time scale, delta = alpha_p / (rho_f (1/k + U/h + nu_f/h^2)), so the
+  pressure Schur complement and the stabilization stay balanced for every
+  step size (the coarse and the fine propagator each use their own k);
 * quadrature: tensor 2-point Gauss per direction, 2-point (2-d) / 2x2 (3-d)
   on the outflow face.
 """
@@ -57,7 +60,7 @@ class FSIProblem:
     nu_s: float = 0.4
     u_peak: float = 1.0
     ramp_time: float = 0.5
-    alpha_p: float = 0.1
+    alpha_p: float = 1.0
     name: str = "custom"
 
     def __post_init__(self):
@@ -106,11 +109,14 @@ class FSIProblem:
         return 2.0 * self.mu_s * self.nu_s / (1.0 - 2.0 * self.nu_s)
 
     @property
-    def delta_p(self) -> float:
-        """Pressure-stabilization coefficient delta_K (uniform mesh)."""
-        h2 = sum(x * x for x in self.h) / self.dim
-        hk = math.sqrt(h2)
-        return self.alpha_p * h2 / (self.rho_f * (self.nu_f + self.u_peak * hk))
+    def h_k(self) -> float:
+        """Cell size used by the stabilization: sqrt(mean h_m^2)."""
+        return math.sqrt(sum(x * x for x in self.h) / self.dim)
+
+    def delta_p(self, k: float) -> float:
+        """Pressure-stabilization coefficient delta_K for step size k."""
+        hk = self.h_k
+        return self.alpha_p / (self.rho_f * (1.0 / k + self.u_peak / hk + self.nu_f / (hk * hk)))
 
     @property
     def component_names(self) -> Tuple[str, ...]:

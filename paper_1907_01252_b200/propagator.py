@@ -79,7 +79,7 @@ class KrylovSettings:
     max_iters: int = 300
     pre_smooth: int = 2
     post_smooth: int = 2
-    omega: float = 0.7
+    omega: float = 0.5
     max_levels: int = 0
     coarse_sweeps: int = 20
 
@@ -158,7 +158,7 @@ def problem_desc(p: FSIProblem) -> _lib.ProblemDesc:
         d.bar_hi[m] = p.bar_hi[m] if m < p.dim else 0.0
     d.rho_f, d.nu_f, d.rho_s, d.mu_s = p.rho_f, p.nu_f, p.rho_s, p.mu_s
     d.lambda_s = p.lambda_s
-    d.u_peak, d.ramp_time, d.delta_p = p.u_peak, p.ramp_time, p.delta_p
+    d.u_peak, d.ramp_time, d.alpha_p = p.u_peak, p.ramp_time, p.alpha_p
     return d
 
 
@@ -288,6 +288,16 @@ class FSIDevice:
         self.check(self.lib.pint_linear_solve(self.handle, S, _ptr(b), _ptr(out), ctypes.byref(ko), its, res,
                                               _stream()), "pint_linear_solve")
         return out, np.array(its[:]), np.array(res[:])
+
+    def profile(self, enable: bool):
+        self.check(self.lib.pint_profile(self.handle, 1 if enable else 0), "pint_profile")
+
+    def profile_read(self) -> dict:
+        vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()]
+        self.check(self.lib.pint_profile_read(self.handle, *[ctypes.byref(v) for v in vals]), "pint_profile_read")
+        launches, klaunch, slaunch, ms, bpsl = [v.value for v in vals]
+        return {"launches": launches, "kernel_launches": klaunch, "slice_launches": slaunch,
+                "kernel_ms": ms, "bytes_per_slice_launch": bpsl}
 
     def flags(self):
         nf = (ctypes.c_uint8 * self.nn)()
