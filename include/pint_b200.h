@@ -121,8 +121,9 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
                       int32_t* its, double* resid, void* stream);
 
 /* ---- profiling (bench.py) --------------------------------------------
- * enable != 0: count launches and bracket every level-0 smoother sweep (the
- * dominant kernel of the fine step) with CUDA events on its stream.
+ * enable: resets the counters; 1 = count launches only (CUDA-graph replay
+ * stays on), 2 = also bracket every level-0 smoother sweep (the dominant
+ * kernel of the fine step) with CUDA events on its stream (graphs off).
  * read: launches issued, profiled-kernel launches, active slice-launches of it,
  * its summed event time (ms) and its algorithmic bytes per slice-launch. */
 int pint_profile(pint_ctx* ctx, int32_t enable);

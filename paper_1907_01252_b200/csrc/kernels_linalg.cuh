@@ -11,7 +11,7 @@
 namespace pint {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedChunk = 4096;  // elements per reduction block (fixed => batch invariant)
+constexpr int kRedChunk = 1024;  // elements per reduction block (fixed => batch invariant)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -32,6 +32,60 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   }
   __syncthreads();
   return out;
+}
+
+// Neighbour node of every stencil offset; offsets that leave the grid are
+// clamped to the node itself.  Their coefficients are exactly zero (assembly,
+// fix-up and RAP never write a non-zero there), so the products vanish and
+// every load of a sweep is issued without a data-dependent branch.
+template <int D>
+__device__ __forceinline__ void stencil_neighbours(const Grid& g, int n, int (&nbs)[D == 2 ? 9 : 27]) {
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+#pragma unroll
+  for (int off = 0; off < (D == 2 ? 9 : 27); ++off) {
+    int di, dj, dk;
+    offset_delta(off, D, di, dj, dk);
+    const int a = i + di, b = j + dj, c = k + dk;
+    const bool ok = a >= 0 && a < g.n[0] && b >= 0 && b < g.n[1] && c >= 0 && c < g.n[2];
+    nbs[off] = ok ? node_index(g, a, b, c) : n;
+  }
+}
+
+// Read-only global load the compiler may not sink below the FMAs that use it:
+// volatile asm keeps the program order of the loads, so a stencil row issues
+// all its loads back to back (2C per offset) before the first FMA stalls.
+__device__ __forceinline__ double ld_nc(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// One block-stencil row: sum_off sum_cb A[off][ca][cb][n] x[cb][nb(off)].
+// Latency-bound at the small configs (c1/c2 operators are L2-resident), so
+// all 2*C*NOFF loads of the row are put in flight before any FMA.
+template <int D, int BATCH>
+__device__ __forceinline__ double stencil_row(const double* __restrict__ Arow, const double* __restrict__ xs, int np,
+                                              const int (&nbs)[D == 2 ? 9 : 27]) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  double part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int o0 = 0; o0 < NOFF; o0 += BATCH) {
+    double a[BATCH][C], xv[BATCH][C];
+#pragma unroll
+    for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) {
+        a[q][cb] = ld_nc(Arow + ((size_t)(o0 + q) * C * C + cb) * np);
+        xv[q][cb] = ld_nc(xs + cb * np + nbs[o0 + q]);
+      }
+#pragma unroll
+    for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) part[q % 3] = fma(a[q][cb], xv[q][cb], part[q % 3]);
+  }
+  return (part[0] + part[1]) + part[2];
 }
 
 // ---------------------------------------------------------------- generic vector kernels
@@ -125,26 +179,26 @@ __global__ void k_dot_final(const double* __restrict__ partial, int nblk, double
   out[s] = acc;
 }
 
-// multi-dot: partial[s][i][blk] = <V_i, w> over the chunk, i = 0..nv-1
+// multi-dot: partial[s][v][blk] = <V_v, w> over the chunk; grid (nblk, nv, S)
 __global__ void __launch_bounds__(kRedThreads) k_mdot_partial(const double* __restrict__ V, size_t vstride,
                                                              const double* __restrict__ w, int nv, size_t per_slice,
                                                              double* __restrict__ partial, int nblk, int maxv,
                                                              const int* __restrict__ active) {
   __shared__ double sh[kRedThreads / 32];
-  const int s = blockIdx.y;
+  const int s = blockIdx.z;
+  const int v = blockIdx.y;
   if (active && !active[s]) return;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
-  for (int v = 0; v < nv; ++v) {
-    const double* vs = V + v * vstride + s * per_slice;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
-      const size_t e = base + i;
-      if (e < per_slice) acc += vs[e] * ws[e];
-    }
-    acc = block_sum(acc, sh);
-    if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
+  const double* vs = V + v * vstride + s * per_slice;
+  double acc = 0.0;
+#pragma unroll
+  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+    const size_t e = base + i;
+    if (e < per_slice) acc += vs[e] * ws[e];
   }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
 }
 
 // h[s][i] (+)= sum_b partial[s][i][b]
@@ -191,44 +245,32 @@ __global__ void k_mcombine(double* __restrict__ out, const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------- K3 block-stencil SpMV
-// y = A x  or  y = b - A x (residual form)
-template <int D, bool RESID>
-__global__ void __launch_bounds__(128) k_spmv(Grid g, const double* __restrict__ A, const double* __restrict__ x,
-                                             const double* __restrict__ b, double* __restrict__ y,
-                                             const int* __restrict__ active) {
+// y = A x  or  y = b - A x (residual form).  Thread = (node, row component):
+// blockDim (32, C) so a warp reads one coefficient plane of 32 consecutive
+// nodes (256 B, coalesced) and the C row-threads of a node share its x
+// neighbours through L1.  5-7x more threads than node-per-thread: these
+// kernels are latency-bound at the small configs (c1/c2 live in L2).
+template <int D, bool RESID, int BATCH>
+__global__ void __launch_bounds__(32 * (2 * D + 1), 1) k_spmv(Grid g, const double* __restrict__ A,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ b, double* __restrict__ y,
+                                                          const int* __restrict__ active) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.y;
   if (active && !active[s]) return;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.x * 32 + threadIdx.x;
   if (n >= g.nn) return;
+  const int ca = threadIdx.y;
   const int np = g.np;
   const size_t vs = (size_t)C * np;
-  const double* As = A + (size_t)s * NOFF * C * C * np + n;
+  const double* As = A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
   const double* xs = x + s * vs;
-  int i, j, k;
-  node_coords(g, n, i, j, k);
-  double acc[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.0;
-#pragma unroll
-  for (int off = 0; off < NOFF; ++off) {
-    const int nb = neighbour(g, i, j, k, off);
-    if (nb < 0) continue;
-    double xv[C];
-#pragma unroll
-    for (int cb = 0; cb < C; ++cb) xv[cb] = __ldg(xs + cb * np + nb);
-#pragma unroll
-    for (int ca = 0; ca < C; ++ca)
-#pragma unroll
-      for (int cb = 0; cb < C; ++cb) acc[ca] += __ldg(As + ((size_t)(off * C + ca) * C + cb) * np) * xv[cb];
-  }
-  double* ys = y + s * vs;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (RESID) ys[c * np + n] = b[s * vs + c * np + n] - acc[c];
-    else ys[c * np + n] = acc[c];
-  }
+  int nbs[NOFF];
+  stencil_neighbours<D>(g, n, nbs);
+  const double acc = stencil_row<D, BATCH>(As, xs, np, nbs);
+  const size_t o = s * vs + (size_t)ca * np + n;
+  y[o] = RESID ? b[o] - acc : acc;
 }
 
 // ---------------------------------------------------------------- K4 node-block Jacobi
@@ -271,52 +313,49 @@ __global__ void k_block_inverse(Grid g, const double* __restrict__ A, double* __
     for (int c = 0; c < C; ++c) Ds[((size_t)r * C + c) * np + n] = a[r][C + c];
 }
 
-// x_out = (x_in ? x_in : 0) + omega Dinv (b - A x_in)
-template <int D, bool FIRST>
-__global__ void __launch_bounds__(128) k_smooth(Grid g, const double* __restrict__ A, const double* __restrict__ Dinv,
-                                               const double* __restrict__ b, const double* __restrict__ xin,
-                                               double* __restrict__ xout, double omega,
-                                               const int* __restrict__ active,
-                                               unsigned long long* __restrict__ work) {
+// x_out = (x_in ? x_in : 0) + omega Dinv (b - A x_in); thread = (node, row)
+// as k_spmv, the node's C residual rows meet in shared memory for Dinv.
+template <int D, bool FIRST, int BATCH>
+__global__ void __launch_bounds__(32 * (2 * D + 1), 1) k_smooth(Grid g, const double* __restrict__ A,
+                                                            const double* __restrict__ Dinv,
+                                                            const double* __restrict__ b,
+                                                            const double* __restrict__ xin,
+                                                            double* __restrict__ xout, double omega,
+                                                            const int* __restrict__ active,
+                                                            unsigned long long* __restrict__ work) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
+  __shared__ double rsh[C][32];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
-  if (work && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(work, 1ULL);  // profiling: active slice-launches
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= g.nn) return;
+  if (work && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(work, 1ULL);
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int ca = threadIdx.y;
+  const bool live = n < g.nn;
   const int np = g.np;
   const size_t vs = (size_t)C * np;
-  double res[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) res[c] = __ldg(b + s * vs + c * np + n);
-  if (!FIRST) {
-    const double* As = A + (size_t)s * NOFF * C * C * np + n;
-    const double* xs = xin + s * vs;
-    int i, j, k;
-    node_coords(g, n, i, j, k);
-#pragma unroll
-    for (int off = 0; off < NOFF; ++off) {
-      const int nb = neighbour(g, i, j, k, off);
-      if (nb < 0) continue;
-      double xv[C];
-#pragma unroll
-      for (int cb = 0; cb < C; ++cb) xv[cb] = __ldg(xs + cb * np + nb);
-#pragma unroll
-      for (int ca = 0; ca < C; ++ca)
-#pragma unroll
-        for (int cb = 0; cb < C; ++cb) res[ca] -= __ldg(As + ((size_t)(off * C + ca) * C + cb) * np) * xv[cb];
+  double res = 0.0;
+  if (live) {
+    res = __ldg(b + s * vs + (size_t)ca * np + n);
+    if (!FIRST) {
+      const double* As = A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
+      const double* xs = xin + s * vs;
+      int nbs[NOFF];
+      stencil_neighbours<D>(g, n, nbs);
+      const double acc = stencil_row<D, BATCH>(As, xs, np, nbs);
+      res -= acc;
     }
   }
-  const double* Ds = Dinv + (size_t)s * C * C * np + n;
+  rsh[ca][threadIdx.x] = res;
+  __syncthreads();
+  if (!live) return;
+  const double* Ds = Dinv + (size_t)s * C * C * np + (size_t)ca * C * np + n;
+  double z = 0.0;
 #pragma unroll
-  for (int ca = 0; ca < C; ++ca) {
-    double z = 0.0;
-#pragma unroll
-    for (int cb = 0; cb < C; ++cb) z += __ldg(Ds + (size_t)(ca * C + cb) * np) * res[cb];
-    const double base = FIRST ? 0.0 : xin[s * vs + ca * np + n];
-    xout[s * vs + ca * np + n] = base + omega * z;
-  }
+  for (int cb = 0; cb < C; ++cb) z += __ldg(Ds + (size_t)cb * np) * rsh[cb][threadIdx.x];
+  const size_t o = s * vs + (size_t)ca * np + n;
+  const double base = FIRST ? 0.0 : xin[o];
+  xout[o] = base + omega * z;
 }
 
 // ---------------------------------------------------------------- grid transfer (Q1 bilinear / trilinear)

@@ -17,7 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -49,6 +51,15 @@ size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
 struct pint_ctx;
 static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st);
+
+struct GraphKey {
+  int S, j, levels, pre, post, coarse;
+  double omega;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(S, j, levels, pre, post, coarse, omega) <
+           std::tie(o.S, o.j, o.levels, o.pre, o.post, o.coarse, o.omega);
+  }
+};
 
 struct pint_ctx {
   pint_problem_desc desc{};
@@ -88,6 +99,10 @@ struct pint_ctx {
   std::mutex mu;
   std::string err;
   int prec_levels = 0;  // levels set up by the last precond_setup
+  bool use_graphs = true;  // PINT_GRAPHS=0 disables CUDA-graph replay of Arnoldi steps
+  std::map<GraphKey, std::pair<cudaGraphExec_t, long long>> graphs;
+  cudaStream_t stream = nullptr;  // internal non-blocking stream (capturable)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
   // profiling (bench.py roofline): launch count and CUDA-event timing of the
   // level-0 smoother sweeps, the dominant kernel of the fine step
@@ -195,6 +210,12 @@ StepScalars make_step(const pint_problem_desc& d, double k, double theta, double
 }
 
 inline dim3 node_grid(int nn, int S, int bs = 128) { return dim3((nn + bs - 1) / bs, S); }
+inline dim3 row_grid(int nn, int S) { return dim3((nn + 31) / 32, S); }
+// enough CTAs to fill the GPU several times: use the lower-register variant
+// (3 offsets of loads in flight) for occupancy; small grids put all 9 in flight
+inline bool wide(int nn, int S) { return (size_t)((nn + 31) / 32) * S >= 4 * 148; }
+template <int D>
+inline dim3 row_block() { return dim3(32, 2 * D + 1); }
 inline dim3 vec_grid(size_t n, int S) {
   size_t blocks = (n + 255) / 256;
   if (blocks > 1024) blocks = 1024;
@@ -342,7 +363,10 @@ struct Impl {
 
   static void spmv(pint_ctx* ctx, int lvl, int S, const double* x, double* y, const int* mask, cudaStream_t st) {
     Level& L = ctx->lv[lvl];
-    k_spmv<D, false><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
+    if (wide(L.g.nn, S))
+      k_spmv<D, false, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
+    else
+      k_spmv<D, false, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
   }
 
   // ---- multigrid setup: RAP on all levels, block inverses, dense coarsest
@@ -372,8 +396,8 @@ struct Impl {
                      const int* mask, cudaStream_t st, bool first) {
     const double om = ctx->kopt.omega;
     if (first) {
-      k_smooth<D, true><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, nullptr, xout, om,
-                                                                           mask, nullptr);
+      k_smooth<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, nullptr,
+                                                                                    xout, om, mask, nullptr);
       return;
     }
     const bool prof = ctx->prof && &L == &ctx->lv[0];
@@ -383,8 +407,12 @@ struct Impl {
       e1 = next_event(ctx);
       cudaEventRecord(e0, st);
     }
-    k_smooth<D, false><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, xin, xout, om, mask,
-                                                                          prof ? ctx->d_work : nullptr);
+    if (wide(L.g.nn, S))
+      k_smooth<D, false, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(
+          L.g, L.A, L.Dinv, b, xin, xout, om, mask, prof ? ctx->d_work : nullptr);
+    else
+      k_smooth<D, false, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(
+          L.g, L.A, L.Dinv, b, xin, xout, om, mask, prof ? ctx->d_work : nullptr);
     if (prof) {
       cudaEventRecord(e1, st);
       ctx->ev_pairs.emplace_back(e0, e1);
@@ -422,7 +450,10 @@ struct Impl {
       smooth(ctx, L, S, b, cur, nxt, mask, st, false);
       std::swap(cur, nxt);
     }
-    k_spmv<D, true><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
+    if (wide(L.g.nn, S))
+      k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
+    else
+      k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
     k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
@@ -432,6 +463,71 @@ struct Impl {
       smooth(ctx, L, S, b, cur, out, mask, st, false);
       std::swap(cur, nxt);
     }
+  }
+
+  // one Arnoldi step j of GMRES for the slices in gm_active (device mask):
+  // z = M^{-1} v_j, w = J z, CGS2 against v_0..v_j, h_{j+1,j} = ||w||,
+  // v_{j+1} = w / h_{j+1,j}, Givens update.  Every scalar it needs lives in
+  // device memory, so the sequence is captured once per (S, j, options) as
+  // a CUDA graph and replayed.
+  static void arnoldi_step(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    const int m = ctx->restart;
+    const size_t n = vs(ctx);
+    const size_t vstride = (size_t)ctx->maxS * n;
+    const int nblk = ctx->nblk;
+    double* vj = ctx->V + j * vstride;
+    double* vj1 = ctx->V + (j + 1) * vstride;
+    // z = M^{-1} v_j ; w = J z
+    vcycle(ctx, 0, S, vj, ctx->z, ctx->gm_active, st);
+    spmv(ctx, 0, S, ctx->z, ctx->w, ctx->gm_active, st);
+    // CGS2 against v_0..v_j
+    double* hcol = ctx->H + (size_t)j * (m + 1);
+    const int hstride = (m + 1) * m;
+    for (int pass = 0; pass < 2; ++pass) {
+      k_mdot_partial<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
+                                                           m + 1, ctx->gm_active);
+      k_mdot_final<<<S, 32, 0, counted(ctx, st)>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
+                                     pass == 0 ? hstride : (m + 1), 0, S, ctx->gm_active);
+      k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
+                                                pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
+      if (pass == 1) {
+        // h += h2
+        k_add_cols<<<S, 32, 0, counted(ctx, st)>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
+      }
+    }
+    // h_{j+1,j} = ||w|| ; v_{j+1} = w / h_{j+1,j}
+    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
+    k_norm_to_h<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
+    k_scale_col<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
+    k_gmres_givens<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
+                                                   ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, S);
+  }
+
+  static int run_arnoldi(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    if (!ctx->use_graphs || ctx->prof) {
+      arnoldi_step(ctx, S, j, st);
+      PINT_LAUNCHED();
+      return PINT_OK;
+    }
+    const GraphKey key{S, j, ctx->prec_levels, ctx->kopt.pre_smooth, ctx->kopt.post_smooth, ctx->kopt.coarse_sweeps,
+                       ctx->kopt.omega};
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+      cudaGraph_t graph;
+      const long long before = ctx->launches;
+      PINT_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      arnoldi_step(ctx, S, j, st);
+      PINT_CHECK(cudaStreamEndCapture(st, &graph));
+      cudaGraphExec_t exec;
+      PINT_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      const long long nodes = ctx->launches - before;
+      ctx->launches = before;
+      it = ctx->graphs.emplace(key, std::make_pair(exec, nodes)).first;
+    }
+    PINT_CHECK(cudaGraphLaunch(it->second.first, st));
+    ctx->launches += it->second.second;
+    return PINT_OK;
   }
 
   // ---- GMRES(m), right preconditioned:  J x = b  for slices in mask
@@ -484,32 +580,7 @@ struct Impl {
       for (int s = 0; s < S; ++s)
         if (cyc[s]) remaining_cap = std::min(remaining_cap, std::max(1, ko->max_iters - its[s]));
       for (int j = 0; j < m; ++j) {
-        double* vj = ctx->V + j * vstride;
-        double* vj1 = ctx->V + (j + 1) * vstride;
-        // z = M^{-1} v_j ; w = J z
-        vcycle(ctx, 0, S, vj, ctx->z, ctx->gm_active, st);
-        spmv(ctx, 0, S, ctx->z, ctx->w, ctx->gm_active, st);
-        // CGS2 against v_0..v_j
-        double* hcol = ctx->H + (size_t)j * (m + 1);
-        const int hstride = (m + 1) * m;
-        for (int pass = 0; pass < 2; ++pass) {
-          k_mdot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
-                                                               m + 1, ctx->gm_active);
-          k_mdot_final<<<S, 32, 0, counted(ctx, st)>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
-                                         pass == 0 ? hstride : (m + 1), 0, S, ctx->gm_active);
-          k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
-                                                    pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
-          if (pass == 1) {
-            // h += h2
-            k_add_cols<<<S, 32, 0, counted(ctx, st)>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
-          }
-        }
-        // h_{j+1,j} = ||w|| ; v_{j+1} = w / h_{j+1,j}
-        k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
-        k_norm_to_h<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
-        k_scale_col<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
-        k_gmres_givens<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
-                                                       ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, S);
+        PINT_TRY(run_arnoldi(ctx, S, j, st));
         PINT_LAUNCHED();
         if (j + 1 >= remaining_cap) break;
         // poll: any slice still iterating?
@@ -529,7 +600,10 @@ struct Impl {
       vcycle(ctx, 0, S, ctx->u, ctx->z, ctx->cyc_active, st);
       k_axpy_one<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, ctx->z, n, ctx->cyc_active);
       // true residual r = b - J x into ctx->u (reused as cycle start)
-      k_spmv<D, true><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+      if (wide(ctx->g.nn, S))
+        k_spmv<D, true, 3><<<row_grid(ctx->g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+      else
+        k_spmv<D, true, 9><<<row_grid(ctx->g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
       rvec = ctx->u;
       PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
@@ -678,6 +752,21 @@ struct Impl {
   }
 };
 
+// Public calls run on the context's own non-blocking stream (so Arnoldi
+// steps can be graph-captured), ordered after / before the caller's stream.
+struct StreamGuard {
+  pint_ctx* ctx;
+  cudaStream_t user;
+  StreamGuard(pint_ctx* c, void* s) : ctx(c), user((cudaStream_t)s) {
+    cudaEventRecord(ctx->ev_in, user);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0);
+  }
+  ~StreamGuard() {
+    cudaEventRecord(ctx->ev_out, ctx->stream);
+    cudaStreamWaitEvent(user, ctx->ev_out, 0);
+  }
+};
+
 int upload_steps(pint_ctx* ctx, int S, const double* k, const double* theta, const double* t1, cudaStream_t st) {
   std::vector<StepScalars> sts(S);
   for (int s = 0; s < S; ++s) sts[s] = make_step(ctx->desc, k[s], theta[s], t1[s]);
@@ -713,6 +802,13 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->maxS = max_slices;
   ctx->restart = restart;
   ctx->verbose = std::getenv("PINT_VERBOSE") && std::getenv("PINT_VERBOSE")[0] == '1';
+  ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+    ctx->err = "stream/event creation failed";
+    return PINT_CUDA_ERROR;
+  }
   ctx->cells[0] = desc->cells[0];
   ctx->cells[1] = desc->cells[1];
   ctx->cells[2] = desc->dim == 3 ? desc->cells[2] : 1;
@@ -825,6 +921,10 @@ int pint_destroy(pint_ctx* ctx) {
   cudaDeviceSynchronize();
   for (void* p : ctx->allocs) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.first);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   if (ctx->h_dbl) cudaFreeHost(ctx->h_dbl);
   if (ctx->h_int) cudaFreeHost(ctx->h_int);
   delete ctx;
@@ -853,7 +953,7 @@ int pint_profile(pint_ctx* ctx, int32_t enable) {
   if (!ctx) return PINT_INVALID_ARG;
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaDeviceSynchronize();
-  ctx->prof = enable != 0;
+  ctx->prof = enable == 2;  // 1: count launches only (graphs stay on); 2: + CUDA events around the kernel
   ctx->launches = 0;
   ctx->ev_pairs.clear();
   ctx->ev_used = 0;
@@ -904,7 +1004,8 @@ int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, 
     return PINT_INVALID_ARG;
   }
   std::lock_guard<std::mutex> lock(ctx->mu);
-  cudaStream_t st = (cudaStream_t)stream;
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
   return DISPATCH(propagate(ctx, S, y_in, y_out, t0, t_end, nsteps, k, theta0, newton, krylov, newton_iters,
                             krylov_iters, status, fail_t, st));
 }
@@ -914,7 +1015,8 @@ int pint_residual(pint_ctx* ctx, int32_t S, const double* y, const double* y_old
   int rc = check_S(ctx, S);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
-  cudaStream_t st = (cudaStream_t)stream;
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
   if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
   std::vector<double> tmp(S);
   rc = DISPATCH(residual(ctx, S, y, y_old, r, nullptr, tmp.data(), st));
@@ -927,7 +1029,8 @@ int pint_jvp(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, con
   int rc = check_S(ctx, S);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
-  cudaStream_t st = (cudaStream_t)stream;
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
   if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
   return DISPATCH(jvp(ctx, S, y, y_old, w, Jw, st));
 }
@@ -937,7 +1040,8 @@ int pint_assemble(pint_ctx* ctx, int32_t S, const double* y, const double* y_old
   int rc = check_S(ctx, S);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
-  cudaStream_t st = (cudaStream_t)stream;
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
   if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
   return DISPATCH(assemble(ctx, S, y, y_old, nullptr, st));
 }
@@ -947,8 +1051,8 @@ int pint_jacobian_blocks(pint_ctx* ctx, int32_t S, double* out, void* stream) {
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
   const size_t ms = (size_t)ctx->g.noff * ctx->C * ctx->C * ctx->g.np;
-  PINT_CHECK(cudaMemcpyAsync(out, ctx->lv[0].A, sizeof(double) * ms * S, cudaMemcpyDeviceToDevice,
-                             (cudaStream_t)stream));
+  StreamGuard guard(ctx, stream);
+  PINT_CHECK(cudaMemcpyAsync(out, ctx->lv[0].A, sizeof(double) * ms * S, cudaMemcpyDeviceToDevice, ctx->stream));
   return PINT_OK;
 }
 
@@ -956,7 +1060,8 @@ int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream
   int rc = check_S(ctx, S);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
-  DISPATCH(spmv(ctx, 0, S, x, y, nullptr, (cudaStream_t)stream));
+  StreamGuard guard(ctx, stream);
+  DISPATCH(spmv(ctx, 0, S, x, y, nullptr, ctx->stream));
   PINT_LAUNCHED();
   return PINT_OK;
 }
@@ -965,7 +1070,8 @@ int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov,
   int rc = check_S(ctx, S);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
-  return DISPATCH(precond_setup(ctx, S, krylov, nullptr, (cudaStream_t)stream));
+  StreamGuard guard(ctx, stream);
+  return DISPATCH(precond_setup(ctx, S, krylov, nullptr, ctx->stream));
 }
 
 int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, void* stream) {
@@ -976,7 +1082,8 @@ int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, voi
     ctx->err = "pint_precond_apply before pint_precond_setup";
     return PINT_INVALID_ARG;
   }
-  DISPATCH(vcycle(ctx, 0, S, b, x, nullptr, (cudaStream_t)stream));
+  StreamGuard guard(ctx, stream);
+  DISPATCH(vcycle(ctx, 0, S, b, x, nullptr, ctx->stream));
   PINT_LAUNCHED();
   return PINT_OK;
 }
@@ -990,7 +1097,8 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
     return PINT_INVALID_ARG;
   }
   std::lock_guard<std::mutex> lock(ctx->mu);
-  return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, its, resid, (cudaStream_t)stream));
+  StreamGuard guard(ctx, stream);
+  return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, its, resid, ctx->stream));
 }
 
 int pint_parareal_precorrect(int32_t S, int32_t C, int32_t nn, int32_t np, const double* f_old,

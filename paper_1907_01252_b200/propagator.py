@@ -289,8 +289,9 @@ class FSIDevice:
                                               _stream()), "pint_linear_solve")
         return out, np.array(its[:]), np.array(res[:])
 
-    def profile(self, enable: bool):
-        self.check(self.lib.pint_profile(self.handle, 1 if enable else 0), "pint_profile")
+    def profile(self, mode: int):
+        """0 off, 1 count launches, 2 count + CUDA-event timing of the level-0 smoother."""
+        self.check(self.lib.pint_profile(self.handle, int(mode)), "pint_profile")
 
     def profile_read(self) -> dict:
         vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()]
