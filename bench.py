@@ -240,16 +240,16 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = dev.profile_read()["launches"]
-    units = ws * L * m_f * args.steps
-    value = units / (elapsed_ms / 1e3)
-    nit = (F.newton_iterations - nit0) / (L * m_f * args.steps)
-    kit = (F.krylov_iterations - kit0) / max(1, F.newton_iterations - nit0)
     elapsed_ms = ev0.elapsed_time(ev1)
     if ws > 1:
         tt = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed_ms = float(tt.item())
         dist.barrier()
+    units = ws * L * m_f * args.steps
+    value = units / (elapsed_ms / 1e3)
+    nit = (F.newton_iterations - nit0) / (L * m_f * args.steps)
+    kit = (F.krylov_iterations - kit0) / max(1, F.newton_iterations - nit0)
     # kernel pass: one more step with CUDA events bracketing every launch of the
     # dominant kernel (plain launches: events cannot sit inside a replayed graph)
     dev.profile(2)

@@ -250,8 +250,16 @@ __global__ void k_mcombine(double* __restrict__ out, const double* __restrict__ 
 // nodes (256 B, coalesced) and the C row-threads of a node share its x
 // neighbours through L1.  5-7x more threads than node-per-thread: these
 // kernels are latency-bound at the small configs (c1/c2 live in L2).
+// resident CTAs per SM the compiler must allow: the wide (BATCH = 3) variant
+// trades loads-in-flight per thread for occupancy, the narrow one (all 9
+// offsets in flight) is for small grids where occupancy is moot
+template <int D, int BATCH>
+struct StencilOcc {
+  static constexpr int value = BATCH >= 9 ? 1 : (D == 2 ? 4 : 2);
+};
+
 template <int D, bool RESID, int BATCH>
-__global__ void __launch_bounds__(32 * (2 * D + 1), 1) k_spmv(Grid g, const double* __restrict__ A,
+__global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value)) k_spmv(Grid g, const double* __restrict__ A,
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ y,
                                                           const int* __restrict__ active) {
@@ -316,7 +324,7 @@ __global__ void k_block_inverse(Grid g, const double* __restrict__ A, double* __
 // x_out = (x_in ? x_in : 0) + omega Dinv (b - A x_in); thread = (node, row)
 // as k_spmv, the node's C residual rows meet in shared memory for Dinv.
 template <int D, bool FIRST, int BATCH>
-__global__ void __launch_bounds__(32 * (2 * D + 1), 1) k_smooth(Grid g, const double* __restrict__ A,
+__global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value)) k_smooth(Grid g, const double* __restrict__ A,
                                                             const double* __restrict__ Dinv,
                                                             const double* __restrict__ b,
                                                             const double* __restrict__ xin,
