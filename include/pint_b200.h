@@ -72,7 +72,8 @@ typedef struct pint_krylov_opts {
   int32_t pre_smooth, post_smooth;
   double omega;
   int32_t max_levels;    /* 0 = as many as the mesh allows */
-  int32_t coarse_sweeps; /* block-Jacobi sweeps when the coarsest level is too big for a dense inverse */
+  int32_t coarse_sweeps; /* smoothing sweeps when the coarsest level is too big for a dense inverse */
+  int32_t smoother;      /* 0 node-block Jacobi, 1 cell-patch Vanka (default) */
 } pint_krylov_opts;
 
 /* ---- lifetime -------------------------------------------------------- */

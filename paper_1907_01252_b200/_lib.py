@@ -77,6 +77,7 @@ class KrylovOpts(ctypes.Structure):
         ("omega", ctypes.c_double),
         ("max_levels", ctypes.c_int32),
         ("coarse_sweeps", ctypes.c_int32),
+        ("smoother", ctypes.c_int32),
     ]
 
 

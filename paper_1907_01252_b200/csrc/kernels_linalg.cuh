@@ -682,3 +682,185 @@ __global__ void k_axpy_one(double* __restrict__ x, const double* __restrict__ z,
 }
 
 }  // namespace pint
+
+// ======================================================================
+// Cell-patch (Vanka-type) smoother: every cell's L = 2^d C dofs form a local
+// saddle-point block A_c (extracted from the block stencil) that is inverted
+// exactly once per setup; one sweep is x += omega W sum_c P_c^T A_c^{-1} P_c r
+// with r = b - A x and W = 1 / (cells sharing the node).  Robust where the
+// node-block Jacobi smoother stalls (developed-flow c3 states, SURVEY §7 hard
+// part 6): the local solve sees the velocity-pressure and velocity-deformation
+// couplings of the whole cell.
+// ======================================================================
+namespace pint {
+
+template <int D>
+struct Cells {
+  static constexpr int A = 1 << D;
+  static constexpr int C = 2 * D + 1;
+  static constexpr int L = A * C;
+};
+
+// cell index -> corner nodes (x fastest); grid g is the node grid
+template <int D>
+__device__ __forceinline__ void cell_nodes(const Grid& g, int cell, int (&nodes)[1 << D]) {
+  const int cx = g.n[0] - 1, cy = g.n[1] - 1;
+  const int ci = cell % cx;
+  const int r = cell / cx;
+  const int cj = r % cy;
+  const int ck = r / cy;
+#pragma unroll
+  for (int a = 0; a < (1 << D); ++a)
+    nodes[a] = node_index(g, ci + (a & 1), cj + ((a >> 1) & 1), D == 3 ? ck + ((a >> 2) & 1) : 0);
+}
+
+__device__ __forceinline__ int num_cells(const Grid& g) {
+  return (g.n[0] - 1) * (g.n[1] - 1) * (g.dim == 3 ? (g.n[2] - 1) : 1);
+}
+
+// one warp per (cell, slice): gather A_c into shared memory [L][2L] = [A_c | I],
+// Gauss-Jordan with partial pivoting (deterministic: largest |a|, lowest row),
+// store A_c^{-1} as Vinv[s][i*L + j][cell] (coalesced across cells in the apply)
+template <int D, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_vanka_setup(Grid g, const double* __restrict__ Ast,
+                                                          double* __restrict__ Vinv, const int* __restrict__ active) {
+  constexpr int L = Cells<D>::L;
+  constexpr int C = Cells<D>::C;
+  constexpr int A = Cells<D>::A;
+  constexpr int W2 = 2 * L;
+  extern __shared__ double smem[];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncell = num_cells(g);
+  const int cell = blockIdx.x * WARPS + warp;
+  if (cell >= ncell) return;  // whole warp exits together
+  double* M = smem + (size_t)warp * (L * W2 + L);
+  double* fcol = M + L * W2;
+  int nodes[A];
+  cell_nodes<D>(g, cell, nodes);
+  const int np = g.np;
+  const double* As = Ast + (size_t)s * g.noff * C * C * np;
+  for (int idx = lane; idx < L * L; idx += 32) {
+    const int r = idx / L, c = idx % L;
+    const int a = r / C, ca = r % C, b = c / C, cb = c % C;
+    const int di = (b & 1) - (a & 1), dj = ((b >> 1) & 1) - ((a >> 1) & 1);
+    const int dk = D == 3 ? ((b >> 2) & 1) - ((a >> 2) & 1) : 0;
+    const int off = offset_index(di, dj, dk, D);
+    M[r * W2 + c] = As[(((size_t)off * C + ca) * C + cb) * np + nodes[a]];
+    M[r * W2 + L + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  for (int p = 0; p < L; ++p) {
+    double best = -1.0;
+    int bi = p;
+    for (int r = p + lane; r < L; r += 32) {
+      const double v = fabs(M[r * W2 + p]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, best, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    const int piv = __shfl_sync(0xffffffffu, bi, 0);
+    if (piv != p)
+      for (int c = lane; c < W2; c += 32) {
+        const double t = M[p * W2 + c];
+        M[p * W2 + c] = M[piv * W2 + c];
+        M[piv * W2 + c] = t;
+      }
+    __syncwarp();
+    const double d = M[p * W2 + p];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+    __syncwarp();
+    for (int c = lane; c < W2; c += 32) M[p * W2 + c] *= inv;
+    for (int r = lane; r < L; r += 32) fcol[r] = M[r * W2 + p];
+    __syncwarp();
+    for (int r = 0; r < L; ++r) {
+      if (r == p) continue;
+      const double f = fcol[r];
+      if (f == 0.0) continue;
+      for (int c = lane; c < W2; c += 32) M[r * W2 + c] -= f * M[p * W2 + c];
+    }
+    __syncwarp();
+  }
+  double* Vs = Vinv + (size_t)s * L * L * ncell;
+  for (int idx = lane; idx < L * L; idx += 32) {
+    const int r = idx / L, c = idx % L;
+    Vs[(size_t)idx * ncell + cell] = M[r * W2 + L + c];
+  }
+}
+
+// y_c = A_c^{-1} r_c ; thread = (cell, local row); block (CELLS, L)
+template <int D, int CELLS>
+__global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, const double* __restrict__ Vinv,
+                                                                   const double* __restrict__ r,
+                                                                   double* __restrict__ y,
+                                                                   const int* __restrict__ active,
+                                                                   unsigned long long* __restrict__ work) {
+  constexpr int L = Cells<D>::L;
+  constexpr int C = Cells<D>::C;
+  constexpr int A = Cells<D>::A;
+  __shared__ double rc[L][CELLS];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  if (work && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(work, 1ULL);
+  const int ncell = num_cells(g);
+  const int cell = blockIdx.x * CELLS + threadIdx.x;
+  const int row = threadIdx.y;
+  const bool live = cell < ncell;
+  const int np = g.np;
+  if (live) {
+    int nodes[A];
+    cell_nodes<D>(g, cell, nodes);
+    const int a = row / C, ca = row % C;
+    rc[row][threadIdx.x] = r[(size_t)s * C * np + (size_t)ca * np + nodes[a]];
+  }
+  __syncthreads();
+  if (!live) return;
+  const double* Vs = Vinv + (size_t)s * L * L * ncell + (size_t)row * L * ncell + cell;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < L; ++j) acc[j & 3] = fma(__ldg(Vs + (size_t)j * ncell), rc[j][threadIdx.x], acc[j & 3]);
+  y[(size_t)s * L * ncell + (size_t)row * ncell + cell] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// x_out = x_in + omega / count(n) * sum_{cells c containing n} y_c[local(n)]
+// (fixed cell order); thread = (node, comp); block (32, C)
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_gather(Grid g, const double* __restrict__ y,
+                                                                  const double* __restrict__ xin,
+                                                                  double* __restrict__ xout, double omega,
+                                                                  const int* __restrict__ active) {
+  constexpr int C = Cells<D>::C;
+  constexpr int A = Cells<D>::A;
+  constexpr int L = Cells<D>::L;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  if (n >= g.nn) return;
+  const int c = threadIdx.y;
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+  const int cx = g.n[0] - 1, cy = g.n[1] - 1, cz = D == 3 ? g.n[2] - 1 : 1;
+  const int ncell = cx * cy * cz;
+  const double* ys = y + (size_t)s * L * ncell;
+  double acc = 0.0;
+  int cnt = 0;
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+    // node n is local corner a of the cell whose lower corner is n - bits(a)
+    const int ci = i - (a & 1), cj = j - ((a >> 1) & 1), ck = D == 3 ? k - ((a >> 2) & 1) : 0;
+    if (ci < 0 || ci >= cx || cj < 0 || cj >= cy || ck < 0 || ck >= cz) continue;
+    const int cell = (ck * cy + cj) * cx + ci;
+    acc += __ldg(ys + (size_t)(a * C + c) * ncell + cell);
+    ++cnt;
+  }
+  const size_t o = (size_t)s * C * g.np + (size_t)c * g.np + n;
+  const double z = acc / cnt;
+  xout[o] = (FIRST ? 0.0 : xin[o]) + omega * z;
+}
+
+}  // namespace pint

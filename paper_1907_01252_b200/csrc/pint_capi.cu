@@ -43,6 +43,9 @@ struct Level {
   double* xb = nullptr;
   double* res = nullptr;
   double* sol = nullptr;   // coarse-level V-cycle output (l > 0)
+  double* vinv = nullptr;  // Vanka cell inverses [S][L*L][ncell]
+  double* ycell = nullptr; // Vanka cell corrections [S][L][ncell]
+  int ncell = 0;
 };
 
 size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
@@ -53,11 +56,11 @@ struct pint_ctx;
 static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st);
 
 struct GraphKey {
-  int S, j, levels, pre, post, coarse;
+  int S, j, levels, pre, post, coarse, smoother;
   double omega;
   bool operator<(const GraphKey& o) const {
-    return std::tie(S, j, levels, pre, post, coarse, omega) <
-           std::tie(o.S, o.j, o.levels, o.pre, o.post, o.coarse, o.omega);
+    return std::tie(S, j, levels, pre, post, coarse, smoother, omega) <
+           std::tie(o.S, o.j, o.levels, o.pre, o.post, o.coarse, o.smoother, o.omega);
   }
 };
 
@@ -381,7 +384,17 @@ struct Impl {
         Level& F = ctx->lv[l - 1];
         k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, counted(ctx, st)>>>(F.g, L.g, F.A, L.A, mask);
       }
-      k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, mask);
+      const bool last_dense = ctx->dense && nl == (int)ctx->lv.size() && l == nl - 1;
+      if (ko->smoother == 1 && !last_dense) {
+        constexpr int W = D == 2 ? 4 : 2;
+        constexpr int Lc = Cells<D>::L;
+        const size_t smem = (size_t)W * (Lc * 2 * Lc + Lc) * sizeof(double);
+        cudaFuncSetAttribute(k_vanka_setup<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vanka_setup<D, W><<<dim3((L.ncell + W - 1) / W, S), 32 * W, smem, counted(ctx, st)>>>(L.g, L.A, L.vinv,
+                                                                                                mask);
+      } else {
+        k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, mask);
+      }
     }
     if (ctx->dense && nl == (int)ctx->lv.size()) {
       Level& L = ctx->lv[nl - 1];
@@ -395,6 +408,39 @@ struct Impl {
   static void smooth(pint_ctx* ctx, const Level& L, int S, const double* b, const double* xin, double* xout,
                      const int* mask, cudaStream_t st, bool first) {
     const double om = ctx->kopt.omega;
+    if (ctx->kopt.smoother == 1) {
+      constexpr int CELLS = D == 2 ? 16 : 8;
+      const double* r = b;
+      if (!first) {
+        if (wide(L.g.nn, S))
+          k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, xin, b, L.res,
+                                                                                            mask);
+        else
+          k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, xin, b, L.res,
+                                                                                            mask);
+        r = L.res;
+      }
+      const bool prof = ctx->prof && &L == &ctx->lv[0];
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (prof) {
+        e0 = next_event(ctx);
+        e1 = next_event(ctx);
+        cudaEventRecord(e0, st);
+      }
+      k_vanka_cell<D, CELLS><<<dim3((L.ncell + CELLS - 1) / CELLS, S), dim3(CELLS, Cells<D>::L), 0, counted(ctx, st)>>>(
+          L.g, L.vinv, r, L.ycell, mask, prof ? ctx->d_work : nullptr);
+      if (prof) {
+        cudaEventRecord(e1, st);
+        ctx->ev_pairs.emplace_back(e0, e1);
+      }
+      if (first)
+        k_vanka_gather<D, true><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.ycell, nullptr,
+                                                                                              xout, om, mask);
+      else
+        k_vanka_gather<D, false><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.ycell, xin,
+                                                                                               xout, om, mask);
+      return;
+    }
     if (first) {
       k_smooth<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, nullptr,
                                                                                     xout, om, mask, nullptr);
@@ -510,7 +556,7 @@ struct Impl {
       return PINT_OK;
     }
     const GraphKey key{S, j, ctx->prec_levels, ctx->kopt.pre_smooth, ctx->kopt.post_smooth, ctx->kopt.coarse_sweeps,
-                       ctx->kopt.omega};
+                       ctx->kopt.smoother, ctx->kopt.omega};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
       cudaGraph_t graph;
@@ -863,6 +909,13 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
     ALLOC(L.res, (size_t)S * C * np);
     if (l > 0) ALLOC(L.rhs, (size_t)S * C * np);
     if (l > 0) ALLOC(L.sol, (size_t)S * C * np);
+    {
+      int cl2[3] = {L.g.n[0] - 1, L.g.n[1] - 1, ctx->D == 3 ? L.g.n[2] - 1 : 1};
+      L.ncell = cl2[0] * cl2[1] * cl2[2];
+      const size_t Lc = (size_t)(1 << ctx->D) * C;
+      ALLOC(L.vinv, (size_t)S * Lc * Lc * L.ncell);
+      ALLOC(L.ycell, (size_t)S * Lc * L.ncell);
+    }
   }
   const Level& Lc = ctx->lv.back();
   ctx->dense_n = C * Lc.g.nn;
@@ -981,8 +1034,14 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   if (bytes_per_slice_launch) {
     const Grid& g = ctx->lv[0].g;
     const int64_t C = ctx->C;
-    // A (noff C^2) + Dinv (C^2) + b + x_in + x_out (3 C), fp64, per node
-    *bytes_per_slice_launch = (int64_t)g.nn * 8 * ((int64_t)g.noff * C * C + C * C + 3 * C);
+    if (ctx->kopt.smoother == 1) {
+      // k_vanka_cell: cell inverses (L^2) + cell corrections (L) per cell, residual C per node
+      const int64_t Lc = (int64_t)(1 << ctx->D) * C;
+      *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * 8 * (Lc * Lc + Lc) + (int64_t)g.nn * 8 * C;
+    } else {
+      // k_smooth: A (noff C^2) + Dinv (C^2) + b + x_in + x_out (3 C), fp64, per node
+      *bytes_per_slice_launch = (int64_t)g.nn * 8 * ((int64_t)g.noff * C * C + C * C + 3 * C);
+    }
   }
   return PINT_OK;
 }

@@ -79,9 +79,10 @@ class KrylovSettings:
     max_iters: int = 300
     pre_smooth: int = 2
     post_smooth: int = 2
-    omega: float = 0.5
+    omega: float = 0.7
     max_levels: int = 0
     coarse_sweeps: int = 20
+    smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
 
     def __post_init__(self):
         if not 0.0 < self.rtol < 1.0:
@@ -92,10 +93,13 @@ class KrylovSettings:
             raise ValueError("need at least one pre- and post-smoothing sweep")
         if not 0.0 < self.omega <= 1.0:
             raise ValueError("omega must lie in (0, 1]")
+        if self.smoother not in ("vanka", "jacobi"):
+            raise ValueError("smoother must be 'vanka' or 'jacobi'")
 
     def c_struct(self) -> _lib.KrylovOpts:
         return _lib.KrylovOpts(self.rtol, self.atol, self.restart, self.max_iters, self.pre_smooth,
-                               self.post_smooth, self.omega, self.max_levels, self.coarse_sweeps)
+                               self.post_smooth, self.omega, self.max_levels, self.coarse_sweeps,
+                               1 if self.smoother == "vanka" else 0)
 
 
 # one documented setting shared by the GPU path and the CPU oracle
