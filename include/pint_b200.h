@@ -74,6 +74,7 @@ typedef struct pint_krylov_opts {
   int32_t max_levels;    /* 0 = as many as the mesh allows */
   int32_t coarse_sweeps; /* smoothing sweeps when the coarsest level is too big for a dense inverse */
   int32_t smoother;      /* 0 node-block Jacobi, 1 cell-patch Vanka (default) */
+  int32_t precond_reuse; /* 1: rebuild the multigrid hierarchy once per time step (default); 0: every Newton iteration */
 } pint_krylov_opts;
 
 /* ---- lifetime -------------------------------------------------------- */

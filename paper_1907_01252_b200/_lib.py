@@ -78,6 +78,7 @@ class KrylovOpts(ctypes.Structure):
         ("max_levels", ctypes.c_int32),
         ("coarse_sweeps", ctypes.c_int32),
         ("smoother", ctypes.c_int32),
+        ("precond_reuse", ctypes.c_int32),
     ]
 
 

@@ -684,7 +684,7 @@ __global__ void k_axpy_one(double* __restrict__ x, const double* __restrict__ z,
 }  // namespace pint
 
 // ======================================================================
-// Cell-patch (Vanka-type) smoother: every cell's L = 2^d C dofs form a local
+// Cell-patch (Vanka-type) smoother (inverses stored in fp32, applied in fp64): every cell's L = 2^d C dofs form a local
 // saddle-point block A_c (extracted from the block stencil) that is inverted
 // exactly once per setup; one sweep is x += omega W sum_c P_c^T A_c^{-1} P_c r
 // with r = b - A x and W = 1 / (cells sharing the node).  Robust where the
@@ -723,7 +723,7 @@ __device__ __forceinline__ int num_cells(const Grid& g) {
 // store A_c^{-1} as Vinv[s][i*L + j][cell] (coalesced across cells in the apply)
 template <int D, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS) k_vanka_setup(Grid g, const double* __restrict__ Ast,
-                                                          double* __restrict__ Vinv, const int* __restrict__ active) {
+                                                          float* __restrict__ Vinv, const int* __restrict__ active) {
   constexpr int L = Cells<D>::L;
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
@@ -786,16 +786,16 @@ __global__ void __launch_bounds__(32 * WARPS) k_vanka_setup(Grid g, const double
     }
     __syncwarp();
   }
-  double* Vs = Vinv + (size_t)s * L * L * ncell;
+  float* Vs = Vinv + (size_t)s * L * L * ncell;
   for (int idx = lane; idx < L * L; idx += 32) {
     const int r = idx / L, c = idx % L;
-    Vs[(size_t)idx * ncell + cell] = M[r * W2 + L + c];
+    Vs[(size_t)idx * ncell + cell] = (float)M[r * W2 + L + c];
   }
 }
 
 // y_c = A_c^{-1} r_c ; thread = (cell, local row); block (CELLS, L)
 template <int D, int CELLS>
-__global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, const double* __restrict__ Vinv,
+__global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, const float* __restrict__ Vinv,
                                                                    const double* __restrict__ r,
                                                                    double* __restrict__ y,
                                                                    const int* __restrict__ active,
@@ -820,10 +820,11 @@ __global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, cons
   }
   __syncthreads();
   if (!live) return;
-  const double* Vs = Vinv + (size_t)s * L * L * ncell + (size_t)row * L * ncell + cell;
+  const float* Vs = Vinv + (size_t)s * L * L * ncell + (size_t)row * L * ncell + cell;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int j = 0; j < L; ++j) acc[j & 3] = fma(__ldg(Vs + (size_t)j * ncell), rc[j][threadIdx.x], acc[j & 3]);
+  for (int j = 0; j < L; ++j)
+    acc[j & 3] = fma((double)__ldg(Vs + (size_t)j * ncell), rc[j][threadIdx.x], acc[j & 3]);
   y[(size_t)s * L * ncell + (size_t)row * ncell + cell] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 

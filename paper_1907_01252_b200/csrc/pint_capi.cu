@@ -43,7 +43,7 @@ struct Level {
   double* xb = nullptr;
   double* res = nullptr;
   double* sol = nullptr;   // coarse-level V-cycle output (l > 0)
-  double* vinv = nullptr;  // Vanka cell inverses [S][L*L][ncell]
+  float* vinv = nullptr;   // Vanka cell inverses [S][L*L][ncell], fp32 storage (preconditioner only)
   double* ycell = nullptr; // Vanka cell corrections [S][L][ncell]
   int ncell = 0;
 };
@@ -693,7 +693,10 @@ struct Impl {
       if (nrun == 0) break;
       PINT_CHECK(cudaMemcpyAsync(ctx->d_active, running.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
       PINT_TRY(assemble(ctx, S, y, yo, ctx->d_active, st));
-      PINT_TRY(precond_setup(ctx, S, ko, ctx->d_active, st));
+      // the multigrid hierarchy is rebuilt at the first Newton iteration of every
+      // step (or every iteration with precond_reuse = 0) -- per-step policy, so a
+      // slice's preconditioner never depends on the batch
+      if (it == 0 || ko->precond_reuse == 0) PINT_TRY(precond_setup(ctx, S, ko, ctx->d_active, st));
       k_negate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->b, ctx->r, n, ctx->d_active);
       PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, klin.data(), kres.data(), st));
       for (int s = 0; s < S; ++s)
@@ -1037,7 +1040,7 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
     if (ctx->kopt.smoother == 1) {
       // k_vanka_cell: cell inverses (L^2) + cell corrections (L) per cell, residual C per node
       const int64_t Lc = (int64_t)(1 << ctx->D) * C;
-      *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * 8 * (Lc * Lc + Lc) + (int64_t)g.nn * 8 * C;
+      *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * (4 * Lc * Lc + 8 * Lc) + (int64_t)g.nn * 8 * C;
     } else {
       // k_smooth: A (noff C^2) + Dinv (C^2) + b + x_in + x_out (3 C), fp64, per node
       *bytes_per_slice_launch = (int64_t)g.nn * 8 * ((int64_t)g.noff * C * C + C * C + 3 * C);
