@@ -77,9 +77,9 @@ class KrylovSettings:
     atol: float = 1e-300
     restart: int = 30
     max_iters: int = 300
-    pre_smooth: int = 2
-    post_smooth: int = 2
-    omega: float = 0.7
+    pre_smooth: int = 1
+    post_smooth: int = 1
+    omega: float = 0.8
     max_levels: int = 0
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
