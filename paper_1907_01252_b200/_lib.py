@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpint_b200.so")
+LIB_PATH = os.environ.get("PINT_LIB") or os.path.join(_HERE, "libpint_b200.so")
 
 PINT_OK = 0
 PINT_NUMERIC_BREAKDOWN = 1

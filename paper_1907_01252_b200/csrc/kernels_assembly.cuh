@@ -1,12 +1,20 @@
-// K1 residual, K2 Jacobian (colour-ordered element scatter) and the
-// Dirichlet / row-ownership fix-up, batched over slices (grid.z or grid.y).
+// K1 residual, K2 Jacobian (colour-ordered element scatter), K2' J w, and the
+// Dirichlet / row-ownership fix-up, batched over slices.
 //
-// Determinism: elements of one colour share no node, so one launch never has
-// two writers of the same entry; colours run in a fixed order, so every sum
-// has a fixed association order independent of the batch composition.
+// All three element kernels run the pointwise flux of fsi_qfunc.cuh at the
+// 2^d Gauss points (and the outflow face points) of their element; only the
+// scalar type and the seeding differ.  Determinism: elements of one colour
+// share no node, so one launch never has two writers of the same entry;
+// colours run in a fixed order, so every sum has a fixed association order
+// independent of the batch composition.
 #pragma once
 
-#include "fsi_element.cuh"
+#include "fsi_qfunc.cuh"
+
+// resident 128-thread CTAs per SM the element kernels are compiled for
+#ifndef PINT_ELEM_MINB
+#define PINT_ELEM_MINB 4
+#endif
 
 namespace pint {
 
@@ -29,159 +37,231 @@ struct ElemIndex {
 // element (colour, t) -> node list; returns false when t is out of range
 template <int D>
 __device__ __forceinline__ bool colour_element(const MeshDev& m, int colour, int t, ElemIndex<D>& e) {
-  int bx = colour & 1, by = (colour >> 1) & 1, bz = (colour >> 2) & 1;
-  int nex = (m.cells[0] - bx + 1) >> 1;
-  int ney = (m.cells[1] - by + 1) >> 1;
-  int nez = D == 3 ? ((m.cells[2] - bz + 1) >> 1) : 1;
+  const int bx = colour & 1, by = (colour >> 1) & 1, bz = (colour >> 2) & 1;
+  const int nex = (m.cells[0] - bx + 1) >> 1;
+  const int ney = (m.cells[1] - by + 1) >> 1;
+  const int nez = D == 3 ? ((m.cells[2] - bz + 1) >> 1) : 1;
   if (t >= nex * ney * nez) return false;
-  int ex = t % nex;
-  int r = t / nex;
-  int ey = r % ney;
-  int ez = r / ney;
-  int ci = 2 * ex + bx, cj = 2 * ey + by, ck = D == 3 ? 2 * ez + bz : 0;
+  const int ex = t % nex;
+  const int r = t / nex;
+  const int ey = r % ney;
+  const int ez = r / ney;
+  const int ci = 2 * ex + bx, cj = 2 * ey + by, ck = D == 3 ? 2 * ez + bz : 0;
   e.cell = (ck * m.cells[1] + cj) * m.cells[0] + ci;
   e.cflag = m.cell_flags[e.cell];
   e.ext_mask = 0;
 #pragma unroll
   for (int a = 0; a < (1 << D); ++a) {
-    int ax = a & 1, ay = (a >> 1) & 1, az = (a >> 2) & 1;
-    int n = node_index(m.g, ci + ax, cj + ay, D == 3 ? ck + az : 0);
+    const int n = node_index(m.g, ci + (a & 1), cj + ((a >> 1) & 1), D == 3 ? ck + ((a >> 2) & 1) : 0);
     e.node[a] = n;
-    bool allowed = (e.cflag & kCellSolid) || !(m.node_flags[n] & kSolidTouch);
+    const bool allowed = (e.cflag & kCellSolid) || !(m.node_flags[n] & kSolidTouch);
     if (allowed) e.ext_mask |= (1u << a);
   }
   return true;
 }
 
 template <int D>
-struct SrcValue {
-  const double* y;
-  const double* yold;
-  int np;
-  const int* node;
-  __device__ __forceinline__ double yn(int a, int c) const { return __ldg(y + c * np + node[a]); }
-  __device__ __forceinline__ double yo(int a, int c) const { return __ldg(yold + c * np + node[a]); }
-};
+__device__ __forceinline__ void zero_acc(double (&acc)[1 << D][2 * D + 1]) {
+#pragma unroll
+  for (int a = 0; a < (1 << D); ++a)
+#pragma unroll
+    for (int c = 0; c < 2 * D + 1; ++c) acc[a][c] = 0.0;
+}
 
-template <int D>
-struct SrcUnitDir {
-  const double* y;
-  const double* yold;
-  int np;
-  const int* node;
-  int astar, cstar;
-  __device__ __forceinline__ Dual yn(int a, int c) const {
-    return Dual(__ldg(y + c * np + node[a]), (a == astar && c == cstar) ? 1.0 : 0.0);
+// Contribution of ONE quadrature point q (and, on outflow cells, of face
+// point q when q < 2^(d-1)) to the element integral of the CN residual
+// (MODE 0), of J w (MODE 1, w given) or of one Jacobian column (MODE 2, trial
+// function (astar, cstar)).  2^d consecutive lanes own the 2^d points of one
+// element; their partial sums are combined by an xor butterfly, which yields
+// bit-identical totals in every lane (fp addition is commutative), so the
+// result is deterministic and independent of the batch.
+template <int D, int MODE>
+__device__ __forceinline__ void qp_integral(const Phys& ph, const StepScalars& st, const ElemIndex<D>& e, int q,
+                                            const double* __restrict__ y, const double* __restrict__ yo,
+                                            const double* __restrict__ w, int np, int astar, int cstar,
+                                            double (&acc)[1 << D][2 * D + 1], bool& degen) {
+  constexpr int A = 1 << D;
+  const bool solid = e.cflag & kCellSolid;
+  auto gy = [&](int a, int c) { return __ldg(y + c * np + e.node[a]); };
+  auto go = [&](int a, int c) { return __ldg(yo + c * np + e.node[a]); };
+  auto gw = [&](int a, int c) { return __ldg(w + c * np + e.node[a]); };
+  const int npts = ((e.cflag & kCellOutflow) && q < (A >> 1)) ? 2 : 1;
+#pragma unroll 1
+  for (int pt = 0; pt < npts; ++pt) {
+    const bool face = pt == 1;
+    double xi[D], N[A], dN[A][D];
+    gauss_point<D>(q, face, xi);
+    q1_shape<D>(xi, ph.h, N, dN);
+    QFields<D, double> fn, fo;
+    interp<D>(N, dN, gy, fn);
+    interp<D>(N, dN, go, fo);
+    if (!face) {
+      if (MODE == 0) {
+        QFlux<D, double> fx;
+        qflux<D, double>(ph, st, solid, fn, fo, fx, degen);
+        accumulate<D, false>(fx, ph.wq, N, dN, e.ext_mask, acc);
+      } else {
+        QFields<D, Dual> fd;
+        if (MODE == 1) {
+          QFields<D, double> fw;
+          interp<D>(N, dN, gw, fw);
+          seed_fields<D>(fn, fw, fd);
+        } else {
+          seed_basis<D>(fn, cstar, N[astar], dN[astar], fd);
+        }
+        QFlux<D, Dual> fx;
+        bool dg = false;
+        qflux<D, Dual>(ph, st, solid, fd, fo, fx, dg);
+        accumulate<D, true>(fx, ph.wq, N, dN, e.ext_mask, acc);
+      }
+    } else {
+      // do-nothing outflow correction  -< rho nu J F^{-T} grad v^T F^{-T} n , phi >
+      if (MODE == 0) {
+        double B[D];
+        qflux_outflow<D, double>(ph, st, fn, fo, B);
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) acc[a][i] += (-ph.wf) * (B[i] * N[a]);
+      } else {
+        QFields<D, Dual> fd;
+        if (MODE == 1) {
+          QFields<D, double> fw;
+          interp<D>(N, dN, gw, fw);
+          seed_fields<D>(fn, fw, fd);
+        } else {
+          seed_basis<D>(fn, cstar, N[astar], dN[astar], fd);
+        }
+        Dual B[D];
+        qflux_outflow<D, Dual>(ph, st, fd, fo, B);
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) acc[a][i] += (-ph.wf) * (B[i].d * N[a]);
+      }
+    }
   }
-  __device__ __forceinline__ double yo(int a, int c) const { return __ldg(yold + c * np + node[a]); }
-};
+}
 
+// xor-butterfly sum of acc over the 2^d lanes of one element
 template <int D>
-struct SrcVecDir {
-  const double* y;
-  const double* yold;
-  const double* w;
-  int np;
-  const int* node;
-  __device__ __forceinline__ Dual yn(int a, int c) const {
-    return Dual(__ldg(y + c * np + node[a]), __ldg(w + c * np + node[a]));
-  }
-  __device__ __forceinline__ double yo(int a, int c) const { return __ldg(yold + c * np + node[a]); }
-};
+__device__ __forceinline__ void reduce_points(double (&acc)[1 << D][2 * D + 1]) {
+#pragma unroll
+  for (int a = 0; a < (1 << D); ++a)
+#pragma unroll
+    for (int c = 0; c < 2 * D + 1; ++c) {
+      double v = acc[a][c];
+#pragma unroll
+      for (int o = 1; o < (1 << D); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[a][c] = v;
+    }
+}
 
 // ---------------------------------------------------------------- K1 residual
+// thread = (element of the colour, quadrature point); lane q scatters node q
 template <int D>
-__global__ void __launch_bounds__(128) k_residual_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_residual_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                         const double* __restrict__ y, const double* __restrict__ yo,
                                                         double* __restrict__ r, int* __restrict__ degen,
                                                         const int* __restrict__ active, int colour) {
   constexpr int C = 2 * D + 1;
+  constexpr int A = 1 << D;
   const int s = blockIdx.y;
-  if (active && !active[s]) return;
+  if (active && !active[s]) return;  // uniform per block
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = gt & (A - 1);
   ElemIndex<D> e;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!colour_element<D>(m, colour, t, e)) return;
+  const bool valid = colour_element<D>(m, colour, gt / A, e);
   const size_t vs = (size_t)C * m.g.np;
-  SrcValue<D> src{y + s * vs, yo + s * vs, m.g.np, e.node};
-  double R[1 << D][C];
+  double R[A][C];
+  zero_acc<D>(R);
   bool dg = false;
-  fsi_element<D, double>(ph, st[s], e.cflag, e.ext_mask, src, R, dg);
+  if (valid) qp_integral<D, 0>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, m.g.np, 0, 0, R, dg);
+  reduce_points<D>(R);
+  if (!valid) return;
   if (dg) degen[s] = 1;  // benign: every writer stores 1
   double* rs = r + s * vs;
 #pragma unroll
-  for (int a = 0; a < (1 << D); ++a)
+  for (int c = 0; c < C; ++c) {
+    if (c == 2 * D && (e.cflag & kCellSolid)) continue;  // solid cells own no p rows
+    double v = R[0][c];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      if (c == 2 * D && (e.cflag & kCellSolid)) continue;  // solid cells own no p rows
-      double* p = rs + c * m.g.np + e.node[a];
-      *p += R[a][c];
-    }
+    for (int a = 1; a < A; ++a) v = (q == a) ? R[a][c] : v;
+    rs[c * m.g.np + e.node[q]] += v;
+  }
 }
 
 // ---------------------------------------------------------------- K2 Jacobian columns
-// thread = (element of the colour, local column dof); grid (elements, cols, slices)
+// thread = (element of the colour, quadrature point); grid (elements, cols, slices)
 template <int D>
-__global__ void __launch_bounds__(64) k_jacobian_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
-                                                       const double* __restrict__ y, const double* __restrict__ yo,
-                                                       double* __restrict__ J, const int* __restrict__ active,
-                                                       int colour) {
+__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jacobian_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+                                                        const double* __restrict__ y, const double* __restrict__ yo,
+                                                        double* __restrict__ J, const int* __restrict__ active,
+                                                        int colour) {
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   const int s = blockIdx.z;
   if (active && !active[s]) return;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = gt & (A - 1);
   ElemIndex<D> e;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!colour_element<D>(m, colour, t, e)) return;
+  const bool valid = colour_element<D>(m, colour, gt / A, e);
   const int col = blockIdx.y;
   const int astar = col / C, cstar = col % C;
   const int np = m.g.np;
   const size_t vs = (size_t)C * np;
-  SrcUnitDir<D> src{y + s * vs, yo + s * vs, np, e.node, astar, cstar};
-  Dual R[A][C];
+  double K[A][C];
+  zero_acc<D>(K);
   bool dg = false;
-  fsi_element<D, Dual>(ph, st[s], e.cflag, e.ext_mask, src, R, dg);
-  const int noff = m.g.noff;
-  double* Js = J + (size_t)s * noff * C * C * np;
+  if (valid) qp_integral<D, 2>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, np, astar, cstar, K, dg);
+  reduce_points<D>(K);
+  if (!valid) return;
+  double* Js = J + (size_t)s * m.g.noff * C * C * np;
+  const int a = q;  // this lane scatters the rows of local node a
+  const int di = (astar & 1) - (a & 1);
+  const int dj = ((astar >> 1) & 1) - ((a >> 1) & 1);
+  const int dk = D == 3 ? ((astar >> 2) & 1) - ((a >> 2) & 1) : 0;
+  const int off = offset_index(di, dj, dk, D);
 #pragma unroll
-  for (int a = 0; a < A; ++a) {
-    const int di = (astar & 1) - (a & 1);
-    const int dj = ((astar >> 1) & 1) - ((a >> 1) & 1);
-    const int dk = D == 3 ? ((astar >> 2) & 1) - ((a >> 2) & 1) : 0;
-    const int off = offset_index(di, dj, dk, D);
+  for (int c = 0; c < C; ++c) {
+    if (c == 2 * D && (e.cflag & kCellSolid)) continue;
+    double v = K[0][c];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      if (c == 2 * D && (e.cflag & kCellSolid)) continue;
-      double* p = Js + (((size_t)off * C + c) * C + cstar) * np + e.node[a];
-      *p += R[a][c].d;
-    }
+    for (int b = 1; b < A; ++b) v = (a == b) ? K[b][c] : v;
+    Js[(((size_t)off * C + c) * C + cstar) * np + e.node[a]] += v;
   }
 }
 
 // ---------------------------------------------------------------- Jacobian-vector product (matrix-free)
 template <int D>
-__global__ void __launch_bounds__(128) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                    const double* __restrict__ y, const double* __restrict__ yo,
                                                    const double* __restrict__ w, double* __restrict__ out,
                                                    const int* __restrict__ active, int colour) {
   constexpr int C = 2 * D + 1;
+  constexpr int A = 1 << D;
   const int s = blockIdx.y;
   if (active && !active[s]) return;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = gt & (A - 1);
   ElemIndex<D> e;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!colour_element<D>(m, colour, t, e)) return;
+  const bool valid = colour_element<D>(m, colour, gt / A, e);
   const size_t vs = (size_t)C * m.g.np;
-  SrcVecDir<D> src{y + s * vs, yo + s * vs, w + s * vs, m.g.np, e.node};
-  Dual R[1 << D][C];
+  double R[A][C];
+  zero_acc<D>(R);
   bool dg = false;
-  fsi_element<D, Dual>(ph, st[s], e.cflag, e.ext_mask, src, R, dg);
+  if (valid) qp_integral<D, 1>(ph, st[s], e, q, y + s * vs, yo + s * vs, w + s * vs, m.g.np, 0, 0, R, dg);
+  reduce_points<D>(R);
+  if (!valid) return;
   double* os = out + s * vs;
 #pragma unroll
-  for (int a = 0; a < (1 << D); ++a)
+  for (int c = 0; c < C; ++c) {
+    if (c == 2 * D && (e.cflag & kCellSolid)) continue;
+    double v = R[0][c];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      if (c == 2 * D && (e.cflag & kCellSolid)) continue;
-      os[c * m.g.np + e.node[a]] += R[a][c].d;
-    }
+    for (int a = 1; a < A; ++a) v = (q == a) ? R[a][c] : v;
+    os[c * m.g.np + e.node[q]] += v;
+  }
 }
 
 // ---------------------------------------------------------------- fixed rows

@@ -309,7 +309,7 @@ struct Impl {
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_residual_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
+      k_residual_colour<D><<<dim3((ne * (1 << D) + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
                                                                       mask, c);
     }
     k_fix_residual<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, ctx->d_st, y, r, mask);
@@ -342,7 +342,7 @@ struct Impl {
     for (int c = 0; c < A; ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_jacobian_colour<D><<<dim3((ne + 63) / 64, A * C, S), 64, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
+      k_jacobian_colour<D><<<dim3((ne * A + 127) / 128, A * C, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
                                                                          c);
     }
     k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, L0.A, mask);
@@ -357,7 +357,7 @@ struct Impl {
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_jvp_colour<D><<<dim3((ne + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
+      k_jvp_colour<D><<<dim3((ne * (1 << D) + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
     }
     k_fix_jvp<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, w, out, nullptr);
     PINT_LAUNCHED();
@@ -582,7 +582,6 @@ struct Impl {
     const int m = ctx->restart;
     const size_t n = vs(ctx);
     const size_t vstride = (size_t)ctx->maxS * n;
-    const int nblk = ctx->nblk;
     std::vector<int> host_mask(S, 1);
     if (mask) {
       PINT_CHECK(cudaMemcpyAsync(ctx->h_int, mask, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
