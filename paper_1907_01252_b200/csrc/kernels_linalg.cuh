@@ -865,3 +865,121 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_gather(Grid g, const
 }
 
 }  // namespace pint
+
+// ======================================================================
+// Fused GMRES reductions: the last block to finish a slice (atomic ticket)
+// sums that slice's partials in a FIXED order, so the result is the same bits
+// whichever block arrives last and whatever else shares the launch.
+// ======================================================================
+namespace pint {
+
+__device__ __forceinline__ bool last_block_of_slice(unsigned int* counter, unsigned int total) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == total - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// Givens update of column j for one slice (body of k_gmres_givens)
+__device__ __forceinline__ void givens_one(int s, int j, int m, double* H, double* cs, double* sn, double* gv,
+                                           const double* tol, int* gm_active, int* gm_steps, int* its,
+                                           double* resid) {
+  double* h = H + (size_t)s * (m + 1) * m + (size_t)j * (m + 1);
+  double* c = cs + (size_t)s * m;
+  double* sv = sn + (size_t)s * m;
+  double* g = gv + (size_t)s * (m + 1);
+  for (int i = 0; i < j; ++i) {
+    const double t = c[i] * h[i] + sv[i] * h[i + 1];
+    h[i + 1] = -sv[i] * h[i] + c[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double a = h[j], b = h[j + 1];
+  const double r = hypot(a, b);
+  double cj = 1.0, sj = 0.0;
+  if (r != 0.0) { cj = a / r; sj = b / r; }
+  c[j] = cj;
+  sv[j] = sj;
+  h[j] = r;
+  h[j + 1] = 0.0;
+  g[j + 1] = -sj * g[j];
+  g[j] = cj * g[j];
+  gm_steps[s] = j + 1;
+  its[s] += 1;
+  const double res = fabs(g[j + 1]);
+  resid[s] = res;
+  if (res <= tol[s] || b == 0.0 || j + 1 == m) gm_active[s] = 0;
+}
+
+// CGS pass: h[v] = <V_v, w> (mode 0) or h2[v] = <V_v, w>, h[v] += h2[v] (mode 1);
+// grid (nblk, nv, S)
+__global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __restrict__ V, size_t vstride,
+                                                           const double* __restrict__ w, int nv, size_t per_slice,
+                                                           double* __restrict__ partial, int nblk, int maxv,
+                                                           double* __restrict__ h, int hstride, int mode,
+                                                           double* __restrict__ h2, int h2stride,
+                                                           unsigned int* __restrict__ counters,
+                                                           const int* __restrict__ active) {
+  __shared__ double sh[kRedThreads / 32];
+  const int s = blockIdx.z;
+  const int v = blockIdx.y;
+  if (active && !active[s]) return;  // uniform per slice: the ticket count stays consistent
+  const size_t base = (size_t)blockIdx.x * kRedChunk;
+  const double* ws = w + s * per_slice;
+  const double* vs = V + v * vstride + s * per_slice;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+    const size_t e = base + i;
+    if (e < per_slice) acc += vs[e] * ws[e];
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
+  if (!last_block_of_slice(counters + s, (unsigned)(nblk * nv))) return;
+  for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + ((size_t)s * maxv + vv) * nblk + b);
+    if (mode == 0) {
+      h[(size_t)s * hstride + vv] = t;
+    } else {
+      h2[(size_t)s * h2stride + vv] = t;
+      h[(size_t)s * hstride + vv] += t;
+    }
+  }
+  if (threadIdx.x == 0) counters[s] = 0u;
+}
+
+// h_{j+1,j} = ||w|| and the Givens update of column j; grid (nblk, S)
+__global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __restrict__ w, size_t per_slice,
+                                                            double* __restrict__ partial, int nblk, int j, int m,
+                                                            double* __restrict__ H, double* __restrict__ cs,
+                                                            double* __restrict__ sn, double* __restrict__ gv,
+                                                            const double* __restrict__ tol, int* __restrict__ gm_active,
+                                                            int* __restrict__ gm_steps, int* __restrict__ its,
+                                                            double* __restrict__ resid, double* __restrict__ hnorm,
+                                                            unsigned int* __restrict__ counters) {
+  __shared__ double sh[kRedThreads / 32];
+  const int s = blockIdx.y;
+  if (!gm_active[s]) return;
+  const size_t base = (size_t)blockIdx.x * kRedChunk;
+  const double* ws = w + s * per_slice;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+    const size_t e = base + i;
+    if (e < per_slice) acc += ws[e] * ws[e];
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partial[(size_t)s * nblk + blockIdx.x] = acc;
+  if (!last_block_of_slice(counters + s, (unsigned)nblk)) return;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + (size_t)s * nblk + b);
+    H[(size_t)s * (m + 1) * m + (size_t)j * (m + 1) + j + 1] = sqrt(t);
+    hnorm[s] = sqrt(t);  // kept for v_{j+1} = w / h_{j+1,j}: the rotation zeroes H[j+1][j]
+    counters[s] = 0u;
+    givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid);
+  }
+}
+
+}  // namespace pint

@@ -86,6 +86,8 @@ struct pint_ctx {
   double *V = nullptr, *H = nullptr, *gv = nullptr, *cs = nullptr, *sn = nullptr, *ybuf = nullptr, *z = nullptr,
          *w = nullptr, *u = nullptr, *gm_res = nullptr, *gm_tol = nullptr, *gm_beta = nullptr;
   int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
+  double* gm_hnorm = nullptr;
+  unsigned int *ctr_mdot = nullptr, *ctr_norm = nullptr;  // last-block tickets, reset by the last block
   // reductions / per-slice scalars
   double* partial = nullptr;
   int nblk = 0;
@@ -520,33 +522,27 @@ struct Impl {
     const int m = ctx->restart;
     const size_t n = vs(ctx);
     const size_t vstride = (size_t)ctx->maxS * n;
-    const int nblk = ctx->nblk;
     double* vj = ctx->V + j * vstride;
-    double* vj1 = ctx->V + (j + 1) * vstride;
     // z = M^{-1} v_j ; w = J z
     vcycle(ctx, 0, S, vj, ctx->z, ctx->gm_active, st);
     spmv(ctx, 0, S, ctx->z, ctx->w, ctx->gm_active, st);
-    // CGS2 against v_0..v_j
+    // CGS2 against v_0..v_j (fused partial + last-block reductions)
     double* hcol = ctx->H + (size_t)j * (m + 1);
     const int hstride = (m + 1) * m;
+    const int nblk = ctx->nblk;
     for (int pass = 0; pass < 2; ++pass) {
-      k_mdot_partial<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk,
-                                                           m + 1, ctx->gm_active);
-      k_mdot_final<<<S, 32, 0, counted(ctx, st)>>>(ctx->partial, nblk, j + 1, m + 1, pass == 0 ? hcol : ctx->ybuf,
-                                     pass == 0 ? hstride : (m + 1), 0, S, ctx->gm_active);
+      k_mdot_fused<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(
+          ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
+          ctx->ctr_mdot, ctx->gm_active);
       k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
-                                                pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
-      if (pass == 1) {
-        // h += h2
-        k_add_cols<<<S, 32, 0, counted(ctx, st)>>>(hcol, hstride, ctx->ybuf, m + 1, j + 1, S, ctx->gm_active);
-      }
+                                                             pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
     }
-    // h_{j+1,j} = ||w|| ; v_{j+1} = w / h_{j+1,j}
-    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(ctx->w, ctx->w, n, ctx->partial, nblk, ctx->gm_active);
-    k_norm_to_h<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, hcol, hstride, j + 1, S, ctx->gm_active);
-    k_scale_col<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, hcol, hstride, j + 1, n, ctx->gm_active);
-    k_gmres_givens<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol,
-                                                   ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, S);
+    // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
+    k_norm_givens<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(
+        ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
+        ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
+    double* vj1 = ctx->V + (j + 1) * vstride;
+    k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
   static int run_arnoldi(pint_ctx* ctx, int S, int j, cudaStream_t st) {
@@ -948,6 +944,9 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->gm_steps, (size_t)S);
   ALLOC(ctx->gm_its, (size_t)S);
   ALLOC(ctx->cyc_active, (size_t)S);
+  ALLOC(ctx->gm_hnorm, (size_t)S);
+  ALLOC(ctx->ctr_mdot, (size_t)S);
+  ALLOC(ctx->ctr_norm, (size_t)S);
   ctx->nblk = (int)((vsz + kRedChunk - 1) / kRedChunk);
   ALLOC(ctx->partial, (size_t)S * (m + 1) * ctx->nblk);
   ALLOC(ctx->d_norms, (size_t)S);
