@@ -74,7 +74,8 @@ typedef struct pint_krylov_opts {
   int32_t max_levels;    /* 0 = as many as the mesh allows */
   int32_t coarse_sweeps; /* smoothing sweeps when the coarsest level is too big for a dense inverse */
   int32_t smoother;      /* 0 node-block Jacobi, 1 cell-patch Vanka (default) */
-  int32_t precond_reuse; /* 1: rebuild the multigrid hierarchy once per time step (default); 0: every Newton iteration */
+  int32_t precond_reuse; /* k >= 1: rebuild a slice's multigrid hierarchy at its first Newton iteration
+                            every k steps; 0: every Newton iteration */
 } pint_krylov_opts;
 
 /* ---- lifetime -------------------------------------------------------- */

@@ -983,3 +983,237 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
 }
 
 }  // namespace pint
+
+// ======================================================================
+// Fused V-cycle tail: the small coarse levels of the hierarchy (a few
+// hundred nodes per slice) are latency-bound when every smoothing / transfer
+// phase is its own launch.  Here ONE CTA per slice runs the whole sub-cycle
+// from level `first` down to the coarsest and back, with __syncthreads()
+// between phases: same arithmetic (same per-row sums in the same order as
+// the standalone kernels), ~15 launches per V-cycle fewer.
+// ======================================================================
+namespace pint {
+
+constexpr int kMaxLevels = 12;
+
+struct LevelDev {
+  Grid g;
+  const double* A;
+  const float* vinv;
+  double* rhs;
+  double* xa;
+  double* xb;
+  double* res;
+  double* sol;
+  double* ycell;
+  int ncell;
+};
+
+struct TailArgs {
+  LevelDev lv[kMaxLevels];
+  int first, last;       // levels handled: first..last (last = coarsest)
+  const double* dense;   // coarsest dense inverse [S][n][2n] (nullptr: smoothing sweeps)
+  int coarse_sweeps;
+  int pre, post;
+  double omega;
+};
+
+template <int D>
+__device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const double* x, const double* b,
+                                                double* out) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int np = L.g.np;
+  const size_t vs = (size_t)C * np;
+  for (int idx = threadIdx.x; idx < L.g.nn * C; idx += blockDim.x) {
+    const int ca = idx / L.g.nn, n = idx % L.g.nn;
+    int nbs[NOFF];
+    stencil_neighbours<D>(L.g, n, nbs);
+    const double* Arow = L.A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
+    const double acc = stencil_row<D, (D == 2 ? 9 : 3)>(Arow, x + s * vs, np, nbs);
+    const size_t o = s * vs + (size_t)ca * np + n;
+    out[o] = b[o] - acc;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const double* r) {
+  constexpr int C = 2 * D + 1;
+  constexpr int A = 1 << D;
+  constexpr int LL = A * C;
+  const int ncell = L.ncell, np = L.g.np;
+  for (int idx = threadIdx.x; idx < ncell * LL; idx += blockDim.x) {
+    const int row = idx / ncell, cell = idx % ncell;
+    int nodes[A];
+    cell_nodes<D>(L.g, cell, nodes);
+    const float* Vs = L.vinv + (size_t)s * LL * LL * ncell + (size_t)row * LL * ncell + cell;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < LL; ++j) {
+      const double rj = r[(size_t)s * C * np + (size_t)(j % C) * np + nodes[j / C]];
+      acc[j & 3] = fma((double)__ldg(Vs + (size_t)j * ncell), rj, acc[j & 3]);
+    }
+    L.ycell[(size_t)s * LL * ncell + (size_t)row * ncell + cell] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tail_vanka_gather(const LevelDev& L, int s, const double* xin, double* xout,
+                                                  double omega, bool first) {
+  constexpr int C = 2 * D + 1;
+  constexpr int A = 1 << D;
+  constexpr int LL = A * C;
+  const int np = L.g.np;
+  const int cx = L.g.n[0] - 1, cy = L.g.n[1] - 1, cz = D == 3 ? L.g.n[2] - 1 : 1;
+  const double* ys = L.ycell + (size_t)s * LL * L.ncell;
+  for (int idx = threadIdx.x; idx < L.g.nn * C; idx += blockDim.x) {
+    const int c = idx / L.g.nn, n = idx % L.g.nn;
+    int i, j, k;
+    node_coords(L.g, n, i, j, k);
+    double acc = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int ci = i - (a & 1), cj = j - ((a >> 1) & 1), ck = D == 3 ? k - ((a >> 2) & 1) : 0;
+      if (ci < 0 || ci >= cx || cj < 0 || cj >= cy || ck < 0 || ck >= cz) continue;
+      acc += ys[(size_t)(a * C + c) * L.ncell + (ck * cy + cj) * cx + ci];
+      ++cnt;
+    }
+    const size_t o = (size_t)s * C * np + (size_t)c * np + n;
+    xout[o] = (first ? 0.0 : xin[o]) + omega * (acc / cnt);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tail_restrict(const LevelDev& F, const LevelDev& Cc, int s) {
+  constexpr int C = 2 * D + 1;
+  const Grid& gf = F.g;
+  const Grid& gc = Cc.g;
+  for (int idx = threadIdx.x; idx < gc.nn * C; idx += blockDim.x) {
+    const int c = idx / gc.nn, I = idx % gc.nn;
+    int ci, cj, ck;
+    node_coords(gc, I, ci, cj, ck);
+    double acc = 0.0;
+    for (int dk = (D == 3 ? -1 : 0); dk <= (D == 3 ? 1 : 0); ++dk)
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int fi = 2 * ci + di, fj = 2 * cj + dj, fk = 2 * ck + dk;
+          if (fi < 0 || fi >= gf.n[0] || fj < 0 || fj >= gf.n[1] || fk < 0 || fk >= gf.n[2]) continue;
+          const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
+          acc += w * F.res[(size_t)s * C * gf.np + (size_t)c * gf.np + node_index(gf, fi, fj, fk)];
+        }
+    Cc.rhs[(size_t)s * C * gc.np + (size_t)c * gc.np + I] = acc;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& Cc, int s, double* xf) {
+  constexpr int C = 2 * D + 1;
+  const Grid& gf = F.g;
+  const Grid& gc = Cc.g;
+  for (int idx = threadIdx.x; idx < gf.nn * C; idx += blockDim.x) {
+    const int c = idx / gf.nn, f = idx % gf.nn;
+    int fi, fj, fk;
+    node_coords(gf, f, fi, fj, fk);
+    double acc = 0.0;
+    const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
+    for (int ck = k0; ck <= (D == 3 ? k0 + (fk & 1) : k0); ++ck)
+      for (int cj = j0; cj <= j0 + (fj & 1); ++cj)
+        for (int ci = i0; ci <= i0 + (fi & 1); ++ci) {
+          const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
+          acc += w * Cc.sol[(size_t)s * C * gc.np + (size_t)c * gc.np + node_index(gc, ci, cj, ck)];
+        }
+    xf[(size_t)s * C * gf.np + (size_t)c * gf.np + f] += acc;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tail_dense(const LevelDev& L, const double* M, int s, const double* b, double* x) {
+  constexpr int C = 2 * D + 1;
+  const int n = C * L.g.nn;
+  const double* Ms = M + (size_t)s * n * 2 * n;
+  const double* bs = b + (size_t)s * C * L.g.np;
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < n; ++c) acc += Ms[(size_t)row * 2 * n + n + c] * bs[(c / L.g.nn) * L.g.np + (c % L.g.nn)];
+    x[(size_t)s * C * L.g.np + (row / L.g.nn) * L.g.np + (row % L.g.nn)] = acc;
+  }
+}
+
+// one Vanka smoothing sweep on level L inside the CTA: xout = xin + omega W sum_c A_c^{-1} (b - A xin)
+template <int D>
+__device__ __forceinline__ void tail_sweep(const LevelDev& L, int s, const double* b, const double* xin, double* xout,
+                                           double omega, bool first) {
+  const double* r = b;
+  if (!first) {
+    tail_spmv_resid<D>(L, s, xin, b, L.res);
+    __syncthreads();
+    r = L.res;
+  }
+  tail_vanka_cell<D>(L, s, r);
+  __syncthreads();
+  tail_vanka_gather<D>(L, s, xin, xout, omega, first);
+  __syncthreads();
+}
+
+// grid.x = S (one CTA per slice); computes x = V-cycle(b) from level a.first down
+template <int D>
+__global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* __restrict__ b_top,
+                                                     double* __restrict__ x_top, const int* __restrict__ active) {
+  const int s = blockIdx.x;
+  if (active && !active[s]) return;
+  const double* bl[kMaxLevels];
+  double* cur[kMaxLevels];
+  double* nxt[kMaxLevels];
+  // ---- down: pre-smooth, residual, restrict
+  for (int l = a.first; l < a.last; ++l) {
+    const LevelDev& L = a.lv[l];
+    bl[l] = (l == a.first) ? b_top : L.rhs;
+    cur[l] = L.xa;
+    nxt[l] = L.xb;
+    tail_sweep<D>(L, s, bl[l], nullptr, cur[l], a.omega, true);
+    for (int i = 1; i < a.pre; ++i) {
+      tail_sweep<D>(L, s, bl[l], cur[l], nxt[l], a.omega, false);
+      double* t = cur[l]; cur[l] = nxt[l]; nxt[l] = t;
+    }
+    tail_spmv_resid<D>(L, s, cur[l], bl[l], L.res);
+    __syncthreads();
+    tail_restrict<D>(L, a.lv[l + 1], s);
+    __syncthreads();
+  }
+  // ---- coarsest
+  {
+    const LevelDev& L = a.lv[a.last];
+    const double* bc = (a.last == a.first) ? b_top : L.rhs;
+    double* xc = (a.last == a.first) ? x_top : L.sol;
+    if (a.dense) {
+      tail_dense<D>(L, a.dense, s, bc, xc);
+      __syncthreads();
+    } else {
+      double* c0 = L.xa;
+      double* c1 = L.xb;
+      const int sw = a.coarse_sweeps < 1 ? 1 : a.coarse_sweeps;
+      tail_sweep<D>(L, s, bc, nullptr, sw == 1 ? xc : c0, a.omega, true);
+      for (int i = 1; i < sw; ++i) {
+        double* o = (i == sw - 1) ? xc : c1;
+        tail_sweep<D>(L, s, bc, c0, o, a.omega, false);
+        double* t = c0; c0 = c1; c1 = t;
+      }
+    }
+  }
+  // ---- up: prolongate, post-smooth (the last sweep writes the level's output)
+  for (int l = a.last - 1; l >= a.first; --l) {
+    const LevelDev& L = a.lv[l];
+    tail_prolong<D>(L, a.lv[l + 1], s, cur[l]);
+    __syncthreads();
+    double* outp = (l == a.first) ? x_top : L.sol;
+    const int post = a.post < 1 ? 1 : a.post;
+    for (int i = 0; i < post; ++i) {
+      double* o = (i == post - 1) ? outp : nxt[l];
+      tail_sweep<D>(L, s, bl[l], cur[l], o, a.omega, false);
+      double* t = cur[l]; cur[l] = nxt[l]; nxt[l] = t;
+    }
+  }
+}
+
+}  // namespace pint

@@ -109,6 +109,10 @@ struct pint_ctx {
   cudaStream_t stream = nullptr;  // internal non-blocking stream (capturable)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
+  bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
+  std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
+  int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
+  TailArgs tail{};
   // profiling (bench.py roofline): launch count and CUDA-event timing of the
   // level-0 smoother sweeps, the dominant kernel of the fine step
   long long launches = 0;
@@ -403,6 +407,26 @@ struct Impl {
       k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
       k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->dense_n, mask);
     }
+    // fused V-cycle tail: from the first level with <= 4096 rows per slice down
+    ctx->tail_first = -1;
+    if (ctx->use_tail && ko->smoother == 1 && nl <= kMaxLevels) {
+      for (int l = 0; l < nl; ++l)
+        if ((size_t)ctx->lv[l].g.nn * C <= 4096) { ctx->tail_first = l; break; }
+      if (ctx->tail_first >= 0) {
+        TailArgs& t = ctx->tail;
+        for (int l = 0; l < nl; ++l) {
+          Level& L = ctx->lv[l];
+          t.lv[l] = LevelDev{L.g, L.A, L.vinv, L.rhs, L.xa, L.xb, L.res, L.sol, L.ycell, L.ncell};
+        }
+        t.first = ctx->tail_first;
+        t.last = nl - 1;
+        t.dense = (ctx->dense && nl == (int)ctx->lv.size()) ? ctx->d_dense : nullptr;
+        t.coarse_sweeps = ko->coarse_sweeps;
+        t.pre = ko->pre_smooth;
+        t.post = ko->post_smooth;
+        t.omega = ko->omega;
+      }
+    }
     PINT_LAUNCHED();
     return PINT_OK;
   }
@@ -472,6 +496,10 @@ struct Impl {
     Level& L = ctx->lv[l];
     const int nl = ctx->prec_levels;
     const pint_krylov_opts& ko = ctx->kopt;
+    if (l == ctx->tail_first) {
+      k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+      return;
+    }
     if (l == nl - 1) {
       if (ctx->dense && nl == (int)ctx->lv.size()) {
         k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense, b, x, mask);
@@ -552,7 +580,7 @@ struct Impl {
       return PINT_OK;
     }
     const GraphKey key{S, j, ctx->prec_levels, ctx->kopt.pre_smooth, ctx->kopt.post_smooth, ctx->kopt.coarse_sweeps,
-                       ctx->kopt.smoother, ctx->kopt.omega};
+                       ctx->kopt.smoother * 100 + ctx->tail_first, ctx->kopt.omega};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
       cudaGraph_t graph;
@@ -665,7 +693,7 @@ struct Impl {
 
   // ---- one shifted-CN step for the slices in `act` (host), Newton per slice
   //      (control flow of linalg.py:207-248)
-  static int newton_step(pint_ctx* ctx, int S, const double* yo, double* y, const std::vector<int>& act,
+  static int newton_step(pint_ctx* ctx, int S, int step, const double* yo, double* y, const std::vector<int>& act,
                          const pint_newton_opts* no, const pint_krylov_opts* ko, std::vector<int>& nit,
                          std::vector<int>& kit, std::vector<int>& status, cudaStream_t st) {
     const size_t n = vs(ctx);
@@ -691,7 +719,24 @@ struct Impl {
       // the multigrid hierarchy is rebuilt at the first Newton iteration of every
       // step (or every iteration with precond_reuse = 0) -- per-step policy, so a
       // slice's preconditioner never depends on the batch
-      if (it == 0 || ko->precond_reuse == 0) PINT_TRY(precond_setup(ctx, S, ko, ctx->d_active, st));
+      // multigrid hierarchy per slice: rebuilt every Newton iteration
+      // (precond_reuse = 0) or at the first Newton iteration of every
+      // precond_reuse-th step since the slice's last build -- a per-slice rule,
+      // so a slice's preconditioner never depends on the batch
+      {
+        std::vector<int> need(S, 0);
+        int nneed = 0;
+        for (int s = 0; s < S; ++s) {
+          if (!running[s]) continue;
+          const int last = ctx->built_step[s];
+          need[s] = ko->precond_reuse <= 0 || last < 0 || (it == 0 && step - last >= ko->precond_reuse);
+          if (need[s]) { ctx->built_step[s] = step; ++nneed; }
+        }
+        if (nneed) {
+          PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, need.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+          PINT_TRY(precond_setup(ctx, S, ko, ctx->d_mask2, st));
+        }
+      }
       k_negate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->b, ctx->r, n, ctx->d_active);
       PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, klin.data(), kres.data(), st));
       for (int s = 0; s < S; ++s)
@@ -756,6 +801,7 @@ struct Impl {
     PINT_CHECK(cudaMemcpyAsync(ctx->ystate, y_in, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
     std::vector<double> t(t0, t0 + S);
     std::vector<int> nit(S, 0), kit(S, 0), status(S, PINT_OK);
+    ctx->built_step.assign(ctx->maxS, -1);
     std::vector<double> ft(S, 0.0);
     int nmax = 0;
     for (int s = 0; s < S; ++s) nmax = std::max(nmax, nsteps[s]);
@@ -772,7 +818,7 @@ struct Impl {
         act[s] = 1;
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_st, sts.data(), sizeof(StepScalars) * S, cudaMemcpyHostToDevice, st));
-      PINT_TRY(newton_step(ctx, S, ctx->ystate, ctx->ynew, act, no, ko, nit, kit, status, st));
+      PINT_TRY(newton_step(ctx, S, j, ctx->ystate, ctx->ynew, act, no, ko, nit, kit, status, st));
       std::vector<int> ok(S, 0);
       for (int s = 0; s < S; ++s) {
         if (!act[s]) continue;
@@ -847,6 +893,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->restart = restart;
   ctx->verbose = std::getenv("PINT_VERBOSE") && std::getenv("PINT_VERBOSE")[0] == '1';
   ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
+  ctx->use_tail = !(std::getenv("PINT_TAIL") && std::getenv("PINT_TAIL")[0] == '0');
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
