@@ -133,7 +133,6 @@ def cpu_oracle_sample(cfg, slices: int, steps: int, starts=None):
 
 def _ref_worker(args):
     name, slices_idx, steps = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
     from paper_1907_01252_b200.problem import CONFIGS
     cfg = CONFIGS[name]
     rate, dt = cpu_oracle_sample(cfg, len(slices_idx), steps)
@@ -153,7 +152,10 @@ def run_reference(args):
     steps_per = 2
     ctx = mp.get_context("spawn")
     times = []
-    with ctx.Pool(nproc, initializer=os.environ.__setitem__, initargs=("OMP_NUM_THREADS", "1")) as pool:
+    # one BLAS thread per worker process: the workers inherit the environment at spawn
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    with ctx.Pool(nproc) as pool:
         for it in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             pool.map(_ref_worker, [(args.config, [p], steps_per) for p in range(nproc)])
@@ -170,9 +172,9 @@ def run_reference(args):
         "config": {"workload": f"{args.config} fine phase sample", "mesh": list(cfg.problem.cells),
                    "slices": nproc, "fine_steps_per_slice": steps_per},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "port",
-                         "sample": f"{nproc} slices x {steps_per} fine CN steps of {args.config} per step, "
-                                   "one process per slice (oracle/fsi_oracle.py; the reference ships no FSI "
-                                   "propagator, SURVEY §0.1)"},
+                         "sample": f"{nproc} slices x {steps_per} fine CN steps of {args.config} per step from "
+                                   "rest at each window start, one process per slice (oracle/fsi_oracle.py; the "
+                                   "reference ships no FSI propagator, SURVEY §0.1)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

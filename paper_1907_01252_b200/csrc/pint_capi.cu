@@ -407,11 +407,11 @@ struct Impl {
       k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
       k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->dense_n, mask);
     }
-    // fused V-cycle tail: from the first level with <= 4096 rows per slice down
+    // fused V-cycle tail: from the first level with <= 2048 rows per slice down
     ctx->tail_first = -1;
     if (ctx->use_tail && ko->smoother == 1 && nl <= kMaxLevels) {
       for (int l = 0; l < nl; ++l)
-        if ((size_t)ctx->lv[l].g.nn * C <= 4096) { ctx->tail_first = l; break; }
+        if ((size_t)ctx->lv[l].g.nn * C <= 2048) { ctx->tail_first = l; break; }
       if (ctx->tail_first >= 0) {
         TailArgs& t = ctx->tail;
         for (int l = 0; l < nl; ++l) {
