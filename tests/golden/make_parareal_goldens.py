@@ -24,7 +24,7 @@ sys.path.insert(0, os.environ.get("PINT_REF_SRC", "/root/reference/pkg/src"))
 from pintbench.parareal import PararealConfig, run_parareal  # noqa: E402  (reference driver)
 
 from oracle import fsi_oracle as O  # noqa: E402
-from paper_1907_01252_b200.problem import CONFIGS, small_problem  # noqa: E402
+from paper_1907_01252_b200.problem import CONFIGS, channel_3d, small_problem  # noqa: E402
 
 NEWTON = O.OracleNewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
 
@@ -32,6 +32,7 @@ CASES = {
     # name: (problem, t_end, fine step, coarse step, intervals, iterations)
     "c1": (CONFIGS["c1"].problem, 1.0, 0.002, 0.02, 10, 5),
     "small": (small_problem(8, 2), 0.8, 0.01, 0.05, 8, 4),
+    "small3d": (channel_3d(10, 2, 2, name="small3d"), 0.2, 0.01, 0.05, 4, 3),
 }
 
 

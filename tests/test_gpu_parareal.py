@@ -13,13 +13,14 @@ import numpy as np
 import pytest
 
 from fields import field_errors
-from paper_1907_01252_b200.problem import CONFIGS, small_problem
+from paper_1907_01252_b200.problem import CONFIGS, channel_3d, small_problem
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 CASES = {
     "small": (small_problem(8, 2), 0.8, 0.01, 0.05, 8, 4),
     "c1": (CONFIGS["c1"].problem, 1.0, 0.002, 0.02, 10, 5),
+    "small3d": (channel_3d(10, 2, 2, name="small3d"), 0.2, 0.01, 0.05, 4, 3),
 }
 
 
@@ -65,6 +66,10 @@ def _check_against_golden(case, variant, driver):
 @pytest.mark.parametrize("driver", ["device", "batched"])
 def test_small_classic_matches_reference_driver_on_oracle(cuda, driver):
     _check_against_golden("small", "classic", driver)
+
+
+def test_3d_classic_matches_reference_driver_on_oracle(cuda):
+    _check_against_golden("small3d", "classic", "device")
 
 
 def test_c1_classic_matches_reference_driver_on_oracle(cuda):

@@ -56,6 +56,7 @@ def main():
     ap.add_argument("--mem-gb", type=float, default=150.0, help="skip (size, S) whose context exceeds this")
     a = ap.parse_args()
     pk, pk_kind = peak()
+    fp64_tflops = 36.59  # measured DFMA peak on this pool's B200 (tools/fp64_peak.cu, profiles/)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     krylov = KrylovSettings(rtol=1e-30, max_iters=1, restart=1)
     for size in a.sizes:
@@ -90,8 +91,10 @@ def main():
             # (SpMV + inverses + gather) + restriction/prolongation; coarse levels add ~1/3
             lvl0 = (ncell * (400 * 4 + 160) + V) * 2 + (Ablk + 2 * V) * 2 + 4 * V
             res["vcycle"] = (timed(lambda: dev.precond_apply(w, out=out), flush), int(lvl0 * 4 / 3))
+            # one GMRES(1) solve = Arnoldi step (V-cycle + SpMV + CGS2/norm on 2 vectors) + the
+            # right-preconditioned update x = M^{-1}(V y) (second V-cycle) + true-residual SpMV
             res["gmres_iteration"] = (timed(lambda: dev.linear_solve(w, krylov, out=out), flush),
-                                      int(lvl0 * 4 / 3) + 2 * (Ablk + 2 * V) + 12 * V)
+                                      2 * int(lvl0 * 4 / 3) + 2 * (Ablk + 2 * V) + 16 * V)
             line = {"config": "c5", "size": size, "mesh": list(C5_MESHES[size]), "slices": S,
                     "dofs_per_slice": P.num_dofs, "seed": a.seed, "peak_gbs": pk, "peak_kind": pk_kind,
                     "kernels": {}}
