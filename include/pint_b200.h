@@ -65,7 +65,7 @@ typedef struct pint_newton_opts {
   double damping_min;
 } pint_newton_opts;
 
-/* GMRES(restart) right-preconditioned by a geometric V-cycle. */
+/* flexible GMRES(restart) preconditioned by a geometric V-cycle. */
 typedef struct pint_krylov_opts {
   double rtol, atol;
   int32_t restart, max_iters;

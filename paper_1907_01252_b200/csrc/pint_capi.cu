@@ -87,6 +87,7 @@ struct pint_ctx {
          *w = nullptr, *u = nullptr, *gm_res = nullptr, *gm_tol = nullptr, *gm_beta = nullptr;
   int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
   double* gm_hnorm = nullptr;
+  double* Z = nullptr;  // flexible-GMRES preconditioned basis z_j = M^{-1} v_j, [m][S][C][np]
   unsigned int *ctr_mdot = nullptr, *ctr_norm = nullptr;  // last-block tickets, reset by the last block
   // reductions / per-slice scalars
   double* partial = nullptr;
@@ -552,8 +553,10 @@ struct Impl {
     const size_t vstride = (size_t)ctx->maxS * n;
     double* vj = ctx->V + j * vstride;
     // z = M^{-1} v_j ; w = J z
-    vcycle(ctx, 0, S, vj, ctx->z, ctx->gm_active, st);
-    spmv(ctx, 0, S, ctx->z, ctx->w, ctx->gm_active, st);
+    // flexible GMRES: keep z_j = M^{-1} v_j, so the update x += Z y needs no extra V-cycle
+    double* zj = ctx->Z + j * vstride;
+    vcycle(ctx, 0, S, vj, zj, ctx->gm_active, st);
+    spmv(ctx, 0, S, zj, ctx->w, ctx->gm_active, st);
     // CGS2 against v_0..v_j (fused partial + last-block reductions)
     double* hcol = ctx->H + (size_t)j * (m + 1);
     const int hstride = (m + 1) * m;
@@ -661,13 +664,12 @@ struct Impl {
           if (!any) break;
         }
       }
-      // x += M^{-1} (V y)
+      // x += Z y  (flexible GMRES: the preconditioned directions are stored)
       k_gmres_solve<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
                                                     S);
-      k_mcombine<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->u, ctx->V, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
+      k_mcombine<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->u, ctx->Z, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
                                                  ctx->cyc_active);
-      vcycle(ctx, 0, S, ctx->u, ctx->z, ctx->cyc_active, st);
-      k_axpy_one<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, ctx->z, n, ctx->cyc_active);
+      k_axpy_one<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, ctx->u, n, ctx->cyc_active);
       // true residual r = b - J x into ctx->u (reused as cycle start)
       if (wide(ctx->g.nn, S))
         k_spmv<D, true, 3><<<row_grid(ctx->g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
@@ -977,6 +979,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   const int m = restart;
   ALLOC(ctx->V, (size_t)(m + 1) * S * vsz);
   ALLOC(ctx->z, S * vsz);
+  ALLOC(ctx->Z, (size_t)m * S * vsz);
   ALLOC(ctx->w, S * vsz);
   ALLOC(ctx->u, S * vsz);
   ALLOC(ctx->H, (size_t)S * (m + 1) * m);
