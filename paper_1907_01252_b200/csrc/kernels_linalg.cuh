@@ -6,7 +6,11 @@
 // invariance, SURVEY.md §8b Determinism row).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "pint_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pint {
 
@@ -1020,12 +1024,12 @@ struct TailArgs {
 
 template <int D>
 __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const double* x, const double* b,
-                                                double* out) {
+                                                double* out, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int np = L.g.np;
   const size_t vs = (size_t)C * np;
-  for (int idx = threadIdx.x; idx < L.g.nn * C; idx += blockDim.x) {
+  for (int idx = tid; idx < L.g.nn * C; idx += nth) {
     const int ca = idx / L.g.nn, n = idx % L.g.nn;
     int nbs[NOFF];
     stencil_neighbours<D>(L.g, n, nbs);
@@ -1037,12 +1041,12 @@ __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const 
 }
 
 template <int D>
-__device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const double* r) {
+__device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const double* r, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   constexpr int LL = A * C;
   const int ncell = L.ncell, np = L.g.np;
-  for (int idx = threadIdx.x; idx < ncell * LL; idx += blockDim.x) {
+  for (int idx = tid; idx < ncell * LL; idx += nth) {
     const int row = idx / ncell, cell = idx % ncell;
     int nodes[A];
     cell_nodes<D>(L.g, cell, nodes);
@@ -1059,14 +1063,14 @@ __device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const 
 
 template <int D>
 __device__ __forceinline__ void tail_vanka_gather(const LevelDev& L, int s, const double* xin, double* xout,
-                                                  double omega, bool first) {
+                                                  double omega, bool first, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   constexpr int LL = A * C;
   const int np = L.g.np;
   const int cx = L.g.n[0] - 1, cy = L.g.n[1] - 1, cz = D == 3 ? L.g.n[2] - 1 : 1;
   const double* ys = L.ycell + (size_t)s * LL * L.ncell;
-  for (int idx = threadIdx.x; idx < L.g.nn * C; idx += blockDim.x) {
+  for (int idx = tid; idx < L.g.nn * C; idx += nth) {
     const int c = idx / L.g.nn, n = idx % L.g.nn;
     int i, j, k;
     node_coords(L.g, n, i, j, k);
@@ -1085,11 +1089,11 @@ __device__ __forceinline__ void tail_vanka_gather(const LevelDev& L, int s, cons
 }
 
 template <int D>
-__device__ __forceinline__ void tail_restrict(const LevelDev& F, const LevelDev& Cc, int s) {
+__device__ __forceinline__ void tail_restrict(const LevelDev& F, const LevelDev& Cc, int s, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   const Grid& gf = F.g;
   const Grid& gc = Cc.g;
-  for (int idx = threadIdx.x; idx < gc.nn * C; idx += blockDim.x) {
+  for (int idx = tid; idx < gc.nn * C; idx += nth) {
     const int c = idx / gc.nn, I = idx % gc.nn;
     int ci, cj, ck;
     node_coords(gc, I, ci, cj, ck);
@@ -1107,11 +1111,11 @@ __device__ __forceinline__ void tail_restrict(const LevelDev& F, const LevelDev&
 }
 
 template <int D>
-__device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& Cc, int s, double* xf) {
+__device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& Cc, int s, double* xf, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   const Grid& gf = F.g;
   const Grid& gc = Cc.g;
-  for (int idx = threadIdx.x; idx < gf.nn * C; idx += blockDim.x) {
+  for (int idx = tid; idx < gf.nn * C; idx += nth) {
     const int c = idx / gf.nn, f = idx % gf.nn;
     int fi, fj, fk;
     node_coords(gf, f, fi, fj, fk);
@@ -1128,92 +1132,117 @@ __device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& 
 }
 
 template <int D>
-__device__ __forceinline__ void tail_dense(const LevelDev& L, const double* M, int s, const double* b, double* x) {
+__device__ __forceinline__ void tail_dense(const LevelDev& L, const double* M, int s, const double* b, double* x, int tid,
+                                           int nth) {
   constexpr int C = 2 * D + 1;
   const int n = C * L.g.nn;
   const double* Ms = M + (size_t)s * n * 2 * n;
   const double* bs = b + (size_t)s * C * L.g.np;
-  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+  for (int row = tid; row < n; row += nth) {
     double acc = 0.0;
     for (int c = 0; c < n; ++c) acc += Ms[(size_t)row * 2 * n + n + c] * bs[(c / L.g.nn) * L.g.np + (c % L.g.nn)];
     x[(size_t)s * C * L.g.np + (row / L.g.nn) * L.g.np + (row % L.g.nn)] = acc;
   }
 }
 
-// one Vanka smoothing sweep on level L inside the CTA: xout = xin + omega W sum_c A_c^{-1} (b - A xin)
-template <int D>
-__device__ __forceinline__ void tail_sweep(const LevelDev& L, int s, const double* b, const double* xin, double* xout,
-                                           double omega, bool first) {
-  const double* r = b;
-  if (!first) {
-    tail_spmv_resid<D>(L, s, xin, b, L.res);
+// barrier over the CTAs that cooperate on one slice (a thread-block cluster)
+template <int CL>
+__device__ __forceinline__ void tail_sync() {
+  if constexpr (CL == 1) {
     __syncthreads();
-    r = L.res;
+  } else {
+    cg::this_cluster().sync();
   }
-  tail_vanka_cell<D>(L, s, r);
-  __syncthreads();
-  tail_vanka_gather<D>(L, s, xin, xout, omega, first);
-  __syncthreads();
 }
 
-// grid.x = S (one CTA per slice); computes x = V-cycle(b) from level a.first down
-template <int D>
-__global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* __restrict__ b_top,
-                                                     double* __restrict__ x_top, const int* __restrict__ active) {
-  const int s = blockIdx.x;
-  if (active && !active[s]) return;
+// one Vanka smoothing sweep on level L: xout = xin + omega W sum_c A_c^{-1} (b - A xin)
+template <int D, int CL>
+__device__ __forceinline__ void tail_sweep(const LevelDev& L, int s, const double* b, const double* xin, double* xout,
+                                           double omega, bool first, int tid, int nth) {
+  const double* r = b;
+  if (!first) {
+    tail_spmv_resid<D>(L, s, xin, b, L.res, tid, nth);
+    tail_sync<CL>();
+    r = L.res;
+  }
+  tail_vanka_cell<D>(L, s, r, tid, nth);
+  tail_sync<CL>();
+  tail_vanka_gather<D>(L, s, xin, xout, omega, first, tid, nth);
+  tail_sync<CL>();
+}
+
+// x = V-cycle(b) from level a.first down; CL CTAs (one cluster) per slice
+template <int D, int CL>
+__device__ __forceinline__ void vcycle_tail_body(const TailArgs& a, const double* __restrict__ b_top,
+                                                 double* __restrict__ x_top, const int* __restrict__ active) {
+  const int s = blockIdx.x / CL;
+  if (active && !active[s]) return;  // uniform over the cluster
+  const int tid = (blockIdx.x % CL) * blockDim.x + threadIdx.x;
+  const int nth = CL * blockDim.x;
   const double* bl[kMaxLevels];
   double* cur[kMaxLevels];
   double* nxt[kMaxLevels];
-  // ---- down: pre-smooth, residual, restrict
   for (int l = a.first; l < a.last; ++l) {
     const LevelDev& L = a.lv[l];
     bl[l] = (l == a.first) ? b_top : L.rhs;
     cur[l] = L.xa;
     nxt[l] = L.xb;
-    tail_sweep<D>(L, s, bl[l], nullptr, cur[l], a.omega, true);
+    tail_sweep<D, CL>(L, s, bl[l], nullptr, cur[l], a.omega, true, tid, nth);
     for (int i = 1; i < a.pre; ++i) {
-      tail_sweep<D>(L, s, bl[l], cur[l], nxt[l], a.omega, false);
+      tail_sweep<D, CL>(L, s, bl[l], cur[l], nxt[l], a.omega, false, tid, nth);
       double* t = cur[l]; cur[l] = nxt[l]; nxt[l] = t;
     }
-    tail_spmv_resid<D>(L, s, cur[l], bl[l], L.res);
-    __syncthreads();
-    tail_restrict<D>(L, a.lv[l + 1], s);
-    __syncthreads();
+    tail_spmv_resid<D>(L, s, cur[l], bl[l], L.res, tid, nth);
+    tail_sync<CL>();
+    tail_restrict<D>(L, a.lv[l + 1], s, tid, nth);
+    tail_sync<CL>();
   }
-  // ---- coarsest
   {
     const LevelDev& L = a.lv[a.last];
     const double* bc = (a.last == a.first) ? b_top : L.rhs;
     double* xc = (a.last == a.first) ? x_top : L.sol;
     if (a.dense) {
-      tail_dense<D>(L, a.dense, s, bc, xc);
-      __syncthreads();
+      tail_dense<D>(L, a.dense, s, bc, xc, tid, nth);
+      tail_sync<CL>();
     } else {
       double* c0 = L.xa;
       double* c1 = L.xb;
       const int sw = a.coarse_sweeps < 1 ? 1 : a.coarse_sweeps;
-      tail_sweep<D>(L, s, bc, nullptr, sw == 1 ? xc : c0, a.omega, true);
+      tail_sweep<D, CL>(L, s, bc, nullptr, sw == 1 ? xc : c0, a.omega, true, tid, nth);
       for (int i = 1; i < sw; ++i) {
         double* o = (i == sw - 1) ? xc : c1;
-        tail_sweep<D>(L, s, bc, c0, o, a.omega, false);
+        tail_sweep<D, CL>(L, s, bc, c0, o, a.omega, false, tid, nth);
         double* t = c0; c0 = c1; c1 = t;
       }
     }
   }
-  // ---- up: prolongate, post-smooth (the last sweep writes the level's output)
   for (int l = a.last - 1; l >= a.first; --l) {
     const LevelDev& L = a.lv[l];
-    tail_prolong<D>(L, a.lv[l + 1], s, cur[l]);
-    __syncthreads();
+    tail_prolong<D>(L, a.lv[l + 1], s, cur[l], tid, nth);
+    tail_sync<CL>();
     double* outp = (l == a.first) ? x_top : L.sol;
     const int post = a.post < 1 ? 1 : a.post;
     for (int i = 0; i < post; ++i) {
       double* o = (i == post - 1) ? outp : nxt[l];
-      tail_sweep<D>(L, s, bl[l], cur[l], o, a.omega, false);
+      tail_sweep<D, CL>(L, s, bl[l], cur[l], o, a.omega, false, tid, nth);
       double* t = cur[l]; cur[l] = nxt[l]; nxt[l] = t;
     }
   }
+}
+
+template <int D>
+__global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* __restrict__ b_top,
+                                                     double* __restrict__ x_top, const int* __restrict__ active) {
+  vcycle_tail_body<D, 1>(a, b_top, x_top, active);
+}
+
+// cluster variant: 4 CTAs per slice cooperate through cluster barriers
+constexpr int kTailCluster = 4;
+template <int D>
+__global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(1024)
+    k_vcycle_tail_cl(TailArgs a, const double* __restrict__ b_top, double* __restrict__ x_top,
+                     const int* __restrict__ active) {
+  vcycle_tail_body<D, kTailCluster>(a, b_top, x_top, active);
 }
 
 }  // namespace pint

@@ -113,6 +113,7 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
+  bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a 4-CTA cluster
   TailArgs tail{};
   // profiling (bench.py roofline): launch count and CUDA-event timing of the
   // level-0 smoother sweeps, the dominant kernel of the fine step
@@ -498,7 +499,10 @@ struct Impl {
     const int nl = ctx->prec_levels;
     const pint_krylov_opts& ko = ctx->kopt;
     if (l == ctx->tail_first) {
-      k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+      if (ctx->tail_cluster)
+        k_vcycle_tail_cl<D><<<S * kTailCluster, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+      else
+        k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
       return;
     }
     if (l == nl - 1) {
@@ -896,6 +900,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->verbose = std::getenv("PINT_VERBOSE") && std::getenv("PINT_VERBOSE")[0] == '1';
   ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
   ctx->use_tail = !(std::getenv("PINT_TAIL") && std::getenv("PINT_TAIL")[0] == '0');
+  ctx->tail_cluster = !(std::getenv("PINT_TAIL_CLUSTER") && std::getenv("PINT_TAIL_CLUSTER")[0] == '0');
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
