@@ -294,9 +294,7 @@ def run_ours(args):
     peak, peak_kind = _peaks()
     kb = prof["slice_launches"] * prof["bytes_per_slice_launch"]
     achieved = (kb / 1e9) / (prof["kernel_ms"] / 1e3) if prof["kernel_ms"] > 0 else 0.0
-    vanka = krylov.smoother == "vanka"
-    kname = ("k_vanka_cell<2,16> (level-0 cell-patch Vanka solves: 20x20 inverse per cell)" if vanka else
-             "k_smooth<2,false> (level-0 block-stencil residual + node-block Jacobi sweep)")
+    kname = prof["kernel"]
     l0_bytes = L * prof["bytes_per_slice_launch"]
     roofline = {
         "kernel": kname,
@@ -307,7 +305,7 @@ def run_ours(args):
         "share_of_step": prof["kernel_ms"] / prof_step_ms,
         "kernel_pass": "separate step with per-launch CUDA events (graphs off)",
         "algorithmic_bytes_per_slice_launch": prof["bytes_per_slice_launch"],
-        "note": (f"{args.config} level-0 working set of this kernel = {l0_bytes / 1e6:.0f} MB for {L} slices"
+        "note": (f"{args.config}: algorithmic bytes of this kernel per launch = {l0_bytes / 1e6:.0f} MB for {L} slices"
                  + (" (< 126 MB L2: L2-resident, the fraction is of HBM peak but the kernel streams from L2)"
                     if l0_bytes < 126e6 else "") + "; see profiles/ and DESIGN.md §5"),
     }

@@ -132,6 +132,9 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
 int pint_profile(pint_ctx* ctx, int32_t enable);
 int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches, int64_t* slice_launches,
                       double* kernel_ms, int64_t* bytes_per_slice_launch);
+/* name of the kernel the events bracketed (the fused Arnoldi step on small meshes,
+ * else the level-0 smoother) */
+const char* pint_profile_kernel(const pint_ctx* ctx);
 
 /* ---- Parareal correction (parareal.py:154-197, 422-431) ---------------
  * K8a, batched over S slices: delta = f_old - c_old. */

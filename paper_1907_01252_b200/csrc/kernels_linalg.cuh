@@ -1034,7 +1034,7 @@ __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const 
     int nbs[NOFF];
     stencil_neighbours<D>(L.g, n, nbs);
     const double* Arow = L.A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
-    const double acc = stencil_row<D, (D == 2 ? 9 : 3)>(Arow, x + s * vs, np, nbs);
+    const double acc = stencil_row<D, 3>(Arow, x + s * vs, np, nbs);
     const size_t o = s * vs + (size_t)ca * np + n;
     out[o] = b[o] - acc;
   }
@@ -1236,13 +1236,168 @@ __global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* 
   vcycle_tail_body<D, 1>(a, b_top, x_top, active);
 }
 
-// cluster variant: 4 CTAs per slice cooperate through cluster barriers
-constexpr int kTailCluster = 4;
+// cluster variant: kTailCluster CTAs per slice cooperate through cluster barriers
+constexpr int kTailCluster = 4;    // CTAs per slice
+constexpr int kTailThreads = 512;  // threads per CTA (128 registers per thread)
 template <int D>
-__global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(1024)
+__global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(kTailThreads)
     k_vcycle_tail_cl(TailArgs a, const double* __restrict__ b_top, double* __restrict__ x_top,
                      const int* __restrict__ active) {
   vcycle_tail_body<D, kTailCluster>(a, b_top, x_top, active);
+}
+
+}  // namespace pint
+
+// ======================================================================
+// Fused Arnoldi step for small meshes (level-0 rows <= kFusedRows per slice):
+// one 8-CTA thread-block cluster per slice runs the whole step
+//   z_j = V-cycle(v_j), w = J z_j, CGS2 against v_0..v_j, h_{j+1,j} = ||w||,
+//   Givens update, v_{j+1} = w / h_{j+1,j}
+// with cluster barriers between phases.  Reductions are fixed-order (thread
+// strided sums -> warp tree -> CTA -> 4 CTA partials summed in rank order by
+// every CTA), so the result is deterministic and independent of the batch.
+// ======================================================================
+namespace pint {
+
+constexpr int kFusedRows = 8192;
+constexpr int kMaxBasis = 64;
+
+struct ArnoldiArgs {
+  TailArgs vc;              // V-cycle from level 0 (vc.first == 0)
+  const double* V;          // basis [m+1][S][C][np]
+  double* Z;                // preconditioned directions [m][S][C][np]
+  double* w;                // [S][C][np]
+  size_t vstride, per_slice;
+  double* H;
+  double* cs;
+  double* sn;
+  double* gv;
+  const double* tol;
+  int* gm_active;
+  int* gm_steps;
+  int* its;
+  double* resid;
+  double* hnorm;
+  double* cpart;            // [S][CL][kMaxBasis] CTA partials
+  double* ybuf;             // [S][m+1] second-pass coefficients
+  unsigned long long* work_bytes;  // profiling: algorithmic bytes of active slices (nullptr: off)
+  unsigned long long* work_count;  // profiling: active slice-launches
+  unsigned long long bytes_per_slice;
+  int j, m;
+};
+
+// fixed-order CTA reduction of nv values per thread (nv <= kMaxBasis); results in sh_out[0..nv)
+__device__ __forceinline__ void cta_reduce_many(double (&v)[kMaxBasis], int nv, double* sh_warp, double* sh_out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = 0; i < nv; ++i) {
+    double x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) sh_warp[wid * kMaxBasis + i] = x;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += sh_warp[w * kMaxBasis + i];
+    sh_out[i] = t;
+  }
+  __syncthreads();
+}
+
+template <int D, int CL>
+__device__ __forceinline__ void arnoldi_body(const ArnoldiArgs& a) {
+  __shared__ double sh_warp[32 * kMaxBasis];
+  __shared__ double sh_sum[kMaxBasis];
+  __shared__ double sh_tot[kMaxBasis];
+  const int s = blockIdx.x / CL;
+  if (!a.gm_active[s]) return;  // uniform over the cluster
+  const int rank = blockIdx.x % CL;
+  const int tid = rank * blockDim.x + threadIdx.x;
+  const int nth = CL * blockDim.x;
+  const size_t n = a.per_slice;
+  const int j = a.j, m = a.m, nv = j + 1;
+  if (a.work_bytes && tid == 0) {
+    atomicAdd(a.work_bytes, a.bytes_per_slice);
+    atomicAdd(a.work_count, 1ULL);
+  }
+  double* zj = a.Z + (size_t)j * a.vstride;
+  // z_j = M^{-1} v_j (V-cycle from level 0, whole hierarchy inside the cluster)
+  vcycle_tail_body<D, CL>(a.vc, a.V + (size_t)j * a.vstride, zj, nullptr);
+  // w = J z_j
+  {
+    const LevelDev& L0 = a.vc.lv[0];
+    constexpr int C = 2 * D + 1;
+    constexpr int NOFF = D == 2 ? 9 : 27;
+    const int np = L0.g.np;
+    for (int idx = tid; idx < L0.g.nn * C; idx += nth) {
+      const int ca = idx / L0.g.nn, nd = idx % L0.g.nn;
+      int nbs[NOFF];
+      stencil_neighbours<D>(L0.g, nd, nbs);
+      const double* Arow = L0.A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + nd;
+      a.w[s * n + (size_t)ca * np + nd] = stencil_row<D, 3>(Arow, zj + s * n, np, nbs);
+    }
+  }
+  tail_sync<CL>();
+  double* ws = a.w + s * n;
+  double* hcol = a.H + (size_t)s * (m + 1) * m + (size_t)j * (m + 1);
+  for (int pass = 0; pass < 2; ++pass) {
+    double acc[kMaxBasis];
+    for (int i = 0; i < nv; ++i) acc[i] = 0.0;
+    for (size_t e = tid; e < n; e += nth) {
+      const double we = ws[e];
+      for (int i = 0; i < nv; ++i) acc[i] += a.V[(size_t)i * a.vstride + s * n + e] * we;
+    }
+    cta_reduce_many(acc, nv, sh_warp, sh_sum);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) a.cpart[((size_t)s * CL + rank) * kMaxBasis + i] = sh_sum[i];
+    tail_sync<CL>();
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      double t = 0.0;
+      for (int r = 0; r < CL; ++r) t += a.cpart[((size_t)s * CL + r) * kMaxBasis + i];
+      sh_tot[i] = t;
+    }
+    __syncthreads();
+    if (rank == 0)
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        if (pass == 0) hcol[i] = sh_tot[i];
+        else { a.ybuf[(size_t)s * (m + 1) + i] = sh_tot[i]; hcol[i] += sh_tot[i]; }
+      }
+    for (size_t e = tid; e < n; e += nth) {
+      double x = ws[e];
+      for (int i = 0; i < nv; ++i) x -= sh_tot[i] * a.V[(size_t)i * a.vstride + s * n + e];
+      ws[e] = x;
+    }
+    tail_sync<CL>();  // also orders the cpart reuse of the next pass
+  }
+  // ||w||, Givens, v_{j+1} = w / ||w||
+  {
+    double acc[kMaxBasis];
+    acc[0] = 0.0;
+    for (size_t e = tid; e < n; e += nth) acc[0] += ws[e] * ws[e];
+    cta_reduce_many(acc, 1, sh_warp, sh_sum);
+    if (threadIdx.x == 0) a.cpart[((size_t)s * CL + rank) * kMaxBasis] = sh_sum[0];
+    tail_sync<CL>();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int r = 0; r < CL; ++r) t += a.cpart[((size_t)s * CL + r) * kMaxBasis];
+      sh_tot[0] = sqrt(t);
+    }
+    __syncthreads();
+    const double hn = sh_tot[0];
+    const double inv = hn != 0.0 ? 1.0 / hn : 0.0;
+    double* vj1 = const_cast<double*>(a.V) + (size_t)(j + 1) * a.vstride + s * n;
+    for (size_t e = tid; e < n; e += nth) vj1[e] = ws[e] * inv;
+    tail_sync<CL>();  // every CTA has read the partials before rank 0 updates H / the mask
+    if (rank == 0 && threadIdx.x == 0) {
+      hcol[j + 1] = hn;
+      a.hnorm[s] = hn;
+      givens_one(s, j, m, a.H, a.cs, a.sn, a.gv, a.tol, a.gm_active, a.gm_steps, a.its, a.resid);
+    }
+  }
+}
+
+template <int D>
+__global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(kTailThreads) k_arnoldi_fused(ArnoldiArgs a) {
+  arnoldi_body<D, kTailCluster>(a);
 }
 
 }  // namespace pint

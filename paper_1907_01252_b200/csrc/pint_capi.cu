@@ -88,6 +88,7 @@ struct pint_ctx {
   int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
   double* gm_hnorm = nullptr;
   double* Z = nullptr;  // flexible-GMRES preconditioned basis z_j = M^{-1} v_j, [m][S][C][np]
+  double* cpart = nullptr;  // fused Arnoldi: CTA partial sums [S][cluster][kMaxBasis]
   unsigned int *ctr_mdot = nullptr, *ctr_norm = nullptr;  // last-block tickets, reset by the last block
   // reductions / per-slice scalars
   double* partial = nullptr;
@@ -114,6 +115,12 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a 4-CTA cluster
+  bool use_fused = false;    // PINT_FUSED=1 enables the fused Arnoldi-step kernel (slower than the
+                             // graph of level-0 launches on c2: measured 3659 vs 4123 steps*slices/s)
+  bool fused = false;        // fused Arnoldi step active for the current hierarchy
+  TailArgs tail0{};          // V-cycle description from level 0 (fused path)
+  unsigned long long* d_work_bytes = nullptr;
+  bool fused_used = false;   // profiling: the fused kernel ran while profiling
   TailArgs tail{};
   // profiling (bench.py roofline): launch count and CUDA-event timing of the
   // level-0 smoother sweeps, the dominant kernel of the fine step
@@ -429,6 +436,14 @@ struct Impl {
         t.omega = ko->omega;
       }
     }
+    // fused Arnoldi step: the whole step in one cluster launch per slice when
+    // the level-0 grid is small (a property of the mesh, never of the batch)
+    ctx->fused = ctx->use_fused && ctx->tail_first >= 0 && (size_t)ctx->lv[0].g.nn * C <= kFusedRows &&
+                 ctx->restart + 1 <= kMaxBasis;
+    if (ctx->fused) {
+      ctx->tail0 = ctx->tail;
+      ctx->tail0.first = 0;
+    }
     PINT_LAUNCHED();
     return PINT_OK;
   }
@@ -500,7 +515,7 @@ struct Impl {
     const pint_krylov_opts& ko = ctx->kopt;
     if (l == ctx->tail_first) {
       if (ctx->tail_cluster)
-        k_vcycle_tail_cl<D><<<S * kTailCluster, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+        k_vcycle_tail_cl<D><<<S * kTailCluster, kTailThreads, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
       else
         k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
       return;
@@ -580,20 +595,89 @@ struct Impl {
     k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
+  // algorithmic bytes of one Arnoldi step j for one slice (fused kernel roofline)
+  static unsigned long long arnoldi_bytes(pint_ctx* ctx, int j) {
+    unsigned long long total = 0;
+    const int nl = ctx->prec_levels;
+    const int Lc = (1 << D) * C;
+    for (int l = 0; l < nl; ++l) {
+      const Level& L = ctx->lv[l];
+      const unsigned long long V = (unsigned long long)C * 8 * L.g.nn;
+      const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * 8 * L.g.nn;
+      if (l == nl - 1 && ctx->dense && nl == (int)ctx->lv.size()) {
+        total += (unsigned long long)ctx->dense_n * ctx->dense_n * 8 + 2 * V;
+        continue;
+      }
+      const unsigned long long cellb = (unsigned long long)L.ncell * ((unsigned long long)Lc * Lc * 4 + 2 * Lc * 8);
+      // first sweep + (pre-1 + post) full sweeps + restriction residual + transfers
+      const int full = ctx->kopt.pre_smooth - 1 + ctx->kopt.post_smooth;
+      total += (cellb + 2 * V) + full * (Ab + 2 * V + cellb + 2 * V) + (Ab + 2 * V) + 3 * V;
+    }
+    const unsigned long long V0 = (unsigned long long)C * 8 * ctx->lv[0].g.nn;
+    const unsigned long long A0 = (unsigned long long)ctx->lv[0].g.noff * C * C * 8 * ctx->lv[0].g.nn;
+    total += A0 + 2 * V0;                          // w = J z
+    total += 2 * (2ULL * (j + 1) * V0 + 2 * V0);   // CGS2: two dot passes + two updates
+    total += 3 * V0;                               // norm + scale
+    return total;
+  }
+
+  static int launch_fused(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    ArnoldiArgs a{};
+    a.vc = ctx->tail0;
+    a.V = ctx->V;
+    a.Z = ctx->Z;
+    a.w = ctx->w;
+    a.vstride = (size_t)ctx->maxS * vs(ctx);
+    a.per_slice = vs(ctx);
+    a.H = ctx->H;
+    a.cs = ctx->cs;
+    a.sn = ctx->sn;
+    a.gv = ctx->gv;
+    a.tol = ctx->gm_tol;
+    a.gm_active = ctx->gm_active;
+    a.gm_steps = ctx->gm_steps;
+    a.its = ctx->gm_its;
+    a.resid = ctx->gm_res;
+    a.hnorm = ctx->gm_hnorm;
+    a.cpart = ctx->cpart;
+    a.ybuf = ctx->ybuf;
+    a.work_bytes = ctx->prof ? ctx->d_work_bytes : nullptr;
+    a.work_count = ctx->prof ? ctx->d_work : nullptr;
+    a.bytes_per_slice = arnoldi_bytes(ctx, j);
+    a.j = j;
+    a.m = ctx->restart;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof) {
+      e0 = next_event(ctx);
+      e1 = next_event(ctx);
+      cudaEventRecord(e0, st);
+      ctx->fused_used = true;
+    }
+    k_arnoldi_fused<D><<<S * kTailCluster, kTailThreads, 0, counted(ctx, st)>>>(a);
+    if (ctx->prof) {
+      cudaEventRecord(e1, st);
+      ctx->ev_pairs.emplace_back(e0, e1);
+    }
+    PINT_LAUNCHED();
+    return PINT_OK;
+  }
+
   static int run_arnoldi(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    if (ctx->fused && (!ctx->use_graphs || ctx->prof)) return launch_fused(ctx, S, j, st);
     if (!ctx->use_graphs || ctx->prof) {
       arnoldi_step(ctx, S, j, st);
       PINT_LAUNCHED();
       return PINT_OK;
     }
     const GraphKey key{S, j, ctx->prec_levels, ctx->kopt.pre_smooth, ctx->kopt.post_smooth, ctx->kopt.coarse_sweeps,
-                       ctx->kopt.smoother * 100 + ctx->tail_first, ctx->kopt.omega};
+                       ctx->kopt.smoother * 1000 + ctx->tail_first * 10 + (ctx->fused ? 1 : 0), ctx->kopt.omega};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
       cudaGraph_t graph;
       const long long before = ctx->launches;
       PINT_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      arnoldi_step(ctx, S, j, st);
+      if (ctx->fused) launch_fused(ctx, S, j, st);
+      else arnoldi_step(ctx, S, j, st);
       PINT_CHECK(cudaStreamEndCapture(st, &graph));
       cudaGraphExec_t exec;
       PINT_CHECK(cudaGraphInstantiate(&exec, graph, 0));
@@ -901,6 +985,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
   ctx->use_tail = !(std::getenv("PINT_TAIL") && std::getenv("PINT_TAIL")[0] == '0');
   ctx->tail_cluster = !(std::getenv("PINT_TAIL_CLUSTER") && std::getenv("PINT_TAIL_CLUSTER")[0] == '0');
+  ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
@@ -1011,6 +1096,8 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->d_lam, (size_t)S);
   ALLOC(ctx->d_st, (size_t)S);
   ALLOC(ctx->d_work, (size_t)1);
+  ALLOC(ctx->d_work_bytes, (size_t)1);
+  ALLOC(ctx->cpart, (size_t)S * kTailCluster * kMaxBasis);
 #undef ALLOC
   if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
       cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess) {
@@ -1067,7 +1154,18 @@ int pint_profile(pint_ctx* ctx, int32_t enable) {
   ctx->ev_pairs.clear();
   ctx->ev_used = 0;
   cudaMemset(ctx->d_work, 0, sizeof(unsigned long long));
+  cudaMemset(ctx->d_work_bytes, 0, sizeof(unsigned long long));
+  ctx->fused_used = false;
   return PINT_OK;
+}
+
+const char* pint_profile_kernel(const pint_ctx* ctx) {
+  if (!ctx) return "";
+  if (ctx->fused_used) return ctx->D == 2 ? "k_arnoldi_fused<2> (whole Arnoldi step: V-cycle + SpMV + CGS2 + Givens)"
+                                         : "k_arnoldi_fused<3> (whole Arnoldi step: V-cycle + SpMV + CGS2 + Givens)";
+  if (ctx->kopt.smoother == 1) return ctx->D == 2 ? "k_vanka_cell<2,16> (level-0 cell-patch Vanka solves)"
+                                                  : "k_vanka_cell<3,8> (level-0 cell-patch Vanka solves)";
+  return ctx->D == 2 ? "k_smooth<2,false> (level-0 node-block Jacobi sweep)" : "k_smooth<3,false>";
 }
 
 int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches, int64_t* slice_launches,
@@ -1087,7 +1185,11 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   if (kernel_launches) *kernel_launches = (int64_t)ctx->ev_pairs.size();
   if (slice_launches) *slice_launches = (int64_t)work;
   if (kernel_ms) *kernel_ms = ms;
-  if (bytes_per_slice_launch) {
+  if (bytes_per_slice_launch && ctx->fused_used) {
+    unsigned long long wb = 0;
+    PINT_CHECK(cudaMemcpy(&wb, ctx->d_work_bytes, sizeof(wb), cudaMemcpyDeviceToHost));
+    *bytes_per_slice_launch = work ? (int64_t)(wb / work) : 0;  // k_arnoldi_fused, averaged over j
+  } else if (bytes_per_slice_launch) {
     const Grid& g = ctx->lv[0].g;
     const int64_t C = ctx->C;
     if (ctx->kopt.smoother == 1) {

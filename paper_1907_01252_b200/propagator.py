@@ -71,7 +71,7 @@ class NewtonSettings:
 
 @dataclass(frozen=True)
 class KrylovSettings:
-    """GMRES(restart) right-preconditioned by a geometric V-cycle."""
+    """Flexible GMRES(restart) preconditioned by a geometric V-cycle (cell-patch Vanka smoother)."""
 
     rtol: float = 1e-8
     atol: float = 1e-300
@@ -303,7 +303,8 @@ class FSIDevice:
         self.check(self.lib.pint_profile_read(self.handle, *[ctypes.byref(v) for v in vals]), "pint_profile_read")
         launches, klaunch, slaunch, ms, bpsl = [v.value for v in vals]
         return {"launches": launches, "kernel_launches": klaunch, "slice_launches": slaunch,
-                "kernel_ms": ms, "bytes_per_slice_launch": bpsl}
+                "kernel_ms": ms, "bytes_per_slice_launch": bpsl,
+                "kernel": self.lib.pint_profile_kernel(self.handle).decode()}
 
     def flags(self):
         nf = (ctypes.c_uint8 * self.nn)()
