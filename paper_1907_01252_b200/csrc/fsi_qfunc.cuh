@@ -17,6 +17,8 @@
 //              the whole element (field interpolation is shared).
 #pragma once
 
+#include <type_traits>
+
 #include "pint_common.cuh"
 
 namespace pint {
@@ -121,9 +123,30 @@ PINT_HD void gauss_point(int q, bool face, double (&xi)[D]) {
 }
 
 // ---------------------------------------------------------------- fields and fluxes
-template <int D, typename T>
+// Scalar promotion: double op double -> double, anything with a Dual -> Dual.
+template <class A, class B>
+struct PromoteT {
+  using type = Dual;
+};
+template <>
+struct PromoteT<double, double> {
+  using type = double;
+};
+template <class A, class B>
+using P2 = typename PromoteT<A, B>::type;
+template <class A, class B, class C>
+using P3 = P2<P2<A, B>, C>;
+
+// Fields at a point.  The velocity, deformation and pressure groups carry their
+// own scalar type: a Jacobian column seeds only ONE group with dual numbers,
+// so everything that does not depend on it stays plain double and the compiler
+// drops the dead derivative arithmetic (e.g. a velocity column never
+// differentiates F = I + grad u, its inverse or determinant).
+template <int D, typename TV, typename TU = TV, typename TP = TV>
 struct QFields {
-  T v[D], Gv[D][D], u[D], Gu[D][D], p, gp[D];
+  TV v[D], Gv[D][D];
+  TU u[D], Gu[D][D];
+  TP p, gp[D];
 };
 
 template <int D, typename T>
@@ -164,12 +187,16 @@ __device__ __forceinline__ void interp(const double (&N)[1 << D], const double (
   }
 }
 
-// pointwise CN flux; n = new-state fields (T), o = old-state fields (double)
-template <int D, typename T>
-__device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, bool solid, const QFields<D, T>& n,
-                                      const QFields<D, double>& o, QFlux<D, T>& out, bool& degen) {
+// pointwise CN flux; n = new-state fields, o = old-state fields (double)
+template <int D, typename TV, typename TU, typename TP>
+__device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, bool solid,
+                                      const QFields<D, TV, TU, TP>& n, const QFields<D, double>& o,
+                                      QFlux<D, P3<TV, TU, TP>>& out, bool& degen) {
+  using TVU = P2<TV, TU>;
+  using TVP = P2<TV, TP>;
+  using TA = P3<TV, TU, TP>;
   const double kt = st.kt, ko = st.ko, k = st.k;
-  T Fn[D][D], Fin[D][D];
+  TU Fn[D][D], Fin[D][D];
   double Fo[D][D], Fio[D][D];
 #pragma unroll
   for (int i = 0; i < D; ++i)
@@ -178,25 +205,25 @@ __device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, boo
       Fn[i][j] = n.Gu[i][j] + (i == j ? 1.0 : 0.0);
       Fo[i][j] = o.Gu[i][j] + (i == j ? 1.0 : 0.0);
     }
-  const T Jn = det_inv<D>(Fn, Fin);
+  const TU Jn = det_inv<D>(Fn, Fin);
   const double Jo = det_inv<D>(Fo, Fio);
   if (value_of(Jn) <= 0.0) degen = true;
   if (!solid) {
     // mass / ALE term at n-1/2
-    T Fm[D][D], Fim[D][D];
+    TU Fm[D][D], Fim[D][D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) Fm[i][j] = 0.5 * (Fn[i][j] + Fo[i][j]);
     det_inv<D>(Fm, Fim);
-    const T Jm = 0.5 * (Jn + Jo);
-    T GvFin[D][D];
+    const TU Jm = 0.5 * (Jn + Jo);
+    TVU GvFin[D][D];
     double GvFio[D][D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        T a = n.Gv[i][0] * Fin[0][j];
+        TVU a = n.Gv[i][0] * Fin[0][j];
         double b = o.Gv[i][0] * Fio[0][j];
 #pragma unroll
         for (int m = 1; m < D; ++m) { a = a + n.Gv[i][m] * Fin[m][j]; b += o.Gv[i][m] * Fio[m][j]; }
@@ -205,11 +232,11 @@ __device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, boo
       }
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      T ale = T(0.0), cn = T(0.0);
+      TVU ale = TVU(0.0), cn = TVU(0.0);
       double co = 0.0;
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        T gm = T(0.0);  // (grad v_{n-1/2} F_{n-1/2}^{-1})_{ij}
+        TVU gm = TVU(0.0);  // (grad v_{n-1/2} F_{n-1/2}^{-1})_{ij}
 #pragma unroll
         for (int m = 0; m < D; ++m) gm = gm + (0.5 * (n.Gv[i][m] + o.Gv[i][m])) * Fim[m][j];
         ale = ale + gm * (n.u[j] - o.u[j]);
@@ -223,11 +250,12 @@ __device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, boo
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        T pn_ij = T(0.0), po_ij = T(0.0);
+        TA pn_ij = TA(0.0);
+        TP po_ij = TP(0.0);
 #pragma unroll
         for (int m = 0; m < D; ++m) {
-          T sn = ph.rnu * (GvFin[i][m] + GvFin[m][i]);
-          T so = T(ph.rnu * (GvFio[i][m] + GvFio[m][i]));
+          TA sn = ph.rnu * (GvFin[i][m] + GvFin[m][i]);
+          TP so = TP(ph.rnu * (GvFio[i][m] + GvFio[m][i]));
           if (i == m) { sn = sn - n.p; so = so - n.p; }
           pn_ij = pn_ij + sn * Fin[j][m];
           po_ij = po_ij + so * Fio[j][m];
@@ -235,31 +263,31 @@ __device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, boo
         out.ten[i][j] = kt * (Jn * pn_ij) + ko * (Jo * po_ij);
         out.uten[i][j] = kt * n.Gu[i][j] + ko * o.Gu[i][j];  // harmonic extension
       }
-    T div = GvFin[0][0];
+    TVU div = GvFin[0][0];
 #pragma unroll
     for (int i = 1; i < D; ++i) div = div + GvFin[i][i];
     out.pv = k * (Jn * div);
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       out.pt[j] = (k * st.delta) * n.gp[j];
-      out.uvec[j] = T(0.0);
+      out.uvec[j] = TA(0.0);
     }
   } else {
     // St. Venant-Kirchhoff: F Sigma(E), E = (F^T F - I)/2
-    T En[D][D];
+    TU En[D][D];
     double Eo[D][D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        T sn = Fn[0][i] * Fn[0][j];
+        TU sn = Fn[0][i] * Fn[0][j];
         double so = Fo[0][i] * Fo[0][j];
 #pragma unroll
         for (int m = 1; m < D; ++m) { sn = sn + Fn[m][i] * Fn[m][j]; so += Fo[m][i] * Fo[m][j]; }
         En[i][j] = 0.5 * (sn - (i == j ? 1.0 : 0.0));
         Eo[i][j] = 0.5 * (so - (i == j ? 1.0 : 0.0));
       }
-    T trn = En[0][0];
+    TU trn = En[0][0];
     double tro = Eo[0][0];
 #pragma unroll
     for (int i = 1; i < D; ++i) { trn = trn + En[i][i]; tro += Eo[i][i]; }
@@ -267,34 +295,36 @@ __device__ __forceinline__ void qflux(const Phys& ph, const StepScalars& st, boo
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        T pn = T(0.0);
+        TU pn = TU(0.0);
         double po = 0.0;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
-          T sg = 2.0 * ph.mu * En[m][j];
+          TU sg = 2.0 * ph.mu * En[m][j];
           double sgo = 2.0 * ph.mu * Eo[m][j];
           if (m == j) { sg = sg + ph.lam * trn; sgo += ph.lam * tro; }
           pn = pn + Fn[i][m] * sg;
           po += Fo[i][m] * sgo;
         }
         out.ten[i][j] = kt * pn + ko * po;
-        out.uten[i][j] = T(0.0);
+        out.uten[i][j] = TA(0.0);
       }
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       out.vec[i] = ph.rho_s * (n.v[i] - o.v[i]);
       out.uvec[i] = (n.u[i] - o.u[i]) - kt * n.v[i] - ko * o.v[i];  // kinematic row
-      out.pt[i] = T(0.0);
+      out.pt[i] = TA(0.0);
     }
-    out.pv = T(0.0);
+    out.pv = TA(0.0);
   }
 }
 
 // do-nothing outflow correction at a face point: B_i = kt rnu Jn (Fin^T Gvn^T Fin^T e_x)_i + ko (...)_old
-template <int D, typename T>
-__device__ __forceinline__ void qflux_outflow(const Phys& ph, const StepScalars& st, const QFields<D, T>& n,
-                                              const QFields<D, double>& o, T (&B)[D]) {
-  T Fn[D][D], Fin[D][D];
+template <int D, typename TV, typename TU, typename TP>
+__device__ __forceinline__ void qflux_outflow(const Phys& ph, const StepScalars& st,
+                                              const QFields<D, TV, TU, TP>& n, const QFields<D, double>& o,
+                                              P2<TV, TU> (&B)[D]) {
+  using TVU = P2<TV, TU>;
+  TU Fn[D][D], Fin[D][D];
   double Fo[D][D], Fio[D][D];
 #pragma unroll
   for (int i = 0; i < D; ++i)
@@ -303,11 +333,11 @@ __device__ __forceinline__ void qflux_outflow(const Phys& ph, const StepScalars&
       Fn[i][j] = n.Gu[i][j] + (i == j ? 1.0 : 0.0);
       Fo[i][j] = o.Gu[i][j] + (i == j ? 1.0 : 0.0);
     }
-  const T Jn = det_inv<D>(Fn, Fin);
+  const TU Jn = det_inv<D>(Fn, Fin);
   const double Jo = det_inv<D>(Fo, Fio);
 #pragma unroll
   for (int i = 0; i < D; ++i) {
-    T mn = T(0.0);
+    TVU mn = TVU(0.0);
     double mo = 0.0;
 #pragma unroll
     for (int kk = 0; kk < D; ++kk)
@@ -320,22 +350,55 @@ __device__ __forceinline__ void qflux_outflow(const Phys& ph, const StepScalars&
   }
 }
 
-// dual fields: values from f, derivative = one trial function (N_b, dN_b) in component cb
-template <int D>
+// fields with dual parts in ONE group only: the trial function (N_b, dN_b)
+// of component cb (G = 0 velocity, 1 deformation, 2 pressure group)
+template <int D, int G>
+struct SeedTypes {
+  using TV = std::conditional_t<G == 0, Dual, double>;
+  using TU = std::conditional_t<G == 1, Dual, double>;
+  using TP = std::conditional_t<G == 2, Dual, double>;
+  using F = QFields<D, TV, TU, TP>;
+};
+
+template <int D, int G>
 __device__ __forceinline__ void seed_basis(const QFields<D, double>& f, int cb, double Nb, const double (&dNb)[D],
-                                           QFields<D, Dual>& n) {
+                                           typename SeedTypes<D, G>::F& n) {
 #pragma unroll
   for (int i = 0; i < D; ++i) {
-    n.v[i] = Dual(f.v[i], cb == i ? Nb : 0.0);
-    n.u[i] = Dual(f.u[i], cb == D + i ? Nb : 0.0);
-    n.gp[i] = Dual(f.gp[i], cb == 2 * D ? dNb[i] : 0.0);
+    if constexpr (G == 0) {
+      n.v[i] = Dual(f.v[i], cb == i ? Nb : 0.0);
+    } else {
+      n.v[i] = f.v[i];
+    }
+    if constexpr (G == 1) {
+      n.u[i] = Dual(f.u[i], cb == D + i ? Nb : 0.0);
+    } else {
+      n.u[i] = f.u[i];
+    }
+    if constexpr (G == 2) {
+      n.gp[i] = Dual(f.gp[i], dNb[i]);
+    } else {
+      n.gp[i] = f.gp[i];
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      n.Gv[i][j] = Dual(f.Gv[i][j], cb == i ? dNb[j] : 0.0);
-      n.Gu[i][j] = Dual(f.Gu[i][j], cb == D + i ? dNb[j] : 0.0);
+      if constexpr (G == 0) {
+        n.Gv[i][j] = Dual(f.Gv[i][j], cb == i ? dNb[j] : 0.0);
+      } else {
+        n.Gv[i][j] = f.Gv[i][j];
+      }
+      if constexpr (G == 1) {
+        n.Gu[i][j] = Dual(f.Gu[i][j], cb == D + i ? dNb[j] : 0.0);
+      } else {
+        n.Gu[i][j] = f.Gu[i][j];
+      }
     }
   }
-  n.p = Dual(f.p, cb == 2 * D ? Nb : 0.0);
+  if constexpr (G == 2) {
+    n.p = Dual(f.p, Nb);
+  } else {
+    n.p = f.p;
+  }
 }
 
 // dual fields: values from f, derivatives from the interpolated direction w

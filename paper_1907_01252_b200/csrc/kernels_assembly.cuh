@@ -11,10 +11,12 @@
 
 #include "fsi_qfunc.cuh"
 
-// resident 128-thread CTAs per SM the element kernels are compiled for
-#ifndef PINT_ELEM_MINB
-#define PINT_ELEM_MINB 4
-#endif
+// resident 128-thread CTAs per SM the element kernels are compiled for:
+// 4 in 2-d (128 registers), 2 in 3-d (the 3-d flux needs ~250 registers)
+template <int D>
+struct ElemOcc {
+  static constexpr int value = D == 2 ? 4 : 2;
+};
 
 namespace pint {
 
@@ -75,7 +77,7 @@ __device__ __forceinline__ void zero_acc(double (&acc)[1 << D][2 * D + 1]) {
 // element; their partial sums are combined by an xor butterfly, which yields
 // bit-identical totals in every lane (fp addition is commutative), so the
 // result is deterministic and independent of the batch.
-template <int D, int MODE>
+template <int D, int MODE, int G = 0>
 __device__ __forceinline__ void qp_integral(const Phys& ph, const StepScalars& st, const ElemIndex<D>& e, int q,
                                             const double* __restrict__ y, const double* __restrict__ yo,
                                             const double* __restrict__ w, int np, int astar, int cstar,
@@ -95,45 +97,49 @@ __device__ __forceinline__ void qp_integral(const Phys& ph, const StepScalars& s
     QFields<D, double> fn, fo;
     interp<D>(N, dN, gy, fn);
     interp<D>(N, dN, go, fo);
-    if (!face) {
-      if (MODE == 0) {
+    if (MODE == 0) {
+      if (!face) {
         QFlux<D, double> fx;
-        qflux<D, double>(ph, st, solid, fn, fo, fx, degen);
+        qflux<D, double, double, double>(ph, st, solid, fn, fo, fx, degen);
         accumulate<D, false>(fx, ph.wq, N, dN, e.ext_mask, acc);
       } else {
-        QFields<D, Dual> fd;
-        if (MODE == 1) {
-          QFields<D, double> fw;
-          interp<D>(N, dN, gw, fw);
-          seed_fields<D>(fn, fw, fd);
-        } else {
-          seed_basis<D>(fn, cstar, N[astar], dN[astar], fd);
-        }
-        QFlux<D, Dual> fx;
-        bool dg = false;
-        qflux<D, Dual>(ph, st, solid, fd, fo, fx, dg);
-        accumulate<D, true>(fx, ph.wq, N, dN, e.ext_mask, acc);
-      }
-    } else {
-      // do-nothing outflow correction  -< rho nu J F^{-T} grad v^T F^{-T} n , phi >
-      if (MODE == 0) {
         double B[D];
-        qflux_outflow<D, double>(ph, st, fn, fo, B);
+        qflux_outflow<D, double, double, double>(ph, st, fn, fo, B);
 #pragma unroll
         for (int a = 0; a < A; ++a)
 #pragma unroll
           for (int i = 0; i < D; ++i) acc[a][i] += (-ph.wf) * (B[i] * N[a]);
+      }
+    } else if (MODE == 1) {
+      QFields<D, double> fw;
+      interp<D>(N, dN, gw, fw);
+      QFields<D, Dual> fd;
+      seed_fields<D>(fn, fw, fd);
+      if (!face) {
+        QFlux<D, Dual> fx;
+        bool dg = false;
+        qflux<D, Dual, Dual, Dual>(ph, st, solid, fd, fo, fx, dg);
+        accumulate<D, true>(fx, ph.wq, N, dN, e.ext_mask, acc);
       } else {
-        QFields<D, Dual> fd;
-        if (MODE == 1) {
-          QFields<D, double> fw;
-          interp<D>(N, dN, gw, fw);
-          seed_fields<D>(fn, fw, fd);
-        } else {
-          seed_basis<D>(fn, cstar, N[astar], dN[astar], fd);
-        }
         Dual B[D];
-        qflux_outflow<D, Dual>(ph, st, fd, fo, B);
+        qflux_outflow<D, Dual, Dual, Dual>(ph, st, fd, fo, B);
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) acc[a][i] += (-ph.wf) * (B[i].d * N[a]);
+      }
+    } else {
+      using ST = SeedTypes<D, G>;
+      typename ST::F fd;
+      seed_basis<D, G>(fn, cstar, N[astar], dN[astar], fd);
+      if (!face) {
+        QFlux<D, Dual> fx;
+        bool dg = false;
+        qflux<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, solid, fd, fo, fx, dg);
+        accumulate<D, true>(fx, ph.wq, N, dN, e.ext_mask, acc);
+      } else if constexpr (G != 2) {
+        Dual B[D];
+        qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, fo, B);
 #pragma unroll
         for (int a = 0; a < A; ++a)
 #pragma unroll
@@ -160,7 +166,7 @@ __device__ __forceinline__ void reduce_points(double (&acc)[1 << D][2 * D + 1]) 
 // ---------------------------------------------------------------- K1 residual
 // thread = (element of the colour, quadrature point); lane q scatters node q
 template <int D>
-__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_residual_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+__global__ void __launch_bounds__(128, ElemOcc<D>::value) k_residual_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                         const double* __restrict__ y, const double* __restrict__ yo,
                                                         double* __restrict__ r, int* __restrict__ degen,
                                                         const int* __restrict__ active, int colour) {
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_residual_colour(MeshDev
 // ---------------------------------------------------------------- K2 Jacobian columns
 // thread = (element of the colour, quadrature point); grid (elements, cols, slices)
 template <int D>
-__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jacobian_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+__global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jacobian_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                         const double* __restrict__ y, const double* __restrict__ yo,
                                                         double* __restrict__ J, const int* __restrict__ active,
                                                         int colour) {
@@ -213,7 +219,15 @@ __global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jacobian_colour(MeshDev
   double K[A][C];
   zero_acc<D>(K);
   bool dg = false;
-  if (valid) qp_integral<D, 2>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, np, astar, cstar, K, dg);
+  // the column's component group is uniform over the block (blockIdx.y)
+  if (valid) {
+    if (cstar < D)
+      qp_integral<D, 2, 0>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, np, astar, cstar, K, dg);
+    else if (cstar < 2 * D)
+      qp_integral<D, 2, 1>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, np, astar, cstar, K, dg);
+    else
+      qp_integral<D, 2, 2>(ph, st[s], e, q, y + s * vs, yo + s * vs, nullptr, np, astar, cstar, K, dg);
+  }
   reduce_points<D>(K);
   if (!valid) return;
   double* Js = J + (size_t)s * m.g.noff * C * C * np;
@@ -234,7 +248,7 @@ __global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jacobian_colour(MeshDev
 
 // ---------------------------------------------------------------- Jacobian-vector product (matrix-free)
 template <int D>
-__global__ void __launch_bounds__(128, PINT_ELEM_MINB) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+__global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                    const double* __restrict__ y, const double* __restrict__ yo,
                                                    const double* __restrict__ w, double* __restrict__ out,
                                                    const int* __restrict__ active, int colour) {
