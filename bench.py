@@ -213,7 +213,7 @@ def run_ours(args):
     m_f = cfg.fine_steps_per_window
     newton = NewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
     krylov = KrylovSettings(pre_smooth=args.pre, post_smooth=args.post, omega=args.omega, smoother=args.smoother,
-                            precond_reuse=args.reuse)
+                            precond_reuse=args.reuse, max_levels=args.max_levels)
     dev = FSIDevice(P, max_slices=L, restart=krylov.restart)
     F = make_propagator(P, ThetaSettings(cfg.fine_step, cfg.theta0, newton), krylov=krylov, device=dev)
     C = make_propagator(P, ThetaSettings(cfg.coarse_step, cfg.theta0, newton), krylov=krylov, device=dev)
@@ -353,6 +353,7 @@ def main():
     ap.add_argument("--omega", type=float, default=0.8, help="smoother damping")
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
     ap.add_argument("--reuse", type=int, default=8, help="rebuild the multigrid hierarchy every k steps")
+    ap.add_argument("--max-levels", type=int, default=0, help="multigrid levels used (0: all)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

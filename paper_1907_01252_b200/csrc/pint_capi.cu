@@ -76,8 +76,9 @@ struct pint_ctx {
   uint8_t* d_cell_flags = nullptr;
   double* d_profile = nullptr;
   std::vector<Level> lv;
-  bool dense = false;
-  int dense_n = 0;
+  int dense_n = 0;           // dofs of the coarsest used level (set by precond_setup)
+  int dense_cap = 0;         // largest dense dimension the buffer holds
+  bool coarse_dense = false; // coarsest used level solved by its dense inverse
   double* d_dense = nullptr;
   // Newton
   double *ystate = nullptr, *ynew = nullptr, *r = nullptr, *dx = nullptr, *ytrial = nullptr, *rtrial = nullptr,
@@ -393,13 +394,16 @@ struct Impl {
     if (ko->max_levels > 0) nl = std::min(nl, (int)ko->max_levels);
     ctx->prec_levels = nl;
     ctx->kopt = *ko;
+    // coarsest used level solved with a dense inverse when it fits the buffer
+    ctx->dense_n = C * ctx->lv[nl - 1].g.nn;
+    ctx->coarse_dense = ctx->d_dense != nullptr && ctx->dense_n <= ctx->dense_cap;
     for (int l = 0; l < nl; ++l) {
       Level& L = ctx->lv[l];
       if (l > 0) {
         Level& F = ctx->lv[l - 1];
         k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, counted(ctx, st)>>>(F.g, L.g, F.A, L.A, mask);
       }
-      const bool last_dense = ctx->dense && nl == (int)ctx->lv.size() && l == nl - 1;
+      const bool last_dense = ctx->coarse_dense && l == nl - 1;
       if (ko->smoother == 1 && !last_dense) {
         constexpr int W = D == 2 ? 4 : 2;
         constexpr int Lc = Cells<D>::L;
@@ -411,7 +415,7 @@ struct Impl {
         k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, mask);
       }
     }
-    if (ctx->dense && nl == (int)ctx->lv.size()) {
+    if (ctx->coarse_dense) {
       Level& L = ctx->lv[nl - 1];
       k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
       k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->dense_n, mask);
@@ -429,7 +433,7 @@ struct Impl {
         }
         t.first = ctx->tail_first;
         t.last = nl - 1;
-        t.dense = (ctx->dense && nl == (int)ctx->lv.size()) ? ctx->d_dense : nullptr;
+        t.dense = ctx->coarse_dense ? ctx->d_dense : nullptr;
         t.coarse_sweeps = ko->coarse_sweeps;
         t.pre = ko->pre_smooth;
         t.post = ko->post_smooth;
@@ -521,7 +525,7 @@ struct Impl {
       return;
     }
     if (l == nl - 1) {
-      if (ctx->dense && nl == (int)ctx->lv.size()) {
+      if (ctx->coarse_dense) {
         k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense, b, x, mask);
       } else {
         const int sweeps = std::max(1, (int)ko.coarse_sweeps);
@@ -604,7 +608,7 @@ struct Impl {
       const Level& L = ctx->lv[l];
       const unsigned long long V = (unsigned long long)C * 8 * L.g.nn;
       const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * 8 * L.g.nn;
-      if (l == nl - 1 && ctx->dense && nl == (int)ctx->lv.size()) {
+      if (l == nl - 1 && ctx->coarse_dense) {
         total += (unsigned long long)ctx->dense_n * ctx->dense_n * 8 + 2 * V;
         continue;
       }
@@ -1055,9 +1059,13 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
     }
   }
   const Level& Lc = ctx->lv.back();
-  ctx->dense_n = C * Lc.g.nn;
-  ctx->dense = ctx->dense_n <= kDenseMax;
-  if (ctx->dense) ALLOC(ctx->d_dense, (size_t)S * ctx->dense_n * 2 * ctx->dense_n);
+  // dense buffer sized for the largest level that a max_levels choice could make
+  // the coarsest and that still fits kDenseMax dofs
+  ctx->dense_cap = 0;
+  for (const Level& L : ctx->lv)
+    if (C * L.g.nn <= kDenseMax) ctx->dense_cap = std::max(ctx->dense_cap, C * L.g.nn);
+  if (ctx->dense_cap == 0 && C * Lc.g.nn <= kDenseMax) ctx->dense_cap = C * Lc.g.nn;
+  if (ctx->dense_cap > 0) ALLOC(ctx->d_dense, (size_t)S * ctx->dense_cap * 2 * ctx->dense_cap);
 
   ALLOC(ctx->ystate, S * vsz);
   ALLOC(ctx->ynew, S * vsz);
