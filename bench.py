@@ -213,7 +213,7 @@ def run_ours(args):
     m_f = cfg.fine_steps_per_window
     newton = NewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
     krylov = KrylovSettings(pre_smooth=args.pre, post_smooth=args.post, omega=args.omega, smoother=args.smoother,
-                            precond_reuse=args.reuse, max_levels=args.max_levels)
+                            precond_reuse=args.reuse, max_levels=args.max_levels, rtol_first=args.rtol_first)
     dev = FSIDevice(P, max_slices=L, restart=krylov.restart)
     F = make_propagator(P, ThetaSettings(cfg.fine_step, cfg.theta0, newton), krylov=krylov, device=dev)
     C = make_propagator(P, ThetaSettings(cfg.coarse_step, cfg.theta0, newton), krylov=krylov, device=dev)
@@ -354,6 +354,7 @@ def main():
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
     ap.add_argument("--reuse", type=int, default=8, help="rebuild the multigrid hierarchy every k steps")
     ap.add_argument("--max-levels", type=int, default=0, help="multigrid levels used (0: all)")
+    ap.add_argument("--rtol-first", type=float, default=1e-4, help="GMRES rtol of the first Newton iteration")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -80,6 +80,7 @@ class KrylovOpts(ctypes.Structure):
         ("coarse_sweeps", ctypes.c_int32),
         ("smoother", ctypes.c_int32),
         ("precond_reuse", ctypes.c_int32),
+        ("rtol_first", ctypes.c_double),
     ]
 
 

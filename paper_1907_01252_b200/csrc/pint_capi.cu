@@ -697,6 +697,7 @@ struct Impl {
 
   // ---- GMRES(m), right preconditioned:  J x = b  for slices in mask
   static int gmres(pint_ctx* ctx, int S, const double* b, double* x, const int* mask, const pint_krylov_opts* ko,
+                   const double* rtol_s, const double* atol_s,
                    int* h_its, double* h_res, cudaStream_t st) {
     const int m = ctx->restart;
     const size_t n = vs(ctx);
@@ -715,7 +716,8 @@ struct Impl {
     PINT_CHECK(cudaStreamSynchronize(st));
     for (int s = 0; s < S; ++s) {
       beta[s] = ctx->h_dbl[s];
-      tol[s] = std::max(ko->rtol * beta[s], ko->atol);
+      // per-slice stopping test: ||r|| <= max(rtol_s beta, atol_s) (defaults: the options)
+      tol[s] = std::max((rtol_s ? rtol_s[s] : ko->rtol) * beta[s], atol_s ? atol_s[s] : ko->atol);
     }
     PINT_CHECK(cudaMemcpyAsync(ctx->gm_tol, tol.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
     std::vector<int> its(S, 0);
@@ -832,7 +834,16 @@ struct Impl {
         }
       }
       k_negate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->b, ctx->r, n, ctx->d_active);
-      PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, klin.data(), kres.data(), st));
+      // inexact Newton forcing (per slice): the first Newton iteration of a step only
+      // needs rtol_first (its update error is dominated by the nonlinearity); later
+      // iterations solve to rtol, but never below a tenth of the Newton target
+      std::vector<double> lin_rtol(S), lin_atol(S);
+      for (int s = 0; s < S; ++s) {
+        lin_rtol[s] = (its[s] == 0 && ko->rtol_first > 0.0) ? std::max(ko->rtol, ko->rtol_first) : ko->rtol;
+        lin_atol[s] = std::max(ko->atol, 0.1 * target[s]);
+      }
+      PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, lin_rtol.data(), lin_atol.data(), klin.data(),
+                     kres.data(), st));
       for (int s = 0; s < S; ++s)
         if (running[s]) kit[s] += klin[s];
       if (ctx->verbose)
@@ -1323,7 +1334,7 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
   }
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
-  return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, its, resid, ctx->stream));
+  return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, nullptr, nullptr, its, resid, ctx->stream));
 }
 
 int pint_parareal_precorrect(int32_t S, int32_t C, int32_t nn, int32_t np, const double* f_old,

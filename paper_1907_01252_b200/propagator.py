@@ -84,6 +84,7 @@ class KrylovSettings:
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
     precond_reuse: int = 8      # rebuild a slice's multigrid hierarchy every k steps (0: every Newton iteration)
+    rtol_first: float = 1e-4    # inexact-Newton forcing of the first Newton iteration (0: rtol)
 
     def __post_init__(self):
         if not 0.0 < self.rtol < 1.0:
@@ -100,7 +101,8 @@ class KrylovSettings:
     def c_struct(self) -> _lib.KrylovOpts:
         return _lib.KrylovOpts(self.rtol, self.atol, self.restart, self.max_iters, self.pre_smooth,
                                self.post_smooth, self.omega, self.max_levels, self.coarse_sweeps,
-                               1 if self.smoother == "vanka" else 0, int(self.precond_reuse))
+                               1 if self.smoother == "vanka" else 0, int(self.precond_reuse),
+                               float(self.rtol_first))
 
 
 # one documented setting shared by the GPU path and the CPU oracle

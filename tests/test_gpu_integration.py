@@ -64,7 +64,7 @@ def test_raw_ctypes_stub(cuda):
     rc = lib.pint_propagate(ctx, S, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(out.data_ptr()), t0, t1, n,
                             ctypes.c_double(0.002), ctypes.c_double(1.0),
                             ctypes.byref(NewtonOpts(1e-10, 1e-10, 25, 1 / 64)),
-                            ctypes.byref(KrylovOpts(1e-8, 1e-300, 30, 300, 2, 2, 0.7, 0, 20, 1, 1)),
+                            ctypes.byref(KrylovOpts(1e-8, 1e-300, 30, 300, 1, 1, 0.8, 0, 20, 1, 8, 0.0)),
                             its, kits, status, ft, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert rc == 0 and list(status) == [0] * S and min(its) >= 5
     assert torch.isfinite(out).all() and out.abs().max() > 0
