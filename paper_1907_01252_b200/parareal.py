@@ -522,3 +522,153 @@ def run_parareal_device(C, F, s0: State, t_end: float, cfg: PararealConfig,
             st = [s0.with_values(host[i][l], time=t_grid[l]) for l in range(1, L + 1)]
             trace.boundary_errors.append([e.value for e in boundary_error(st, oracle[1:])])
     return states, trace
+
+
+def run_parareal_device_pipelined(C, F, s0: State, t_end: float, cfg: PararealConfig, chunks: int = 4,
+                                  oracle: Optional[Sequence[State]] = None):
+    """Device-resident Parareal with the fine phase of iteration i+1 overlapping
+    the corrector sweep of iteration i (the pipelined task graph of the
+    reference, parareal.py:241-267, at chunk granularity).
+
+    The L slices split into ``chunks`` contiguous groups; a worker thread
+    launches the batched fine propagation of a group as soon as the corrector
+    has published the group's left boundaries, while the calling thread keeps
+    sweeping.  ``C`` and ``F`` must own DIFFERENT device contexts (each context
+    has its own stream, so the two run concurrently on the GPU; ctypes releases
+    the GIL).  Results equal :func:`run_parareal_device` bitwise (the fine
+    propagator is batch-invariant and every task sees the same inputs).
+    """
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .propagator import _ptr, _stream
+
+    if C.device is F.device:
+        raise ValueError("pipelined device driver needs separate device contexts for C and F")
+    dev = F.device
+    lib = _lib.load()
+    L = cfg.intervals
+    if t_end <= s0.time:
+        raise ValueError("t_end must lie beyond the initial time")
+    window = (t_end - s0.time) / L
+    for prop in (C, F):
+        _split_window(window, prop.step)
+    t_grid = _grid(s0, t_end, L)
+    K = cfg.max_iters
+    Cn, nn, npad = dev.C, dev.nn, dev.np
+    chunks = max(1, min(chunks, L))
+    bounds = [(c * L // chunks, (c + 1) * L // chunks) for c in range(chunks)]
+    t0 = time.perf_counter()
+    X = [dev.empty(L + 1) for _ in range(K + 1)]
+    coarse = [dev.empty(L + 1) for _ in range(K + 1)]
+    fine = [dev.empty(L) for _ in range(K + 1)]
+    first = dev.to_device(s0.values)
+    for i in range(K + 1):
+        X[i][0].copy_(first[0])
+    torch.cuda.synchronize()
+    cond = threading.Condition()
+    published = [0] * (K + 1)          # X[i][0..published[i]] are final
+    fine_done = [[False] * chunks for _ in range(K + 1)]
+    stop = {"at": None, "error": None}
+
+    def cadv(src, l, out):
+        C.advance_device(src[None], [t_grid[l]], [t_grid[l + 1]], out=out[None])
+
+    def fine_worker():
+        try:
+            for i in range(1, K + 1):
+                for c, (lo, hi) in enumerate(bounds):
+                    with cond:
+                        # the chunk's inputs X[i-1][lo..hi-1] must be final
+                        while published[i - 1] < hi - 1 and stop["at"] is None and stop["error"] is None:
+                            cond.wait()
+                        if stop["error"] is not None or (stop["at"] is not None and i > stop["at"]):
+                            return
+                    out = F.advance_device(X[i - 1][lo:hi].contiguous(), t_grid[lo:hi], t_grid[lo + 1:hi + 1])
+                    fine[i][lo:hi].copy_(out)
+                    torch.cuda.synchronize()
+                    with cond:
+                        fine_done[i][c] = True
+                        cond.notify_all()
+        except BaseException as exc:  # noqa: BLE001 -- surfaced by the sweep thread
+            with cond:
+                stop["error"] = exc
+                cond.notify_all()
+
+    try:
+        for l in range(L):
+            cadv(X[0][l], l, X[0][l + 1])
+            coarse[0][l + 1].copy_(X[0][l + 1])
+            torch.cuda.synchronize()
+            with cond:
+                published[0] = l + 1
+                cond.notify_all()
+    except Exception as exc:
+        raise PararealError(f"coarse_init failed at iteration 0: {exc}") from exc
+    init_s = time.perf_counter() - t0
+    worker = threading.Thread(target=fine_worker, daemon=True)
+    worker.start()
+    thetas, corrs, it_s = [], [], []
+    stop_at = None
+    try:
+        for i in range(1, K + 1):
+            th_row, c_row = [], []
+            for l in range(L):
+                c = next(ci for ci, (lo, hi) in enumerate(bounds) if lo <= l < hi)
+                with cond:
+                    while not fine_done[i][c] and stop["error"] is None:
+                        cond.wait()
+                    if stop["error"] is not None:
+                        raise PararealError(f"fine failed at iteration {i}: {stop['error']}") from stop["error"]
+                try:
+                    cadv(X[i][l], l, coarse[i][l + 1])
+                except Exception as exc:
+                    raise PararealError(f"correct failed at iteration {i}, interval {l}: {exc}") from exc
+                th, cr = ctypes.c_double(), ctypes.c_double()
+                rc = lib.pint_parareal_correct_one(
+                    Cn, nn, npad, _ptr(coarse[i][l + 1]), _ptr(fine[i][l]), _ptr(coarse[i - 1][l + 1]),
+                    _ptr(X[i - 1][l + 1]), _ptr(X[i][l + 1]), _VARIANT_CODE[cfg.variant],
+                    float(cfg.theta_clamp[0]), float(cfg.theta_clamp[1]), ctypes.byref(th), ctypes.byref(cr),
+                    _stream())
+                if rc != _lib.PINT_OK:
+                    raise PararealError(f"correct failed at iteration {i}, interval {l}: device error {rc}")
+                th_row.append(th.value)
+                c_row.append(cr.value)
+                with cond:
+                    published[i] = l + 1
+                    cond.notify_all()
+            thetas.append(th_row)
+            corrs.append(c_row)
+            it_s.append(time.perf_counter() - t0)
+            if max(c_row) <= cfg.tol:
+                stop_at = i
+                with cond:
+                    stop["at"] = i
+                    cond.notify_all()
+                break
+    finally:
+        with cond:
+            if stop["at"] is None:
+                stop["at"] = K
+            cond.notify_all()
+        worker.join()
+    n_it = stop_at if stop_at is not None else K
+    host = [dev.to_host(X[i]) for i in range(n_it + 1)]
+    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler=f"device-pipelined[{chunks}]")
+    trace.iterations_run = n_it
+    trace.converged = stop_at is not None
+    trace.theta_values = thetas[:n_it]
+    trace.correction_norms = corrs[:n_it]
+    trace.iterate_values = [[host[i][l].copy() for l in range(L + 1)] for i in range(n_it + 1)]
+    trace.init_seconds = init_s
+    trace.iteration_seconds = it_s[:n_it]
+    trace.total_seconds = time.perf_counter() - t0
+    trace.fine_propagations = L * n_it
+    states = [s0] + [s0.with_values(host[n_it][l], time=t_grid[l]) for l in range(1, L + 1)]
+    if oracle is not None:
+        for i in range(1, n_it + 1):
+            st = [s0.with_values(host[i][l], time=t_grid[l]) for l in range(1, L + 1)]
+            trace.boundary_errors.append([e.value for e in boundary_error(st, oracle[1:])])
+    return states, trace

@@ -150,3 +150,45 @@ def test_k8_correction_kernel_matches_host(cuda):
     d = torch.empty_like(f)
     assert lib.pint_parareal_precorrect(3, C, nn, npad, _ptr(f), _ptr(c), _ptr(d), _stream()) == 0
     assert torch.equal(d, f - c)
+
+
+def test_gpu_experiment_rows(cuda, tmp_path):
+    """Device restatement of the reference run_experiment (cli.py:290-371):
+    discretization rows, per-iteration rows and the speed-up summary row, in
+    the reference wire format."""
+    from paper_1907_01252_b200.problem import RunConfig
+    from paper_1907_01252_b200.report import emit_csv, load_rows, run_experiment_gpu
+    rc = RunConfig(small_problem(8, 2), t_end=0.8, fine_step=0.01, coarse_step=0.05, intervals=8, iterations=4)
+    rows = run_experiment_gpu(rc, variants=("classic",), coarse_steps=[0.05, 0.1])
+    disc = [r for r in rows if r.variant == "discretization"]
+    summ = [r for r in rows if r.speedup_meas is not None]
+    assert len(disc) == 8 and len(summ) == 2
+    assert all(r.t_seq_s > 0 and r.speedup_theory > 0 for r in summ)
+    per_iter = [r for r in rows if r.boundary is not None and r.variant == "classic" and r.K == 0.05]
+    assert len(per_iter) == 4 * 8
+    # exactness frontier visible in the rows: boundary <= iteration matches the sequential solve
+    assert all(r.rel_err <= 1e-12 for r in per_iter if r.boundary <= r.iteration)
+    emit_csv(rows, str(tmp_path / "rows.csv"))
+    assert load_rows(str(tmp_path / "rows.csv")) == rows
+
+
+def test_pipelined_device_driver_equals_device_driver(cuda):
+    """Fine phase of iteration i+1 overlapping the sweep of iteration i
+    (separate contexts / streams) gives the same numbers bitwise."""
+    from paper_1907_01252_b200.parareal import (PararealConfig, run_parareal_device,
+                                                 run_parareal_device_pipelined)
+    from paper_1907_01252_b200.propagator import (FSIDevice, NewtonSettings, ThetaSettings, initial_state,
+                                                  make_propagator)
+    P, t_end, kf, kc, L, K = CASES["small"]
+    nw = NewtonSettings(1e-10, 1e-10)
+    F, C = _props(P, kf, kc, L)
+    s0 = initial_state(P)
+    cfg = PararealConfig(intervals=L, max_iters=3, tol=1e-30)
+    a, ta = run_parareal_device(C, F, s0, t_end, cfg)
+    Fp = make_propagator(P, ThetaSettings(kf, 1.0, nw), device=FSIDevice(P, L))
+    Cp = make_propagator(P, ThetaSettings(kc, 1.0, nw), device=FSIDevice(P, 1))
+    b, tb = run_parareal_device_pipelined(Cp, Fp, s0, t_end, cfg, chunks=3)
+    for l in range(L + 1):
+        assert np.array_equal(a[l].values, b[l].values)
+    assert ta.correction_norms == tb.correction_norms and ta.theta_values == tb.theta_values
+    assert tb.fine_propagations == ta.fine_propagations
