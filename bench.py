@@ -354,7 +354,7 @@ def main():
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
     ap.add_argument("--reuse", type=int, default=8, help="rebuild the multigrid hierarchy every k steps")
     ap.add_argument("--max-levels", type=int, default=0, help="multigrid levels used (0: all)")
-    ap.add_argument("--rtol-first", type=float, default=1e-4, help="GMRES rtol of the first Newton iteration")
+    ap.add_argument("--rtol-first", type=float, default=3e-5, help="GMRES rtol of the first Newton iteration")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

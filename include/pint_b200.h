@@ -55,7 +55,8 @@ typedef struct pint_problem_desc {
   double bar_lo[3], bar_hi[3];
   double rho_f, nu_f, rho_s, mu_s, lambda_s;
   double u_peak, ramp_time;
-  double alpha_p;       /* pressure stabilization: delta = alpha_p / (rho_f (1/k + U/h + nu_f/h^2)) */
+  double alpha_p;       /* pressure stabilization: delta = alpha_p / (rho_f (1/tau + U/h + nu_f/h^2)) */
+  double stab_k;        /* tau: > 0 explicit time scale, 0 = the advective scale h/U (step independent) */
 } pint_problem_desc;
 
 /* NewtonSettings (linalg.py:129-149) minus the FD epsilon (exact Jacobian). */

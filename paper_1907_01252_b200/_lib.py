@@ -55,6 +55,7 @@ class ProblemDesc(ctypes.Structure):
         ("u_peak", ctypes.c_double),
         ("ramp_time", ctypes.c_double),
         ("alpha_p", ctypes.c_double),
+        ("stab_k", ctypes.c_double),
     ]
 
 

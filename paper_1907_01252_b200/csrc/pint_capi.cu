@@ -215,7 +215,9 @@ double delta_value(const pint_problem_desc& d, double k) {
     h2 += h * h;
   }
   const double hk = std::sqrt(h2 / d.dim);
-  return d.alpha_p / (d.rho_f * (1.0 / k + d.u_peak / hk + d.nu_f / (hk * hk)));
+  const double tau = d.stab_k > 0.0 ? d.stab_k : hk / d.u_peak;  // k-independent (see FSIProblem.delta_p)
+  (void)k;
+  return d.alpha_p / (d.rho_f * (1.0 / tau + d.u_peak / hk + d.nu_f / (hk * hk)));
 }
 
 StepScalars make_step(const pint_problem_desc& d, double k, double theta, double t1) {

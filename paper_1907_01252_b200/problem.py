@@ -25,10 +25,10 @@ Shared decisions (DESIGN.md §2 restates them):
   x = Lx is do-nothing with the paper's boundary correction term;
 * inflow ramp s(t) = forcing_s(min(t, 0.5), 0.5) (reference problems.py:214-221);
 * pressure stabilization: PSPG-type Brezzi-Pitkaranta term
-  k delta (grad p, grad xi) in reference coordinates with the transient
-  time scale, delta = alpha_p / (rho_f (1/k + U/h + nu_f/h^2)), so the
-  pressure Schur complement and the stabilization stay balanced for every
-  step size (the coarse and the fine propagator each use their own k);
+  k delta (grad p, grad xi) in reference coordinates, delta = alpha_p /
+  (rho_f (1/tau + U/h + nu_f/h^2)) with the advective time scale tau = h/U:
+  independent of the step, so coarse and fine propagators discretize the
+  same spatial problem;
 * quadrature: tensor 2-point Gauss per direction, 2-point (2-d) / 2x2 (3-d)
   on the outflow face.
 """
@@ -61,6 +61,7 @@ class FSIProblem:
     u_peak: float = 1.0
     ramp_time: float = 0.5
     alpha_p: float = 1.0
+    stab_k: float = 0.0      # stabilization time scale tau; 0 = the advective scale h / U
     name: str = "custom"
 
     def __post_init__(self):
@@ -113,10 +114,18 @@ class FSIProblem:
         """Cell size used by the stabilization: sqrt(mean h_m^2)."""
         return math.sqrt(sum(x * x for x in self.h) / self.dim)
 
-    def delta_p(self, k: float) -> float:
-        """Pressure-stabilization coefficient delta_K for step size k."""
+    def delta_p(self, k: float = 0.0) -> float:
+        """Pressure-stabilization coefficient delta_K.
+
+        delta = alpha_p / (rho_f (1/tau + U/h + nu_f/h^2)) with tau = stab_k, or the
+        advective time scale h/U when stab_k = 0 (default).  Independent of the
+        step size k, so the coarse and the fine propagator discretize the SAME
+        spatial problem (a k-dependent delta made Parareal stagnate at defects
+        ~1 on c1; measured).  ``k`` is accepted for API stability.
+        """
         hk = self.h_k
-        return self.alpha_p / (self.rho_f * (1.0 / k + self.u_peak / hk + self.nu_f / (hk * hk)))
+        tau = self.stab_k if self.stab_k > 0.0 else hk / self.u_peak
+        return self.alpha_p / (self.rho_f * (1.0 / tau + self.u_peak / hk + self.nu_f / (hk * hk)))
 
     @property
     def component_names(self) -> Tuple[str, ...]:

@@ -84,7 +84,7 @@ class KrylovSettings:
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
     precond_reuse: int = 8      # rebuild a slice's multigrid hierarchy every k steps (0: every Newton iteration)
-    rtol_first: float = 1e-4    # inexact-Newton forcing of the first Newton iteration (0: rtol)
+    rtol_first: float = 3e-5    # inexact-Newton forcing of the first Newton iteration (0: rtol)
 
     def __post_init__(self):
         if not 0.0 < self.rtol < 1.0:
@@ -165,7 +165,7 @@ def problem_desc(p: FSIProblem) -> _lib.ProblemDesc:
         d.bar_hi[m] = p.bar_hi[m] if m < p.dim else 0.0
     d.rho_f, d.nu_f, d.rho_s, d.mu_s = p.rho_f, p.nu_f, p.rho_s, p.mu_s
     d.lambda_s = p.lambda_s
-    d.u_peak, d.ramp_time, d.alpha_p = p.u_peak, p.ramp_time, p.alpha_p
+    d.u_peak, d.ramp_time, d.alpha_p, d.stab_k = p.u_peak, p.ramp_time, p.alpha_p, p.stab_k
     return d
 
 
