@@ -82,6 +82,7 @@ typedef struct pint_krylov_opts {
 } pint_krylov_opts;
 
 /* ---- lifetime -------------------------------------------------------- */
+/* restart <= 31 (the CGS kernel keeps one accumulator per basis vector in registers) */
 int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out);
 int pint_destroy(pint_ctx* ctx);
 const char* pint_last_error(const pint_ctx* ctx);

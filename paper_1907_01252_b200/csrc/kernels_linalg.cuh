@@ -918,7 +918,9 @@ __device__ __forceinline__ void givens_one(int s, int j, int m, double* H, doubl
 }
 
 // CGS pass: h[v] = <V_v, w> (mode 0) or h2[v] = <V_v, w>, h[v] += h2[v] (mode 1);
-// grid (nblk, nv, S)
+// grid (nblk, S): each block streams its chunk of w ONCE and of every V_v,
+// keeping one accumulator per basis vector in registers (nv <= kMdotMax).
+constexpr int kMdotMax = 32;
 __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __restrict__ V, size_t vstride,
                                                            const double* __restrict__ w, int nv, size_t per_slice,
                                                            double* __restrict__ partial, int nblk, int maxv,
@@ -926,10 +928,62 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __rest
                                                            double* __restrict__ h2, int h2stride,
                                                            unsigned int* __restrict__ counters,
                                                            const int* __restrict__ active) {
+  __shared__ double sh[kRedThreads / 32][kMdotMax];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;  // uniform per slice: the ticket count stays consistent
+  const size_t base = (size_t)blockIdx.x * kRedChunk;
+  const double* ws = w + s * per_slice;
+  const double* vs = V + s * per_slice;
+  double acc[kMdotMax];
+#pragma unroll
+  for (int v = 0; v < kMdotMax; ++v) acc[v] = 0.0;
+  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
+    const size_t e = base + i;
+    if (e >= per_slice) break;
+    const double we = ws[e];
+#pragma unroll
+    for (int v = 0; v < kMdotMax; ++v)
+      if (v < nv) acc[v] = fma(__ldg(vs + v * vstride + e), we, acc[v]);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < kMdotMax; ++v) {
+    if (v >= nv) break;
+    const double x = warp_sum(acc[v]);
+    if (lane == 0) sh[wid][v] = x;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < kRedThreads / 32; ++q) t += sh[q][v];
+    partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = t;
+  }
+  if (!last_block_of_slice(counters + s, (unsigned)nblk)) return;
+  for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + ((size_t)s * maxv + vv) * nblk + b);
+    if (mode == 0) {
+      h[(size_t)s * hstride + vv] = t;
+    } else {
+      h2[(size_t)s * h2stride + vv] = t;
+      h[(size_t)s * hstride + vv] += t;
+    }
+  }
+  if (threadIdx.x == 0) counters[s] = 0u;
+}
+
+// narrow-grid variant (few chunks per slice): one block per (chunk, basis vector)
+__global__ void __launch_bounds__(kRedThreads) k_mdot_fused_v(const double* __restrict__ V, size_t vstride,
+                                                             const double* __restrict__ w, int nv, size_t per_slice,
+                                                             double* __restrict__ partial, int nblk, int maxv,
+                                                             double* __restrict__ h, int hstride, int mode,
+                                                             double* __restrict__ h2, int h2stride,
+                                                             unsigned int* __restrict__ counters,
+                                                             const int* __restrict__ active) {
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.z;
   const int v = blockIdx.y;
-  if (active && !active[s]) return;  // uniform per slice: the ticket count stays consistent
+  if (active && !active[s]) return;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
   const double* vs = V + v * vstride + s * per_slice;

@@ -587,9 +587,15 @@ struct Impl {
     const int hstride = (m + 1) * m;
     const int nblk = ctx->nblk;
     for (int pass = 0; pass < 2; ++pass) {
-      k_mdot_fused<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(
-          ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
-          ctx->ctr_mdot, ctx->gm_active);
+      // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
+      if ((size_t)nblk * S >= 2 * 148)
+        k_mdot_fused<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(
+            ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
+            ctx->ctr_mdot, ctx->gm_active);
+      else
+        k_mdot_fused_v<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(
+            ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
+            ctx->ctr_mdot, ctx->gm_active);
       k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
                                                              pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
     }
@@ -987,7 +993,7 @@ int check_S(pint_ctx* ctx, int S) {
 extern "C" {
 
 int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out) {
-  if (!desc || !out || max_slices < 1 || restart < 1) return PINT_INVALID_ARG;
+  if (!desc || !out || max_slices < 1 || restart < 1 || restart + 1 > kMdotMax) return PINT_INVALID_ARG;
   if (desc->dim != 2 && desc->dim != 3) return PINT_INVALID_ARG;
   for (int m = 0; m < desc->dim; ++m)
     if (desc->cells[m] < 1) return PINT_INVALID_ARG;
