@@ -350,7 +350,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pre", type=int, default=1, help="multigrid pre-smoothing sweeps")
     ap.add_argument("--post", type=int, default=1, help="multigrid post-smoothing sweeps")
-    ap.add_argument("--omega", type=float, default=0.8, help="smoother damping")
+    ap.add_argument("--omega", type=float, default=0.9, help="smoother damping")
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
     ap.add_argument("--reuse", type=int, default=8, help="rebuild the multigrid hierarchy every k steps")
     ap.add_argument("--max-levels", type=int, default=0, help="multigrid levels used (0: all)")

@@ -79,7 +79,7 @@ class KrylovSettings:
     max_iters: int = 300
     pre_smooth: int = 1
     post_smooth: int = 1
-    omega: float = 0.8
+    omega: float = 0.9
     max_levels: int = 0
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
