@@ -119,3 +119,33 @@ def test_gmres_mg_solves_jacobian_system(devices, name):
         assert rel <= 2e-10, (name, s, rel, its[s])
         assert its[s] < 120, (name, its[s])
         assert np.linalg.norm(X[s] - ref) <= 1e-6 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("smoother", ["jacobi", "vanka"])
+def test_both_smoothers_solve_c1_fine_step_system(devices, smoother):
+    """The node-block-Jacobi smoother (omega 0.5) stays selectable and converges
+    on a fine-step system; Vanka (default) too."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS["c1"]
+    dev = devices["c1"]
+    S = 2
+    Y = random_states(P, S, 31, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 32, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    y = dev.to_device(Y)
+    dev.assemble(y, y, k, th, t1)
+    ks = KrylovSettings(rtol=1e-10, max_iters=400, smoother=smoother, omega=0.5 if smoother == "jacobi" else 0.9)
+    dev.precond_setup(S, ks)
+    x, its, res = dev.linear_solve(dev.to_device(B), ks)
+    X = dev.to_host(x)
+    for s in range(S):
+        J = O.jacobian(P, Y[s], Y[s], k[s], th[s], t1[s])
+        assert np.linalg.norm(J @ X[s] - B[s]) <= 2e-10 * np.linalg.norm(B[s]), (smoother, its[s])
+
+
+def test_invalid_arguments_are_reported(devices):
+    from paper_1907_01252_b200.propagator import DeviceError
+    dev = devices["small2d"]
+    y = dev.empty(5)  # more slices than the context holds (3)
+    with pytest.raises(DeviceError, match="batch size"):
+        dev.residual(y, y, [0.01] * 5, [0.51] * 5, [0.1] * 5)
