@@ -570,21 +570,299 @@ __global__ void k_gauss_jordan(double* __restrict__ M, int n, const int* __restr
   }
 }
 
-// x = Ainv b on the coarsest level (grid.x = S)
+// ---------------------------------------------------------------- dense coarsest inverse, cluster version
+// The coarsest operator (n <= a few hundred dofs) is inverted by in-place
+// Gauss-Jordan with partial pivoting, distributed over a cluster of
+// kGJCluster CTAs per slice: each CTA holds ceil(n/CL) rows in shared memory,
+// the pivot candidates and the winning row travel through distributed shared
+// memory, one cluster barrier per pivot.  Pivoting is implicit (no row
+// swaps): step p picks the largest |a_rp| among rows not yet used (lowest
+// global row on ties, deterministic) and the permutations are resolved when
+// the inverse is written out, row-major [n][n].
+// ---------------------------------------------------------------- dense coarsest inverse, cluster version
+// The coarsest operator (n <= 448 dofs) is inverted by in-place Gauss-Jordan
+// with partial pivoting, distributed over a cluster of kGJCluster CTAs per
+// slice.  CTA `rank` owns rows [rank*rp, rank*rp + rp); inside it thread
+// (rg, cg) keeps the kGJTR x kGJTC tile of rows rg*kGJTR + t and columns
+// cg + 64 u in REGISTERS for the whole factorisation, so a pivot step costs
+// two loads (its rows' multipliers, its columns of the pivot row) per 49
+// FMAs instead of a shared-memory round trip per element.  Per pivot: the
+// owners of column p publish it, the local candidate (largest |a| over unused
+// rows, lowest row on ties) is pushed into every CTA of the cluster, one
+// cluster barrier, every CTA picks the same winner and pulls its row through
+// distributed shared memory.  Pivoting is implicit (no row swaps); the
+// permutations are resolved when the inverse is written out: fp32, row-major
+// [n][ld] (ld = n rounded up to 4 floats, so every row starts 16-B aligned for
+// the bulk copies of the V-cycle tail).  Preconditioner storage only: the
+// factorisation itself runs in fp64.
+constexpr int kGJCluster = 8;
+constexpr int kGJThreads = 512;
+constexpr int kGJRG = 8;                        // row groups
+constexpr int kGJCG = kGJThreads / kGJRG;       // column groups (64)
+constexpr int kGJTR = 7, kGJTC = 7;             // register tile
+constexpr int kGJMaxN = kGJCluster * kGJRG * kGJTR < kGJCG * kGJTC ? kGJCluster * kGJRG * kGJTR : kGJCG * kGJTC;
+
+__host__ __device__ inline size_t gj_rows_per(int n) { return (size_t)(n + kGJCluster - 1) / kGJCluster; }
+// Aloc [rp][n] (assembly staging), pub [2][n], prow [n], colf [2][rp], part [kGJRG] x 2,
+// cand [2][CL][2], piv_of [n], pinv [rp]
+__host__ __device__ inline size_t gj_smem_bytes(int n) {
+  const size_t rp = gj_rows_per(n);
+  return 8 * (rp * n + 3 * (size_t)n + 2 * rp + 2 * kGJRG + 4 * kGJCluster) + 4 * ((size_t)n + rp) + 16;
+}
+__host__ __device__ inline bool gj_fits(int n) { return n <= kGJMaxN && gj_smem_bytes(n) <= 227 * 1024; }
+
 template <int D>
-__global__ void k_dense_apply(Grid g, const double* __restrict__ M, const double* __restrict__ b,
+__global__ void __cluster_dims__(kGJCluster, 1, 1) __launch_bounds__(kGJThreads, 1)
+    k_dense_invert_cl(Grid g, const double* __restrict__ A, float* __restrict__ Minv, int n, int ld,
+                      const int* __restrict__ active) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int s = blockIdx.x / kGJCluster;
+  if (active && !active[s]) return;  // uniform over the cluster
+  const int rank = (int)cluster.block_rank();
+  const int rp = (int)gj_rows_per(n);
+  const int r0 = rank * rp;
+  const int nloc = max(0, min(rp, n - r0));
+  extern __shared__ __align__(16) unsigned char gj_smem[];
+  double* Aloc = reinterpret_cast<double*>(gj_smem);  // [rp][n]
+  double* pub = Aloc + (size_t)rp * n;                 // [2][n]: this CTA's candidate row
+  double* prow = pub + 2 * n;                          // scaled pivot row
+  double* colf = prow + n;                             // [2][rp]: column p of the local rows
+  double* part = colf + 2 * rp;                        // [kGJRG][2]: partial candidates (a, row)
+  double* cand = part + 2 * kGJRG;                     // [2][CL][2]: every CTA's candidate (a, local row)
+  int* piv_of = reinterpret_cast<int*>(cand + 4 * kGJCluster);  // [n]: pivot row of step p
+  int* pinv = piv_of + n;                                         // [rp]: step that used local row r
+  const int tid = threadIdx.x;
+  const int rg = tid / kGJCG, cg_ = tid % kGJCG;
+  const int rbase = rg * kGJTR;
+
+  // assemble the local rows from the block-stencil operator (shared staging)
+  for (int idx = tid; idx < rp * n; idx += kGJThreads) Aloc[idx] = 0.0;
+  __syncthreads();
+  const double* As = A + (size_t)s * NOFF * C * C * g.np;
+  for (int idx = tid; idx < nloc * NOFF; idx += kGJThreads) {
+    const int lr = idx / NOFF, off = idx % NOFF;
+    const int row = r0 + lr;
+    const int ca = row / g.nn, node = row % g.nn;
+    int i, j, k;
+    node_coords(g, node, i, j, k);
+    const int nb = neighbour(g, i, j, k, off);
+    if (nb < 0) continue;
+    double v[C];
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) v[cb] = As[(((size_t)off * C + ca) * C + cb) * g.np + node];
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) Aloc[(size_t)lr * n + cb * g.nn + nb] = v[cb];
+  }
+  __syncthreads();
+  double a[kGJTR][kGJTC];
+  unsigned used = 0;  // bit t: local row rbase + t already a pivot row (or absent)
+#pragma unroll
+  for (int t = 0; t < kGJTR; ++t) {
+    const int r = rbase + t;
+    if (r >= nloc) used |= 1u << t;
+#pragma unroll
+    for (int u = 0; u < kGJTC; ++u) {
+      const int j = cg_ + kGJCG * u;
+      a[t][u] = (r < nloc && j < n) ? Aloc[(size_t)r * n + j] : 0.0;
+    }
+  }
+  // column 0 and the partial candidates of step 0 (owners: cg_ == 0, u == 0)
+  if (cg_ == 0) {
+    double ba = 0.0;
+    int br = -1;
+#pragma unroll
+    for (int t = 0; t < kGJTR; ++t) {
+      const int r = rbase + t;
+      if (r < rp) colf[r] = a[t][0];
+      if (!(used >> t & 1u) && (br < 0 || fabs(a[t][0]) > fabs(ba))) { ba = a[t][0]; br = r; }
+    }
+    part[2 * rg] = ba;
+    part[2 * rg + 1] = (double)br;
+  }
+
+  for (int p = 0; p < n; ++p) {
+    const int buf = p & 1;
+    __syncthreads();  // partial candidates and colf[buf] of this step are complete
+    double ca_ = 0.0;
+    int cr = -1;
+#pragma unroll
+    for (int q = 0; q < kGJRG; ++q) {
+      const double qa = part[2 * q];
+      const int qr = (int)part[2 * q + 1];
+      if (qr >= 0 && (cr < 0 || fabs(qa) > fabs(ca_))) { ca_ = qa; cr = qr; }
+    }
+    // the candidate row's owners publish it (all-zero row if this CTA has none left)
+    if (cr >= 0 ? (cr / kGJTR == rg) : (rg == 0)) {
+      double* dst = pub + buf * n + cg_;
+      switch (cr >= 0 ? cr - rbase : -1) {
+#define GJ_PUB(T)                                                              \
+  case T:                                                                      \
+    _Pragma("unroll") for (int u = 0; u < kGJTC; ++u) if (cg_ + kGJCG * u < n) \
+        dst[kGJCG * u] = a[T][u];                                              \
+    break;
+        GJ_PUB(0) GJ_PUB(1) GJ_PUB(2) GJ_PUB(3) GJ_PUB(4) GJ_PUB(5) GJ_PUB(6)
+#undef GJ_PUB
+        default:
+#pragma unroll
+          for (int u = 0; u < kGJTC; ++u)
+            if (cg_ + kGJCG * u < n) dst[kGJCG * u] = 0.0;
+      }
+    }
+    if (tid < kGJCluster) {  // push the candidate into every CTA of the cluster
+      double* dst = cluster.map_shared_rank(cand, tid) + (buf * kGJCluster + rank) * 2;
+      dst[0] = ca_;
+      dst[1] = (double)cr;
+    }
+    cluster.sync();
+    // the winner over the cluster (every thread, from local shared memory; lowest rank on ties)
+    int wrank = -1, wl = -1;
+    double pa = 0.0;
+#pragma unroll
+    for (int q = 0; q < kGJCluster; ++q) {
+      const double qa = cand[(buf * kGJCluster + q) * 2];
+      const int ql = (int)cand[(buf * kGJCluster + q) * 2 + 1];
+      if (ql >= 0 && (wrank < 0 || fabs(qa) > fabs(pa))) { pa = qa; wrank = q; wl = ql; }
+    }
+    const double inv = pa != 0.0 ? 1.0 / pa : 0.0;
+    const double* wsrc = cluster.map_shared_rank(pub, wrank) + buf * n;
+    for (int j = tid; j < n; j += kGJThreads) prow[j] = j == p ? inv : wsrc[j] * inv;
+    if (tid == 0) piv_of[p] = wrank * rp + wl;
+    const int tw = wrank == rank ? wl - rbase : -1;  // my tile row that is the pivot row (if any)
+    if (tw >= 0 && tw < kGJTR) used |= 1u << tw;
+    if (tid % kGJCG == 0 && wrank == rank && wl >= rbase && wl < rbase + kGJTR) pinv[wl] = p;
+    __syncthreads();
+    // a_rj <- a_rj - a_rp prow_j everywhere (49 FMAs, no selects), then the
+    // owners fix column p (a_rp <- -a_rp / pivot) and the pivot row (<- prow)
+    double pj[kGJTC];
+#pragma unroll
+    for (int u = 0; u < kGJTC; ++u) {
+      const int j = cg_ + kGJCG * u;
+      pj[u] = j < n ? prow[j] : 0.0;
+    }
+    const double* cf = colf + buf * rp;
+#pragma unroll
+    for (int t = 0; t < kGJTR; ++t) {
+      const double ft = rbase + t < rp ? cf[rbase + t] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kGJTC; ++u) a[t][u] = fma(-ft, pj[u], a[t][u]);
+    }
+    if (cg_ == p % kGJCG) {
+      switch (p / kGJCG) {
+#define GJ_COL(U)                                                                     \
+  case U:                                                                             \
+    _Pragma("unroll") for (int t = 0; t < kGJTR; ++t) a[t][U] =                      \
+        rbase + t < rp ? -cf[rbase + t] * inv : 0.0;                                  \
+    break;
+        GJ_COL(0) GJ_COL(1) GJ_COL(2) GJ_COL(3) GJ_COL(4) GJ_COL(5) GJ_COL(6)
+#undef GJ_COL
+        default: break;
+      }
+    }
+    switch (tw) {
+#define GJ_ROW(T)                                                   \
+  case T:                                                           \
+    _Pragma("unroll") for (int u = 0; u < kGJTC; ++u) a[T][u] = pj[u]; \
+    break;
+      GJ_ROW(0) GJ_ROW(1) GJ_ROW(2) GJ_ROW(3) GJ_ROW(4) GJ_ROW(5) GJ_ROW(6)
+#undef GJ_ROW
+      default: break;
+    }
+    // owners of column p+1 publish it and their partial candidate
+    const int pn = p + 1;
+    if (pn < n && cg_ == pn % kGJCG) {
+      double v[kGJTR];
+      switch (pn / kGJCG) {
+#define GJ_NEXT(U)                                                          \
+  case U:                                                                   \
+    _Pragma("unroll") for (int t = 0; t < kGJTR; ++t) v[t] = a[t][U];       \
+    break;
+        GJ_NEXT(0) GJ_NEXT(1) GJ_NEXT(2) GJ_NEXT(3) GJ_NEXT(4) GJ_NEXT(5) GJ_NEXT(6)
+#undef GJ_NEXT
+        default:
+#pragma unroll
+          for (int t = 0; t < kGJTR; ++t) v[t] = 0.0;
+      }
+      double* cn = colf + (buf ^ 1) * rp;
+      double ba = 0.0;
+      int br = -1;
+#pragma unroll
+      for (int t = 0; t < kGJTR; ++t) {
+        const int r = rbase + t;
+        if (r < rp) cn[r] = v[t];
+        if (!(used >> t & 1u) && (br < 0 || fabs(v[t]) > fabs(ba))) { ba = v[t]; br = r; }
+      }
+      part[2 * rg] = ba;
+      part[2 * rg + 1] = (double)br;
+    }
+  }
+  __syncthreads();
+  // write out: inverse row pinv[r], column piv_of[j]  <-  local (r, j)
+  float* Ms = Minv + (size_t)s * n * ld;
+#pragma unroll
+  for (int t = 0; t < kGJTR; ++t) {
+    const int r = rbase + t;
+    if (r >= nloc) continue;
+    const size_t ro = (size_t)pinv[r] * ld;
+#pragma unroll
+    for (int u = 0; u < kGJTC; ++u) {
+      const int j = cg_ + kGJCG * u;
+      if (j < n) Ms[ro + piv_of[j]] = (float)a[t][u];
+    }
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+// x = M^{-1} b with the fp32 dense coarsest inverse [S][n][ld]: one warp per
+// row, lanes stride the columns, fp64 accumulation, fixed xor-butterfly order
+// (the tail's shared-memory copy of the rows gives the same bits)
+__device__ __forceinline__ double dense_row_dot(const float* __restrict__ Mr, const double* __restrict__ bsh, int n,
+                                                int lane) {
+  double acc = 0.0;
+  for (int c = lane; c < n; c += 32) acc = fma((double)Mr[c], bsh[c], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+template <int C>
+__device__ __forceinline__ void dense_apply_warps(const Grid& g, const float* __restrict__ M, int ld, int s,
+                                                  const double* __restrict__ b, double* __restrict__ x, int tid,
+                                                  int nth) {
+  const int n = C * g.nn;
+  const float* Ms = M + (size_t)s * n * ld;
+  const double* bs = b + (size_t)s * C * g.np;
+  const int lane = tid & 31;
+  for (int row = tid >> 5; row < n; row += nth >> 5) {
+    const float* Mr = Ms + (size_t)row * ld;
+    double acc = 0.0;
+    for (int c = lane; c < n; c += 32) acc = fma((double)Mr[c], bs[(c / g.nn) * g.np + (c % g.nn)], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[(size_t)s * C * g.np + (row / g.nn) * g.np + (row % g.nn)] = acc;
+  }
+}
+
+// fp64 augmented [n][2n] inverse (single-CTA fallback) -> fp32 [n][ld]
+__global__ void k_dense_to_f32(const double* __restrict__ M, float* __restrict__ out, int n, int ld,
+                               const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double* Ms = M + (size_t)s * n * 2 * n;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    out[(size_t)s * n * ld + (size_t)r * ld + c] = (float)Ms[(size_t)r * 2 * n + n + c];
+  }
+}
+
+template <int D>
+__global__ void k_dense_apply(Grid g, const float* __restrict__ M, int ld, const double* __restrict__ b,
                               double* __restrict__ x, const int* __restrict__ active) {
   constexpr int C = 2 * D + 1;
   const int s = blockIdx.x;
   if (active && !active[s]) return;
-  const int n = C * g.nn;
-  const double* Ms = M + (size_t)s * n * 2 * n;
-  const double* bs = b + (size_t)s * C * g.np;
-  for (int row = threadIdx.x; row < n; row += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < n; ++c) acc += Ms[(size_t)row * 2 * n + n + c] * bs[(c / g.nn) * g.np + (c % g.nn)];
-    x[(size_t)s * C * g.np + (row / g.nn) * g.np + (row % g.nn)] = acc;
-  }
+  dense_apply_warps<C>(g, M, ld, s, b, x, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------------------- GMRES scalar work (one thread per slice)
@@ -1070,7 +1348,9 @@ struct LevelDev {
 struct TailArgs {
   LevelDev lv[kMaxLevels];
   int first, last;       // levels handled: first..last (last = coarsest)
-  const double* dense;   // coarsest dense inverse [S][n][2n] (nullptr: smoothing sweeps)
+  const float* dense;    // coarsest dense inverse, fp32 [S][n][dense_ld] (nullptr: smoothing sweeps)
+  int dense_ld;
+  int dense_stage;       // 1: each CTA bulk-copies its rows of the inverse into shared memory at launch
   int coarse_sweeps;
   int pre, post;
   double omega;
@@ -1185,17 +1465,91 @@ __device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& 
   }
 }
 
-template <int D>
-__device__ __forceinline__ void tail_dense(const LevelDev& L, const double* M, int s, const double* b, double* x, int tid,
-                                           int nth) {
+// ---- bulk-copy (TMA 1-d) staging of the coarsest inverse into shared memory
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// rows of the coarsest inverse that CTA `rank` of a CL-cluster owns in the staged tail
+__host__ __device__ inline int tail_dense_rows(int n, int CL) { return (n + CL - 1) / CL; }
+__host__ __device__ inline size_t tail_dense_bsh_bytes(int n) { return ((size_t)n * 8 + 15) / 16 * 16; }
+__host__ __device__ inline size_t tail_dense_smem(int n, int ld, int CL) {
+  return 16 + tail_dense_bsh_bytes(n) + (size_t)tail_dense_rows(n, CL) * ld * 4;
+}
+struct TailStage {
+  unsigned long long* bar;
+  double* bsh;  // [n] coarse right-hand side
+  float* rows;  // [rows][ld] this CTA's rows of the inverse
+};
+__device__ __forceinline__ TailStage tail_stage_layout(int n) {
+  extern __shared__ __align__(16) unsigned char tail_smem[];
+  TailStage t;
+  t.bar = reinterpret_cast<unsigned long long*>(tail_smem);
+  t.bsh = reinterpret_cast<double*>(tail_smem + 16);
+  t.rows = reinterpret_cast<float*>(tail_smem + 16 + tail_dense_bsh_bytes(n));  // 16-B aligned for the bulk copy
+  return t;
+}
+
+template <int D, int CL>
+__device__ __forceinline__ void tail_dense_prefetch(const TailArgs& a, int s) {
   constexpr int C = 2 * D + 1;
+  const int n = C * a.lv[a.last].g.nn;
+  const TailStage t = tail_stage_layout(n);
+  if (threadIdx.x == 0) {
+    const int rank = blockIdx.x % CL;
+    const int rq = tail_dense_rows(n, CL);
+    const int r0 = rank * rq, r1 = min(n, r0 + rq);
+    mbar_init(t.bar, 1);
+    const unsigned bytes = r1 > r0 ? (unsigned)((size_t)(r1 - r0) * a.dense_ld * 4) : 0u;
+    mbar_expect_tx(t.bar, bytes);
+    const char* src = reinterpret_cast<const char*>(a.dense + (size_t)s * n * a.dense_ld + (size_t)r0 * a.dense_ld);
+    char* dst = reinterpret_cast<char*>(t.rows);
+    for (unsigned off = 0; off < bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), t.bar);
+  }
+}
+
+template <int D, int CL>
+__device__ __forceinline__ void tail_dense(const TailArgs& a, const LevelDev& L, int s, const double* b, double* x,
+                                           int tid, int nth) {
+  constexpr int C = 2 * D + 1;
+  if (!a.dense_stage) {
+    dense_apply_warps<C>(L.g, a.dense, a.dense_ld, s, b, x, tid, nth);
+    return;
+  }
   const int n = C * L.g.nn;
-  const double* Ms = M + (size_t)s * n * 2 * n;
+  const TailStage t = tail_stage_layout(n);
   const double* bs = b + (size_t)s * C * L.g.np;
-  for (int row = tid; row < n; row += nth) {
-    double acc = 0.0;
-    for (int c = 0; c < n; ++c) acc += Ms[(size_t)row * 2 * n + n + c] * bs[(c / L.g.nn) * L.g.np + (c % L.g.nn)];
-    x[(size_t)s * C * L.g.np + (row / L.g.nn) * L.g.np + (row % L.g.nn)] = acc;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) t.bsh[c] = bs[(c / L.g.nn) * L.g.np + (c % L.g.nn)];
+  mbar_wait(t.bar, 0);
+  __syncthreads();
+  const int rank = blockIdx.x % CL;
+  const int rq = tail_dense_rows(n, CL);
+  const int r0 = rank * rq, r1 = min(n, r0 + rq);
+  const int lane = threadIdx.x & 31;
+  for (int row = r0 + (threadIdx.x >> 5); row < r1; row += blockDim.x >> 5) {
+    const double acc = dense_row_dot(t.rows + (size_t)(row - r0) * a.dense_ld, t.bsh, n, lane);
+    if (lane == 0) x[(size_t)s * C * L.g.np + (row / L.g.nn) * L.g.np + (row % L.g.nn)] = acc;
   }
 }
 
@@ -1231,6 +1585,7 @@ __device__ __forceinline__ void vcycle_tail_body(const TailArgs& a, const double
                                                  double* __restrict__ x_top, const int* __restrict__ active) {
   const int s = blockIdx.x / CL;
   if (active && !active[s]) return;  // uniform over the cluster
+  if (a.dense && a.dense_stage) tail_dense_prefetch<D, CL>(a, s);  // lands while the finer levels smooth
   const int tid = (blockIdx.x % CL) * blockDim.x + threadIdx.x;
   const int nth = CL * blockDim.x;
   const double* bl[kMaxLevels];
@@ -1256,7 +1611,7 @@ __device__ __forceinline__ void vcycle_tail_body(const TailArgs& a, const double
     const double* bc = (a.last == a.first) ? b_top : L.rhs;
     double* xc = (a.last == a.first) ? x_top : L.sol;
     if (a.dense) {
-      tail_dense<D>(L, a.dense, s, bc, xc, tid, nth);
+      tail_dense<D, CL>(a, L, s, bc, xc, tid, nth);
       tail_sync<CL>();
     } else {
       double* c0 = L.xa;

@@ -33,6 +33,7 @@ using namespace pint;
 namespace {
 
 constexpr int kDenseMax = 1024;
+constexpr size_t kTailSmemMax = 220 * 1024;  // dynamic shared memory of a staged tail CTA
 
 struct Level {
   Grid g;
@@ -79,7 +80,10 @@ struct pint_ctx {
   int dense_n = 0;           // dofs of the coarsest used level (set by precond_setup)
   int dense_cap = 0;         // largest dense dimension the buffer holds
   bool coarse_dense = false; // coarsest used level solved by its dense inverse
-  double* d_dense = nullptr;
+  int dense_ld = 0;          // row stride (floats) of the fp32 inverse in d_dense32
+  double* d_dense = nullptr;  // fp64 scratch of the single-CTA fallback ([n][2n] augmented)
+  float* d_dense32 = nullptr; // coarsest inverse, fp32 [S][n][dense_ld]
+  bool dense_stage = false;   // tail CTAs bulk-copy their rows of the inverse to shared memory
   // Newton
   double *ystate = nullptr, *ynew = nullptr, *r = nullptr, *dx = nullptr, *ytrial = nullptr, *rtrial = nullptr,
          *b = nullptr;
@@ -115,11 +119,13 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
+  int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
   bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a 4-CTA cluster
   bool use_fused = false;    // PINT_FUSED=1 enables the fused Arnoldi-step kernel (slower than the
                              // graph of level-0 launches on c2: measured 3659 vs 4123 steps*slices/s)
   bool fused = false;        // fused Arnoldi step active for the current hierarchy
   TailArgs tail0{};          // V-cycle description from level 0 (fused path)
+  TailArgs tail_cl{};        // the cluster tail's copy (dense rows staged in shared memory)
   unsigned long long* d_work_bytes = nullptr;
   bool fused_used = false;   // profiling: the fused kernel ran while profiling
   TailArgs tail{};
@@ -393,7 +399,17 @@ struct Impl {
   // ---- multigrid setup: RAP on all levels, block inverses, dense coarsest
   static int precond_setup(pint_ctx* ctx, int S, const pint_krylov_opts* ko, const int* mask, cudaStream_t st) {
     int nl = (int)ctx->lv.size();
-    if (ko->max_levels > 0) nl = std::min(nl, (int)ko->max_levels);
+    if (ko->max_levels > 0) {
+      nl = std::min(nl, (int)ko->max_levels);
+    } else {
+      // default: stop at the first level the cluster Gauss-Jordan inverts; a
+      // dense solve there replaces the latency-bound sweeps of the levels below
+      for (int l = 0; l < nl; ++l)
+        if (C * ctx->lv[l].g.nn <= ctx->dense_cap && gj_fits(C * ctx->lv[l].g.nn)) {
+          nl = l + 1;
+          break;
+        }
+    }
     ctx->prec_levels = nl;
     ctx->kopt = *ko;
     // coarsest used level solved with a dense inverse when it fits the buffer
@@ -419,8 +435,19 @@ struct Impl {
     }
     if (ctx->coarse_dense) {
       Level& L = ctx->lv[nl - 1];
-      k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
-      k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->dense_n, mask);
+      const int n = ctx->dense_n;
+      ctx->dense_ld = (n + 3) / 4 * 4;
+      const size_t smem = gj_smem_bytes(n);
+      if (gj_fits(n)) {
+        cudaFuncSetAttribute(k_dense_invert_cl<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_dense_invert_cl<D><<<S * kGJCluster, kGJThreads, smem, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense32, n,
+                                                                                      ctx->dense_ld, mask);
+      } else {
+        k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
+        k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, n, mask);
+        k_dense_to_f32<<<dim3((n * n + 255) / 256, S), 256, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->d_dense32, n,
+                                                                                 ctx->dense_ld, mask);
+      }
     }
     // fused V-cycle tail: from the first level with <= 2048 rows per slice down
     ctx->tail_first = -1;
@@ -435,11 +462,20 @@ struct Impl {
         }
         t.first = ctx->tail_first;
         t.last = nl - 1;
-        t.dense = ctx->coarse_dense ? ctx->d_dense : nullptr;
+        t.dense = ctx->coarse_dense ? ctx->d_dense32 : nullptr;
+        t.dense_ld = ctx->dense_ld;
+        // cluster tail: each CTA stages its rows of the inverse (fits shared memory up to ~450 dofs)
+        const size_t tsm = ctx->coarse_dense ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, kTailCluster) : 0;
+        ctx->dense_stage = ctx->coarse_dense && ctx->tail_cluster && tsm <= kTailSmemMax;
+        t.dense_stage = 0;
+        if (ctx->dense_stage)
+          cudaFuncSetAttribute(k_vcycle_tail_cl<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
         t.coarse_sweeps = ko->coarse_sweeps;
         t.pre = ko->pre_smooth;
         t.post = ko->post_smooth;
         t.omega = ko->omega;
+        ctx->tail_cl = t;
+        ctx->tail_cl.dense_stage = ctx->dense_stage ? 1 : 0;
       }
     }
     // fused Arnoldi step: the whole step in one cluster launch per slice when
@@ -520,15 +556,30 @@ struct Impl {
     const int nl = ctx->prec_levels;
     const pint_krylov_opts& ko = ctx->kopt;
     if (l == ctx->tail_first) {
+      // whole V-cycle inside the tail kernel (small meshes): it is the profiled kernel
+      const bool prof = ctx->prof && l == 0;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (prof) {
+        e0 = next_event(ctx);
+        e1 = next_event(ctx);
+        cudaEventRecord(e0, st);
+        ctx->tail_slice_launches += S;
+      }
       if (ctx->tail_cluster)
-        k_vcycle_tail_cl<D><<<S * kTailCluster, kTailThreads, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+        k_vcycle_tail_cl<D><<<S * kTailCluster, kTailThreads,
+                              ctx->dense_stage ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, kTailCluster) : 0,
+                              counted(ctx, st)>>>(ctx->tail_cl, b, x, mask);
       else
         k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+      if (prof) {
+        cudaEventRecord(e1, st);
+        ctx->ev_pairs.emplace_back(e0, e1);
+      }
       return;
     }
     if (l == nl - 1) {
       if (ctx->coarse_dense) {
-        k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense, b, x, mask);
+        k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense32, ctx->dense_ld, b, x, mask);
       } else {
         const int sweeps = std::max(1, (int)ko.coarse_sweeps);
         double* cur = L.xa;
@@ -608,16 +659,17 @@ struct Impl {
   }
 
   // algorithmic bytes of one Arnoldi step j for one slice (fused kernel roofline)
-  static unsigned long long arnoldi_bytes(pint_ctx* ctx, int j) {
+  // algorithmic bytes of one V-cycle from level `from` down, for one slice
+  static unsigned long long vcycle_bytes(pint_ctx* ctx, int from) {
     unsigned long long total = 0;
     const int nl = ctx->prec_levels;
     const int Lc = (1 << D) * C;
-    for (int l = 0; l < nl; ++l) {
+    for (int l = from; l < nl; ++l) {
       const Level& L = ctx->lv[l];
       const unsigned long long V = (unsigned long long)C * 8 * L.g.nn;
       const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * 8 * L.g.nn;
       if (l == nl - 1 && ctx->coarse_dense) {
-        total += (unsigned long long)ctx->dense_n * ctx->dense_n * 8 + 2 * V;
+        total += (unsigned long long)ctx->dense_n * ctx->dense_n * 4 + 2 * V;  // fp32 inverse
         continue;
       }
       const unsigned long long cellb = (unsigned long long)L.ncell * ((unsigned long long)Lc * Lc * 4 + 2 * Lc * 8);
@@ -625,6 +677,11 @@ struct Impl {
       const int full = ctx->kopt.pre_smooth - 1 + ctx->kopt.post_smooth;
       total += (cellb + 2 * V) + full * (Ab + 2 * V + cellb + 2 * V) + (Ab + 2 * V) + 3 * V;
     }
+    return total;
+  }
+
+  static unsigned long long arnoldi_bytes(pint_ctx* ctx, int j) {
+    unsigned long long total = vcycle_bytes(ctx, 0);
     const unsigned long long V0 = (unsigned long long)C * 8 * ctx->lv[0].g.nn;
     const unsigned long long A0 = (unsigned long long)ctx->lv[0].g.noff * C * C * 8 * ctx->lv[0].g.nn;
     total += A0 + 2 * V0;                          // w = J z
@@ -1084,7 +1141,10 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   for (const Level& L : ctx->lv)
     if (C * L.g.nn <= kDenseMax) ctx->dense_cap = std::max(ctx->dense_cap, C * L.g.nn);
   if (ctx->dense_cap == 0 && C * Lc.g.nn <= kDenseMax) ctx->dense_cap = C * Lc.g.nn;
-  if (ctx->dense_cap > 0) ALLOC(ctx->d_dense, (size_t)S * ctx->dense_cap * 2 * ctx->dense_cap);
+  if (ctx->dense_cap > 0) {
+    ALLOC(ctx->d_dense, (size_t)S * ctx->dense_cap * 2 * ctx->dense_cap);
+    ALLOC(ctx->d_dense32, (size_t)S * ctx->dense_cap * ((ctx->dense_cap + 3) / 4 * 4));
+  }
 
   ALLOC(ctx->ystate, S * vsz);
   ALLOC(ctx->ynew, S * vsz);
@@ -1183,6 +1243,7 @@ int pint_profile(pint_ctx* ctx, int32_t enable) {
   cudaMemset(ctx->d_work, 0, sizeof(unsigned long long));
   cudaMemset(ctx->d_work_bytes, 0, sizeof(unsigned long long));
   ctx->fused_used = false;
+  ctx->tail_slice_launches = 0;
   return PINT_OK;
 }
 
@@ -1190,6 +1251,9 @@ const char* pint_profile_kernel(const pint_ctx* ctx) {
   if (!ctx) return "";
   if (ctx->fused_used) return ctx->D == 2 ? "k_arnoldi_fused<2> (whole Arnoldi step: V-cycle + SpMV + CGS2 + Givens)"
                                          : "k_arnoldi_fused<3> (whole Arnoldi step: V-cycle + SpMV + CGS2 + Givens)";
+  if (ctx->tail_first == 0)
+    return ctx->D == 2 ? "k_vcycle_tail_cl<2> (whole V-cycle: mesh fits the cluster tail)"
+                       : "k_vcycle_tail_cl<3> (whole V-cycle: mesh fits the cluster tail)";
   if (ctx->kopt.smoother == 1) return ctx->D == 2 ? "k_vanka_cell<2,16> (level-0 cell-patch Vanka solves)"
                                                   : "k_vanka_cell<3,8> (level-0 cell-patch Vanka solves)";
   return ctx->D == 2 ? "k_smooth<2,false> (level-0 node-block Jacobi sweep)" : "k_smooth<3,false>";
@@ -1210,12 +1274,16 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   PINT_CHECK(cudaMemcpy(&work, ctx->d_work, sizeof(work), cudaMemcpyDeviceToHost));
   if (launches) *launches = ctx->launches;
   if (kernel_launches) *kernel_launches = (int64_t)ctx->ev_pairs.size();
-  if (slice_launches) *slice_launches = (int64_t)work;
+  const bool tail_kernel = !ctx->fused_used && ctx->tail_first == 0;
+  if (slice_launches) *slice_launches = tail_kernel ? ctx->tail_slice_launches : (int64_t)work;
   if (kernel_ms) *kernel_ms = ms;
   if (bytes_per_slice_launch && ctx->fused_used) {
     unsigned long long wb = 0;
     PINT_CHECK(cudaMemcpy(&wb, ctx->d_work_bytes, sizeof(wb), cudaMemcpyDeviceToHost));
     *bytes_per_slice_launch = work ? (int64_t)(wb / work) : 0;  // k_arnoldi_fused, averaged over j
+  } else if (bytes_per_slice_launch && tail_kernel) {
+    *bytes_per_slice_launch =
+        (int64_t)(ctx->D == 2 ? Impl<2>::vcycle_bytes(ctx, 0) : Impl<3>::vcycle_bytes(ctx, 0));
   } else if (bytes_per_slice_launch) {
     const Grid& g = ctx->lv[0].g;
     const int64_t C = ctx->C;

@@ -22,14 +22,16 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--slices", type=int, default=0)
+    ap.add_argument("--max-levels", type=int, default=0)
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     P = cfg.problem
     S = a.slices or cfg.intervals
     dev = FSIDevice(P, S)
     newton = NewtonSettings(1e-10, 1e-10)
-    F = make_propagator(P, ThetaSettings(cfg.fine_step, cfg.theta0, newton), krylov=KrylovSettings(), device=dev)
-    C = make_propagator(P, ThetaSettings(cfg.coarse_step, cfg.theta0, newton), krylov=KrylovSettings(), device=dev)
+    ks = KrylovSettings(max_levels=a.max_levels)
+    F = make_propagator(P, ThetaSettings(cfg.fine_step, cfg.theta0, newton), krylov=ks, device=dev)
+    C = make_propagator(P, ThetaSettings(cfg.coarse_step, cfg.theta0, newton), krylov=ks, device=dev)
     # start states: one coarse window from rest, replicated with staggered times
     s0 = initial_state(P)
     y = dev.to_device([s0.values] * S)
