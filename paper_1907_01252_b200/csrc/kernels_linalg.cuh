@@ -1645,14 +1645,17 @@ __global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* 
   vcycle_tail_body<D, 1>(a, b_top, x_top, active);
 }
 
-// cluster variant: kTailCluster CTAs per slice cooperate through cluster barriers
-constexpr int kTailCluster = 4;    // CTAs per slice
-constexpr int kTailThreads = 512;  // threads per CTA (128 registers per thread)
-template <int D>
-__global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(kTailThreads)
+// cluster variant: CL CTAs per slice cooperate through cluster barriers.  The
+// host picks the largest CL (8, 4, 2) with S*CL CTAs in one wave; every output
+// is computed by one thread with a partition-independent formula, so the
+// result does not depend on CL (batch invariance).
+constexpr int kTailCluster = 4;    // CTAs per slice of the fused Arnoldi kernel (PINT_FUSED=1)
+constexpr int kTailThreads = 512;  // threads per CTA
+template <int D, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kTailThreads)
     k_vcycle_tail_cl(TailArgs a, const double* __restrict__ b_top, double* __restrict__ x_top,
                      const int* __restrict__ active) {
-  vcycle_tail_body<D, kTailCluster>(a, b_top, x_top, active);
+  vcycle_tail_body<D, CL>(a, b_top, x_top, active);
 }
 
 }  // namespace pint

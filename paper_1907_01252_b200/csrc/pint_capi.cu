@@ -83,7 +83,6 @@ struct pint_ctx {
   int dense_ld = 0;          // row stride (floats) of the fp32 inverse in d_dense32
   double* d_dense = nullptr;  // fp64 scratch of the single-CTA fallback ([n][2n] augmented)
   float* d_dense32 = nullptr; // coarsest inverse, fp32 [S][n][dense_ld]
-  bool dense_stage = false;   // tail CTAs bulk-copy their rows of the inverse to shared memory
   // Newton
   double *ystate = nullptr, *ynew = nullptr, *r = nullptr, *dx = nullptr, *ytrial = nullptr, *rtrial = nullptr,
          *b = nullptr;
@@ -120,7 +119,9 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
-  bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a 4-CTA cluster
+  bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a cluster
+  int tail_cl_force = 0;     // PINT_TAIL_CL=8|4|2: fixed cluster size (else: largest with one wave)
+  int num_sms = 148;
   bool use_fused = false;    // PINT_FUSED=1 enables the fused Arnoldi-step kernel (slower than the
                              // graph of level-0 launches on c2: measured 3659 vs 4123 steps*slices/s)
   bool fused = false;        // fused Arnoldi step active for the current hierarchy
@@ -139,6 +140,16 @@ struct pint_ctx {
   size_t ev_used = 0;
   pint_krylov_opts kopt{};
 };
+
+// CTAs per slice of the V-cycle tail: the largest cluster whose S*CL CTAs run in
+// one wave (1: the single-CTA kernel).  Results do not depend on the choice.
+static inline int tail_cluster_size(const pint_ctx* ctx, int S) {
+  if (!ctx->tail_cluster) return 1;
+  if (ctx->tail_cl_force) return ctx->tail_cl_force;
+  for (int cl = 8; cl >= 2; cl /= 2)
+    if (S * cl <= ctx->num_sms) return cl;
+  return 1;
+}
 
 static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st) {
   ++ctx->launches;
@@ -464,18 +475,24 @@ struct Impl {
         t.last = nl - 1;
         t.dense = ctx->coarse_dense ? ctx->d_dense32 : nullptr;
         t.dense_ld = ctx->dense_ld;
-        // cluster tail: each CTA stages its rows of the inverse (fits shared memory up to ~450 dofs)
-        const size_t tsm = ctx->coarse_dense ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, kTailCluster) : 0;
-        ctx->dense_stage = ctx->coarse_dense && ctx->tail_cluster && tsm <= kTailSmemMax;
+        // cluster tails: each CTA stages its rows of the inverse when they fit shared memory
         t.dense_stage = 0;
-        if (ctx->dense_stage)
-          cudaFuncSetAttribute(k_vcycle_tail_cl<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        if (ctx->coarse_dense) {
+          const int n = ctx->dense_n, ld = ctx->dense_ld;
+          const size_t t8 = tail_dense_smem(n, ld, 8), t4 = tail_dense_smem(n, ld, 4), t2 = tail_dense_smem(n, ld, 2);
+          if (t8 <= kTailSmemMax)
+            cudaFuncSetAttribute(k_vcycle_tail_cl<D, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t8);
+          if (t4 <= kTailSmemMax)
+            cudaFuncSetAttribute(k_vcycle_tail_cl<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t4);
+          if (t2 <= kTailSmemMax)
+            cudaFuncSetAttribute(k_vcycle_tail_cl<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t2);
+        }
         t.coarse_sweeps = ko->coarse_sweeps;
         t.pre = ko->pre_smooth;
         t.post = ko->post_smooth;
         t.omega = ko->omega;
         ctx->tail_cl = t;
-        ctx->tail_cl.dense_stage = ctx->dense_stage ? 1 : 0;
+        ctx->tail_cl.dense_stage = ctx->coarse_dense ? 1 : 0;
       }
     }
     // fused Arnoldi step: the whole step in one cluster launch per slice when
@@ -565,10 +582,17 @@ struct Impl {
         cudaEventRecord(e0, st);
         ctx->tail_slice_launches += S;
       }
-      if (ctx->tail_cluster)
-        k_vcycle_tail_cl<D><<<S * kTailCluster, kTailThreads,
-                              ctx->dense_stage ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, kTailCluster) : 0,
-                              counted(ctx, st)>>>(ctx->tail_cl, b, x, mask);
+      const int cl = tail_cluster_size(ctx, S);
+      const size_t tsm = ctx->coarse_dense ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, cl) : 0;
+      const bool stage = ctx->coarse_dense && tsm <= kTailSmemMax;
+      const TailArgs& ta = stage ? ctx->tail_cl : ctx->tail;
+      const size_t sm = stage ? tsm : 0;
+      if (cl == 8)
+        k_vcycle_tail_cl<D, 8><<<S * 8, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
+      else if (cl == 4)
+        k_vcycle_tail_cl<D, 4><<<S * 4, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
+      else if (cl == 2)
+        k_vcycle_tail_cl<D, 2><<<S * 2, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
       else
         k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
       if (prof) {
@@ -1065,6 +1089,16 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
   ctx->use_tail = !(std::getenv("PINT_TAIL") && std::getenv("PINT_TAIL")[0] == '0');
   ctx->tail_cluster = !(std::getenv("PINT_TAIL_CLUSTER") && std::getenv("PINT_TAIL_CLUSTER")[0] == '0');
+  if (const char* e = std::getenv("PINT_TAIL_CL")) {
+    const int v = std::atoi(e);
+    ctx->tail_cl_force = (v == 2 || v == 4 || v == 8) ? v : 0;
+  }
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+      ctx->num_sms = sms;
+  }
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
