@@ -682,7 +682,6 @@ struct Impl {
     k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
-  // algorithmic bytes of one Arnoldi step j for one slice (fused kernel roofline)
   // algorithmic bytes of one V-cycle from level `from` down, for one slice
   static unsigned long long vcycle_bytes(pint_ctx* ctx, int from) {
     unsigned long long total = 0;
@@ -704,6 +703,7 @@ struct Impl {
     return total;
   }
 
+  // algorithmic bytes of one Arnoldi step j for one slice (fused kernel roofline)
   static unsigned long long arnoldi_bytes(pint_ctx* ctx, int j) {
     unsigned long long total = vcycle_bytes(ctx, 0);
     const unsigned long long V0 = (unsigned long long)C * 8 * ctx->lv[0].g.nn;
