@@ -88,9 +88,9 @@ PINT_HD T det_inv(const T (&F)[D][D], T (&Fi)[D][D]) {
 constexpr double kGaussLo = 0.21132486540518711775;  // 1/2 - 1/(2 sqrt 3)
 constexpr double kGaussHi = 0.78867513459481288225;  // 1/2 + 1/(2 sqrt 3)
 
-// Q1 shape values and physical gradients at xi in [0,1]^D
+// Q1 shape values and physical gradients at xi in [0,1]^D (ih = 1 / cell size)
 template <int D>
-PINT_HD void q1_shape(const double (&xi)[D], const double* h, double (&N)[1 << D], double (&dN)[1 << D][D]) {
+PINT_HD void q1_shape(const double (&xi)[D], const double* ih, double (&N)[1 << D], double (&dN)[1 << D][D]) {
 #pragma unroll
   for (int a = 0; a < (1 << D); ++a) {
     double n = 1.0;
@@ -103,7 +103,7 @@ PINT_HD void q1_shape(const double (&xi)[D], const double* h, double (&N)[1 << D
 #pragma unroll
       for (int k = 0; k < D; ++k)
         if (k != m) g *= ((a >> k) & 1) ? xi[k] : 1.0 - xi[k];
-      dN[a][m] = g / h[m];
+      dN[a][m] = g * ih[m];
     }
   }
 }
@@ -396,6 +396,54 @@ __device__ __forceinline__ void seed_basis(const QFields<D, double>& f, int cb, 
   }
   if constexpr (G == 2) {
     n.p = Dual(f.p, Nb);
+  } else {
+    n.p = f.p;
+  }
+}
+
+// fields with ONE unit derivative direction of component cb: dir = 0 seeds
+// the value of cb, dir = 1 + k its derivative along x_k.  The derivative of
+// the flux along the trial function (N_b, dN_b) of cb is then the linear
+// combination  dF(dir 0) N_b + sum_k dF(dir 1+k) dN_b,k  -- 1 + D pointwise
+// passes give all 2^D Jacobian columns of the component.
+template <int D, int G>
+__device__ __forceinline__ void seed_dir(const QFields<D, double>& f, int cb, int dir,
+                                         typename SeedTypes<D, G>::F& n) {
+  const double sv = dir == 0 ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    if constexpr (G == 0) {
+      n.v[i] = Dual(f.v[i], cb == i ? sv : 0.0);
+    } else {
+      n.v[i] = f.v[i];
+    }
+    if constexpr (G == 1) {
+      n.u[i] = Dual(f.u[i], cb == D + i ? sv : 0.0);
+    } else {
+      n.u[i] = f.u[i];
+    }
+    if constexpr (G == 2) {
+      n.gp[i] = Dual(f.gp[i], dir == 1 + i ? 1.0 : 0.0);
+    } else {
+      n.gp[i] = f.gp[i];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double sg = (dir == 1 + j) ? 1.0 : 0.0;
+      if constexpr (G == 0) {
+        n.Gv[i][j] = Dual(f.Gv[i][j], cb == i ? sg : 0.0);
+      } else {
+        n.Gv[i][j] = f.Gv[i][j];
+      }
+      if constexpr (G == 1) {
+        n.Gu[i][j] = Dual(f.Gu[i][j], cb == D + i ? sg : 0.0);
+      } else {
+        n.Gu[i][j] = f.Gu[i][j];
+      }
+    }
+  }
+  if constexpr (G == 2) {
+    n.p = Dual(f.p, sv);
   } else {
     n.p = f.p;
   }

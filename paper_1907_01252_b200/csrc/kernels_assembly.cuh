@@ -93,7 +93,7 @@ __device__ __forceinline__ void qp_integral(const Phys& ph, const StepScalars& s
     const bool face = pt == 1;
     double xi[D], N[A], dN[A][D];
     gauss_point<D>(q, face, xi);
-    q1_shape<D>(xi, ph.h, N, dN);
+    q1_shape<D>(xi, ph.ih, N, dN);
     QFields<D, double> fn, fo;
     interp<D>(N, dN, gy, fn);
     interp<D>(N, dN, go, fo);
@@ -163,6 +163,30 @@ __device__ __forceinline__ void reduce_points(double (&acc)[1 << D][2 * D + 1]) 
     }
 }
 
+// lane q adds the rows of local node q to the vector out: all old values are
+// loaded before the first store (no load waits behind a store that might alias)
+template <int D>
+__device__ __forceinline__ void scatter_rows(const double (&R)[1 << D][2 * D + 1], int q, const ElemIndex<D>& e,
+                                             double* __restrict__ out, int np) {
+  constexpr int C = 2 * D + 1, A = 1 << D;
+  const bool solid = e.cflag & kCellSolid;  // solid cells own no p rows
+  double* o = out + e.node[q];
+  double v[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    double x = R[0][c];
+#pragma unroll
+    for (int a = 1; a < A; ++a) x = (q == a) ? R[a][c] : x;
+    v[c] = x;
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!(c == 2 * D && solid)) v[c] += o[c * np];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!(c == 2 * D && solid)) o[c * np] = v[c];
+}
+
 // ---------------------------------------------------------------- K1 residual
 // thread = (element of the colour, quadrature point); lane q scatters node q
 template <int D>
@@ -186,15 +210,7 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_residual_colour(Mesh
   reduce_points<D>(R);
   if (!valid) return;
   if (dg) degen[s] = 1;  // benign: every writer stores 1
-  double* rs = r + s * vs;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (c == 2 * D && (e.cflag & kCellSolid)) continue;  // solid cells own no p rows
-    double v = R[0][c];
-#pragma unroll
-    for (int a = 1; a < A; ++a) v = (q == a) ? R[a][c] : v;
-    rs[c * m.g.np + e.node[q]] += v;
-  }
+  scatter_rows<D>(R, q, e, r + s * vs, m.g.np);
 }
 
 // ---------------------------------------------------------------- K2 Jacobian columns
@@ -236,14 +252,251 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jacobian_colour(Mesh
   const int dj = ((astar >> 1) & 1) - ((a >> 1) & 1);
   const int dk = D == 3 ? ((astar >> 2) & 1) - ((a >> 2) & 1) : 0;
   const int off = offset_index(di, dj, dk, D);
+  double* o = Js + ((size_t)off * C * C + cstar) * np + e.node[a];
+  const bool solid = e.cflag & kCellSolid;
+  double v[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    if (c == 2 * D && (e.cflag & kCellSolid)) continue;
-    double v = K[0][c];
+    double x = K[0][c];
 #pragma unroll
-    for (int b = 1; b < A; ++b) v = (a == b) ? K[b][c] : v;
-    Js[(((size_t)off * C + c) * C + cstar) * np + e.node[a]] += v;
+    for (int b = 1; b < A; ++b) x = (a == b) ? K[b][c] : x;
+    v[c] = x;
   }
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!(c == 2 * D && solid)) v[c] += o[(size_t)c * C * np];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!(c == 2 * D && solid)) o[(size_t)c * C * np] = v[c];
+}
+
+// ---------------------------------------------------------------- K2 Jacobian by pointwise linearisation
+// The element Jacobian column (b, c') is  sum_q W t(a,q)^T dF_q t(b,q)  with
+// t(b,q) = (N_b, grad N_b) at point q: the flux derivative along a trial
+// function is linear in its (value, gradient) seed.  So per (element, point)
+// and column component c' only 1 + D pointwise dual passes are needed (not
+// 2^D, one per column), and the fields are interpolated once per c' (not
+// once per column).
+//   phase 1  thread = (element, point q): G[c][o][i] = derivative of the flux
+//            output o (0: value-tested, 1+j: tested with d/dx_j) of row
+//            component c along seed i (0: value of c', 1+k: d/dx_k of c');
+//            outflow face points add GF[c][i] for the momentum rows.  G lives
+//            in shared memory ([entry][thread], conflict-free).
+//   phase 2  thread = (element, local node a): K[a][c][b] = sum over points in
+//            a fixed order (deterministic), scattered to the block stencil.
+// Grid (element groups, C column components, slices); colour-ordered
+// scatter as in k_jacobian_colour.
+template <int D>
+struct JacLin {
+  static constexpr int A = 1 << D;
+  static constexpr int C = 2 * D + 1;
+  static constexpr int NS = 1 + D;               // seeds / test kinds per component
+  static constexpr int EPB = D == 2 ? 32 : 8;    // elements per block
+  static constexpr int T = EPB * A;              // threads per block
+  static constexpr int OCC = D == 2 ? 4 : 3;     // resident blocks per SM
+  static constexpr int GSZ = C * NS * NS;        // volume entries per (element, point)
+  static constexpr int FSZ = D * NS;             // face entries per (element, face point)
+  static constexpr int TVSZ = A * A * NS;        // volume shape table
+  static constexpr int TFSZ = (A / 2) * A * NS;  // face shape table
+  static constexpr size_t smem = sizeof(double) * ((size_t)(GSZ + FSZ) * T + TVSZ + TFSZ);
+};
+
+template <int D, int G>
+__device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& st, const ElemIndex<D>& e, int q,
+                                             const double* __restrict__ y, const double* __restrict__ yo, int np,
+                                             int cp, double* __restrict__ sg, int T, const double* __restrict__ tv,
+                                             const double* __restrict__ tf) {
+  constexpr int A = 1 << D, NS = 1 + D;
+  // shape values / gradients of point q from the block's tables ([b][NS])
+  auto shape = [&](const double* t, double (&N)[A], double (&dN)[A][D]) {
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      N[b] = t[b * NS];
+#pragma unroll
+      for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+    }
+  };
+  using ST = SeedTypes<D, G>;
+  const bool solid = e.cflag & kCellSolid;
+  auto gy = [&](int a, int c) { return __ldg(y + c * np + e.node[a]); };
+  auto go = [&](int a, int c) { return __ldg(yo + c * np + e.node[a]); };
+  {
+    double N[A], dN[A][D];
+    shape(tv + q * A * NS, N, dN);
+    QFields<D, double> fn, fo;
+    interp<D>(N, dN, gy, fn);
+    interp<D>(N, dN, go, fo);
+#pragma unroll 1
+    for (int dir = 0; dir < NS; ++dir) {
+      typename ST::F fd;
+      seed_dir<D, G>(fn, cp, dir, fd);
+      QFlux<D, Dual> fx;
+      bool dg = false;
+      qflux<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, solid, fd, fo, fx, dg);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        sg[((i * NS + 0) * NS + dir) * T] = fx.vec[i].d;
+        sg[(((D + i) * NS + 0) * NS + dir) * T] = fx.uvec[i].d;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          sg[((i * NS + 1 + j) * NS + dir) * T] = fx.ten[i][j].d;
+          sg[(((D + i) * NS + 1 + j) * NS + dir) * T] = fx.uten[i][j].d;
+        }
+      }
+      sg[((2 * D * NS + 0) * NS + dir) * T] = fx.pv.d;
+#pragma unroll
+      for (int j = 0; j < D; ++j) sg[((2 * D * NS + 1 + j) * NS + dir) * T] = fx.pt[j].d;
+    }
+  }
+  constexpr int GSZ = (2 * D + 1) * NS * NS;
+  if constexpr (G != 2) {
+   if ((e.cflag & kCellOutflow) && q < (A >> 1)) {
+    double N[A], dN[A][D];
+    shape(tf + q * A * NS, N, dN);
+    QFields<D, double> fn, fo;
+    interp<D>(N, dN, gy, fn);
+    interp<D>(N, dN, go, fo);
+#pragma unroll 1
+    for (int dir = 0; dir < NS; ++dir) {
+      typename ST::F fd;
+      seed_dir<D, G>(fn, cp, dir, fd);
+      Dual B[D];
+      qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, fo, B);
+#pragma unroll
+      for (int i = 0; i < D; ++i) sg[(GSZ + i * NS + dir) * T] = B[i].d;
+    }
+   }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+                                                         const double* __restrict__ y, const double* __restrict__ yo,
+                                                         double* __restrict__ J, const int* __restrict__ active,
+                                                         int colour) {
+  using L = JacLin<D>;
+  constexpr int A = L::A, C = L::C, NS = L::NS, T = L::T;
+  extern __shared__ double sm[];
+  double* tv = sm + (size_t)(L::GSZ + L::FSZ) * T;  // [q][b][NS]
+  double* tf = tv + L::TVSZ;                        // [face q][b][NS]
+  const int s = blockIdx.z;
+  if (active && !active[s]) return;  // uniform per block
+  const int cp = blockIdx.y;
+  const int lane = threadIdx.x;
+  const int q = lane & (A - 1);
+  // shape tables (uniform mesh: identical for every element)
+  if (lane < A + (A >> 1)) {
+    const bool face = lane >= A;
+    double xi[D], N[A], dN[A][D];
+    gauss_point<D>(face ? lane - A : lane, face, xi);
+    q1_shape<D>(xi, ph.ih, N, dN);
+    double* t = face ? tf + (lane - A) * A * NS : tv + lane * A * NS;
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      t[b * NS] = N[b];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[b * NS + 1 + k] = dN[b][k];
+    }
+  }
+  ElemIndex<D> e;
+  const bool valid = colour_element<D>(m, colour, blockIdx.x * L::EPB + lane / A, e);
+  const size_t vs = (size_t)C * m.g.np;
+  const bool outflow = valid && (e.cflag & kCellOutflow);
+  __syncthreads();  // shape tables
+  if (valid) {
+    const double* ys = y + s * vs;
+    const double* yos = yo + s * vs;
+    if (cp < D)
+      jaclin_point<D, 0>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+    else if (cp < 2 * D)
+      jaclin_point<D, 1>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+    else
+      jaclin_point<D, 2>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+  }
+  __syncthreads();
+  if (!valid) return;
+  // phase 2: this lane owns local node a = q of its element
+  const int a = q;
+  const int base = lane - q;  // lane of point 0 of this element
+  const bool ext = (e.ext_mask >> a) & 1;
+  double K[C][A];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int b = 0; b < A; ++b) K[c][b] = 0.0;
+#pragma unroll 1
+  for (int qq = 0; qq < A; ++qq) {
+    const double* g = sm + base + qq;
+    const double* ta = tv + (qq * A + a) * NS;
+    double ta_r[NS];
+#pragma unroll
+    for (int o = 0; o < NS; ++o) ta_r[o] = ta[o];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      // u rows of a node without the extension row: value-tested part only
+      const bool full = !(c >= D && c < 2 * D) || ext;
+      double h[NS];
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        double v = g[((c * NS + 0) * NS + i) * T] * ta_r[0];
+        if (full) {
+#pragma unroll
+          for (int o = 1; o < NS; ++o) v += g[((c * NS + o) * NS + i) * T] * ta_r[o];
+        }
+        h[i] = ph.wq * v;
+      }
+#pragma unroll
+      for (int b = 0; b < A; ++b) {
+        const double* tb = tv + (qq * A + b) * NS;
+        double v = h[0] * tb[0];
+#pragma unroll
+        for (int k = 1; k < NS; ++k) v += h[k] * tb[k];
+        K[c][b] += v;
+      }
+    }
+  }
+  if (outflow && cp < 2 * D) {
+#pragma unroll 1
+    for (int qq = 0; qq < (A >> 1); ++qq) {
+      const double* g = sm + (size_t)L::GSZ * T + base + qq;
+      const double na = tf[(qq * A + a) * NS];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        double h[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) h[i] = (-ph.wf) * (g[(c * NS + i) * T] * na);
+#pragma unroll
+        for (int b = 0; b < A; ++b) {
+          const double* tb = tf + (qq * A + b) * NS;
+          double v = h[0] * tb[0];
+#pragma unroll
+          for (int k = 1; k < NS; ++k) v += h[k] * tb[k];
+          K[c][b] += v;
+        }
+      }
+    }
+  }
+  // scatter: every old value is loaded before the first store, so the C 2^d
+  // read-modify-writes overlap instead of serialising behind possible aliasing
+  const int np = m.g.np;
+  double* o = J + (size_t)s * m.g.noff * C * C * np + (size_t)cp * np + e.node[a];
+  const bool solid = e.cflag & kCellSolid;  // solid cells own no p rows
+  auto idx = [&](int b, int c) {
+    const int di = (b & 1) - (a & 1);
+    const int dj = ((b >> 1) & 1) - ((a >> 1) & 1);
+    const int dk = D == 3 ? ((b >> 2) & 1) - ((a >> 2) & 1) : 0;
+    return ((size_t)offset_index(di, dj, dk, D) * C + c) * C * np;
+  };
+#pragma unroll
+  for (int b = 0; b < A; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (!(c == 2 * D && solid)) K[c][b] += o[idx(b, c)];
+#pragma unroll
+  for (int b = 0; b < A; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (!(c == 2 * D && solid)) o[idx(b, c)] = K[c][b];
 }
 
 // ---------------------------------------------------------------- Jacobian-vector product (matrix-free)
@@ -267,15 +520,7 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m
   if (valid) qp_integral<D, 1>(ph, st[s], e, q, y + s * vs, yo + s * vs, w + s * vs, m.g.np, 0, 0, R, dg);
   reduce_points<D>(R);
   if (!valid) return;
-  double* os = out + s * vs;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (c == 2 * D && (e.cflag & kCellSolid)) continue;
-    double v = R[0][c];
-#pragma unroll
-    for (int a = 1; a < A; ++a) v = (q == a) ? R[a][c] : v;
-    os[c * m.g.np + e.node[q]] += v;
-  }
+  scatter_rows<D>(R, q, e, out + s * vs, m.g.np);
 }
 
 // ---------------------------------------------------------------- fixed rows

@@ -116,6 +116,7 @@ struct pint_ctx {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
+  bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
@@ -374,11 +375,26 @@ struct Impl {
     const size_t ms = (size_t)ctx->g.noff * C * C * ctx->g.np;
     k_zero_active<<<vec_grid(ms, S), 256, 0, counted(ctx, st)>>>(L0.A, ms, mask);
     constexpr int A = 1 << D;
-    for (int c = 0; c < A; ++c) {
-      const int ne = colour_count(ctx, c);
-      if (ne == 0) continue;
-      k_jacobian_colour<D><<<dim3((ne * A + 127) / 128, A * C, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
-                                                                         c);
+    if (!ctx->jac_columns) {
+      using JL = JacLin<D>;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_jacobian_lin<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JL::smem);
+        attr = true;
+      }
+      for (int c = 0; c < A; ++c) {
+        const int ne = colour_count(ctx, c);
+        if (ne == 0) continue;
+        k_jacobian_lin<D><<<dim3((ne + JL::EPB - 1) / JL::EPB, C, S), JL::T, JL::smem, counted(ctx, st)>>>(
+            m, ctx->ph, ctx->d_st, y, yo, L0.A, mask, c);
+      }
+    } else {
+      for (int c = 0; c < A; ++c) {
+        const int ne = colour_count(ctx, c);
+        if (ne == 0) continue;
+        k_jacobian_colour<D><<<dim3((ne * A + 127) / 128, A * C, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
+                                                                           c);
+      }
     }
     k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, L0.A, mask);
     PINT_LAUNCHED();
@@ -1100,6 +1116,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
       ctx->num_sms = sms;
   }
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
+  ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
@@ -1119,6 +1136,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   double wq = 1.0, wf = 1.0;
   for (int m = 0; m < 3; ++m) {
     ph.h[m] = m < ctx->D ? desc->extent[m] / desc->cells[m] : 1.0;
+    ph.ih[m] = 1.0 / ph.h[m];
     if (m < ctx->D) wq *= 0.5 * ph.h[m];
     if (m >= 1 && m < ctx->D) wf *= 0.5 * ph.h[m];
   }

@@ -89,6 +89,7 @@ struct StepScalars {
 struct Phys {
   double rho_f, rnu, rho_s, mu, lam;
   double h[3];
+  double ih[3];  // 1 / h (shape gradients multiply, no fp64 division)
   double wq;     // volume quadrature weight per point
   double wf;     // outflow face quadrature weight per point
 };
