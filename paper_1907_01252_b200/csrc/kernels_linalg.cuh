@@ -1212,23 +1212,33 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __rest
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
   const double* vs = V + s * per_slice;
-  double acc[kMdotMax];
+  // basis vectors in groups of 4 (few registers -> full occupancy, 16 loads in
+  // flight per thread); per vector the element order is the same as one pass
+  constexpr int PER = kRedChunk / kRedThreads;
+  double we[PER];
 #pragma unroll
-  for (int v = 0; v < kMdotMax; ++v) acc[v] = 0.0;
-  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
-    const size_t e = base + i;
-    if (e >= per_slice) break;
-    const double we = ws[e];
-#pragma unroll
-    for (int v = 0; v < kMdotMax; ++v)
-      if (v < nv) acc[v] = fma(__ldg(vs + v * vstride + e), we, acc[v]);
+  for (int k = 0; k < PER; ++k) {
+    const size_t e = base + threadIdx.x + k * kRedThreads;
+    we[k] = e < per_slice ? ws[e] : 0.0;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int v0 = 0; v0 < nv; v0 += 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int v = 0; v < kMdotMax; ++v) {
-    if (v >= nv) break;
-    const double x = warp_sum(acc[v]);
-    if (lane == 0) sh[wid][v] = x;
+    for (int k = 0; k < PER; ++k) {
+      const size_t e = base + threadIdx.x + k * kRedThreads;
+      if (e < per_slice) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          if (v0 + g < nv) acc[g] = fma(__ldg(vs + (v0 + g) * vstride + e), we[k], acc[g]);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (v0 + g >= nv) break;
+      const double x = warp_sum(acc[g]);
+      if (lane == 0) sh[wid][v0 + g] = x;
+    }
   }
   __syncthreads();
   for (int v = threadIdx.x; v < nv; v += blockDim.x) {
