@@ -1075,6 +1075,122 @@ __global__ void __launch_bounds__(32 * WARPS) k_vanka_setup(Grid g, const double
   }
 }
 
+// Register-resident variant: ceil(L/32) warps per cell, thread t owns row t of
+// A_c in registers; in-place Gauss-Jordan sweeps with IMPLICIT partial pivoting
+// (no row swaps: the pivot of column p is the unused row with the largest
+// |a|, lowest index on ties -- deterministic).  Per pivot the owner publishes
+// its row through shared memory and every other row is updated from it; the
+// sweep leaves  A_c^{-1}[pos(t)][perm(c)] = M[t][c]  (perm: pivot row of
+// column p, pos: its inverse).  No augmented identity, no shared-memory
+// read-modify-write chains: ~10x faster than the warp-per-cell smem version
+// for the 56x56 blocks of 3-d.
+template <int D>
+struct VankaRows {
+  static constexpr int L = Cells<D>::L;
+  static constexpr int WPC = (L + 31) / 32;  // warps per cell
+  static constexpr int TPC = WPC * 32;       // threads per cell
+  static constexpr int CPB = D == 2 ? 4 : 2; // cells per block
+  static constexpr int T = CPB * TPC;
+};
+
+template <int D>
+__device__ __forceinline__ void cell_sync(int slot) {
+  if constexpr (VankaRows<D>::WPC == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(VankaRows<D>::TPC) : "memory");
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(VankaRows<D>::T) k_vanka_setup_rows(Grid g, const double* __restrict__ Ast,
+                                                                     float* __restrict__ Vinv,
+                                                                     const int* __restrict__ active) {
+  using VR = VankaRows<D>;
+  constexpr int L = VR::L, C = Cells<D>::C, A = Cells<D>::A, WPC = VR::WPC, CPB = VR::CPB;
+  __shared__ double prow[2][CPB][L];
+  __shared__ double cval[2][CPB][WPC];
+  __shared__ int cidx[2][CPB][WPC];
+  __shared__ int perm[CPB][L];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int slot = threadIdx.x / VR::TPC;
+  const int t = threadIdx.x % VR::TPC;  // my row
+  const int lane = threadIdx.x & 31, wic = t >> 5;
+  const int ncell = num_cells(g);
+  const int cell = blockIdx.x * CPB + slot;
+  if (cell >= ncell) return;  // the cell's threads leave together (named barriers are per cell)
+  const bool has = t < L;
+  int nodes[A];
+  cell_nodes<D>(g, cell, nodes);
+  const int np = g.np;
+  const double* As = Ast + (size_t)s * g.noff * C * C * np;
+  double row[L];
+  {
+    const int a = has ? t / C : 0, ca = has ? t % C : 0;
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+      const int b = c / C, cb = c % C;
+      const int di = (b & 1) - (a & 1), dj = ((b >> 1) & 1) - ((a >> 1) & 1);
+      const int dk = D == 3 ? ((b >> 2) & 1) - ((a >> 2) & 1) : 0;
+      row[c] = has ? As[(((size_t)offset_index(di, dj, dk, D) * C + ca) * C + cb) * np + nodes[a]] : 0.0;
+    }
+  }
+  bool used = !has;
+  int mypos = 0;
+#pragma unroll 1
+  for (int p = 0; p < L; ++p) {
+    const int buf = p & 1;
+    double ap = 0.0;
+#pragma unroll
+    for (int c = 0; c < L; ++c) ap = (c == p) ? row[c] : ap;
+    // argmax over unused rows: value desc, row index asc
+    double bv = used ? -1.0 : fabs(ap);
+    int bi = used ? 0x7fffffff : t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if constexpr (WPC > 1) {
+      if (lane == 0) { cval[buf][slot][wic] = bv; cidx[buf][slot][wic] = bi; }
+      cell_sync<D>(slot);
+#pragma unroll
+      for (int w = 0; w < WPC; ++w) {
+        const double ov = cval[buf][slot][w];
+        const int oi = cidx[buf][slot][w];
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+    }
+    const bool mine = bi == t;
+    if (mine) {
+      used = true;
+      mypos = p;
+      perm[slot][p] = t;
+#pragma unroll
+      for (int c = 0; c < L; ++c) prow[buf][slot][c] = row[c];
+    }
+    cell_sync<D>(slot);
+    const double* pr = prow[buf][slot];
+    const double d = pr[p];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+    if (mine) {
+#pragma unroll
+      for (int c = 0; c < L; ++c) row[c] = (c == p) ? inv : row[c] * inv;
+    } else if (has) {
+      const double f = ap;
+#pragma unroll
+      for (int c = 0; c < L; ++c) row[c] = (c == p) ? -f * inv : row[c] - f * (pr[c] * inv);
+    }
+  }
+  cell_sync<D>(slot);
+  if (!has) return;
+  float* Vs = Vinv + (size_t)s * L * L * ncell + cell;
+#pragma unroll
+  for (int c = 0; c < L; ++c) Vs[(size_t)(mypos * L + perm[slot][c]) * ncell] = (float)row[c];
+}
+
 // y_c = A_c^{-1} r_c ; thread = (cell, local row); block (CELLS, L)
 template <int D, int CELLS>
 __global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, const float* __restrict__ Vinv,

@@ -117,6 +117,7 @@ struct pint_ctx {
   bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
+  bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
@@ -449,7 +450,11 @@ struct Impl {
         k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, counted(ctx, st)>>>(F.g, L.g, F.A, L.A, mask);
       }
       const bool last_dense = ctx->coarse_dense && l == nl - 1;
-      if (ko->smoother == 1 && !last_dense) {
+      if (ko->smoother == 1 && !last_dense && !ctx->vanka_smem) {
+        using VR = VankaRows<D>;
+        k_vanka_setup_rows<D><<<dim3((L.ncell + VR::CPB - 1) / VR::CPB, S), VR::T, 0, counted(ctx, st)>>>(
+            L.g, L.A, L.vinv, mask);
+      } else if (ko->smoother == 1 && !last_dense) {
         constexpr int W = D == 2 ? 4 : 2;
         constexpr int Lc = Cells<D>::L;
         const size_t smem = (size_t)W * (Lc * 2 * Lc + Lc) * sizeof(double);
@@ -1117,6 +1122,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   }
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
+  ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
