@@ -65,18 +65,25 @@ __device__ __forceinline__ double ld_nc(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ float ld_nc(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 // One block-stencil row: sum_off sum_cb A[off][ca][cb][n] x[cb][nb(off)].
 // Latency-bound at the small configs (c1/c2 operators are L2-resident), so
 // all 2*C*NOFF loads of the row are put in flight before any FMA.
-template <int D, int BATCH>
-__device__ __forceinline__ double stencil_row(const double* __restrict__ Arow, const double* __restrict__ xs, int np,
+template <int D, int BATCH, typename MT = double>
+__device__ __forceinline__ double stencil_row(const MT* __restrict__ Arow, const double* __restrict__ xs, int np,
                                               const int (&nbs)[D == 2 ? 9 : 27]) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   double part[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int o0 = 0; o0 < NOFF; o0 += BATCH) {
-    double a[BATCH][C], xv[BATCH][C];
+    MT a[BATCH][C];
+    double xv[BATCH][C];
 #pragma unroll
     for (int q = 0; q < BATCH; ++q)
 #pragma unroll
@@ -87,9 +94,22 @@ __device__ __forceinline__ double stencil_row(const double* __restrict__ Arow, c
 #pragma unroll
     for (int q = 0; q < BATCH; ++q)
 #pragma unroll
-      for (int cb = 0; cb < C; ++cb) part[q % 3] = fma(a[q][cb], xv[q][cb], part[q % 3]);
+      for (int cb = 0; cb < C; ++cb) part[q % 3] = fma((double)a[q][cb], xv[q][cb], part[q % 3]);
   }
   return (part[0] + part[1]) + part[2];
+}
+
+// fp32 copy of a block-stencil operator (preconditioner-side residuals only)
+__global__ void k_to_f32(const double* __restrict__ A, float* __restrict__ A32, size_t per_slice,
+                         const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const double2* src = reinterpret_cast<const double2*>(A + s * per_slice);
+  float2* dst = reinterpret_cast<float2*>(A32 + s * per_slice);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice / 2; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(src + i);
+    dst[i] = make_float2((float)v.x, (float)v.y);
+  }
 }
 
 // ---------------------------------------------------------------- generic vector kernels
@@ -262,8 +282,8 @@ struct StencilOcc {
   static constexpr int value = BATCH >= 9 ? 1 : (D == 2 ? 4 : 2);
 };
 
-template <int D, bool RESID, int BATCH>
-__global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value)) k_spmv(Grid g, const double* __restrict__ A,
+template <int D, bool RESID, int BATCH, typename MT = double>
+__global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value)) k_spmv(Grid g, const MT* __restrict__ A,
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ y,
                                                           const int* __restrict__ active) {
@@ -276,11 +296,11 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
   const int ca = threadIdx.y;
   const int np = g.np;
   const size_t vs = (size_t)C * np;
-  const double* As = A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
+  const MT* As = A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
   const double* xs = x + s * vs;
   int nbs[NOFF];
   stencil_neighbours<D>(g, n, nbs);
-  const double acc = stencil_row<D, BATCH>(As, xs, np, nbs);
+  const double acc = stencil_row<D, BATCH, MT>(As, xs, np, nbs);
   const size_t o = s * vs + (size_t)ca * np + n;
   y[o] = RESID ? b[o] - acc : acc;
 }

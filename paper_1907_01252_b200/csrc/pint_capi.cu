@@ -44,6 +44,7 @@ struct Level {
   double* xb = nullptr;
   double* res = nullptr;
   double* sol = nullptr;   // coarse-level V-cycle output (l > 0)
+  float* A32 = nullptr;    // level 0 only: fp32 copy of A for the V-cycle's residuals (preconditioner only)
   float* vinv = nullptr;   // Vanka cell inverses [S][L*L][ncell], fp32 storage (preconditioner only)
   double* ycell = nullptr; // Vanka cell corrections [S][L][ncell]
   int ncell = 0;
@@ -398,8 +399,22 @@ struct Impl {
       }
     }
     k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, L0.A, mask);
+    if (L0.A32) k_to_f32<<<vec_grid(ms / 2, S), 256, 0, counted(ctx, st)>>>(L0.A, L0.A32, ms, mask);
     PINT_LAUNCHED();
     return PINT_OK;
+  }
+
+  // V-cycle residual r = b - A x on level L (fp32 operator copy on level 0 when present)
+  static void vc_resid(pint_ctx* ctx, const Level& L, int S, const double* x, const double* b, double* r,
+                       const int* mask, cudaStream_t st) {
+    const bool w = wide(L.g.nn, S);
+    if (L.A32) {
+      if (w) k_spmv<D, true, 3, float><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A32, x, b, r, mask);
+      else k_spmv<D, true, 9, float><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A32, x, b, r, mask);
+    } else {
+      if (w) k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, b, r, mask);
+      else k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, b, r, mask);
+    }
   }
 
   static int jvp(pint_ctx* ctx, int S, const double* y, const double* yo, const double* w, double* out,
@@ -535,12 +550,7 @@ struct Impl {
       constexpr int CELLS = D == 2 ? 16 : 8;
       const double* r = b;
       if (!first) {
-        if (wide(L.g.nn, S))
-          k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, xin, b, L.res,
-                                                                                            mask);
-        else
-          k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, xin, b, L.res,
-                                                                                            mask);
+        vc_resid(ctx, L, S, xin, b, L.res, mask, st);
         r = L.res;
       }
       const bool prof = ctx->prof && &L == &ctx->lv[0];
@@ -648,10 +658,7 @@ struct Impl {
       smooth(ctx, L, S, b, cur, nxt, mask, st, false);
       std::swap(cur, nxt);
     }
-    if (wide(L.g.nn, S))
-      k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
-    else
-      k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, cur, b, L.res, mask);
+    vc_resid(ctx, L, S, cur, b, L.res, mask, st);
     k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
@@ -1244,6 +1251,21 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->d_work_bytes, (size_t)1);
   ALLOC(ctx->cpart, (size_t)S * kTailCluster * kMaxBasis);
 #undef ALLOC
+  // optional fp32 copy of the level-0 operator for the V-cycle residuals (half
+  // the bytes of the two level-0 SpMVs of every cycle); skipped when it does
+  // not fit next to the rest of the workspace (or with PINT_A32=0)
+  if (!(std::getenv("PINT_A32") && std::getenv("PINT_A32")[0] == '0')) {
+    Level& L0 = ctx->lv[0];
+    const size_t cnt = (size_t)S * L0.g.noff * C * C * L0.g.np;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && cnt * sizeof(float) + (size_t(2) << 30) < free_b) {
+      if (dalloc(ctx, &L0.A32, cnt) != PINT_OK) {
+        L0.A32 = nullptr;
+        ctx->err.clear();
+        cudaGetLastError();
+      }
+    }
+  }
   if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
       cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess) {
     ctx->err = "cudaMallocHost failed";
