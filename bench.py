@@ -9,11 +9,14 @@ Parareal propagates).  Inputs are resident in HBM when the timed region
 starts; L2 (126 MB) is flushed before every timed step (a 256 MB write).
 
 ``value``  : slices x fine steps / device time (CUDA events, max over ranks)
-``e2e``    : the same through the public host-State API (``advance_batch``)
-             with pinned H2D of the inputs and D2H of the results each step
-``roofline``: the level-0 multigrid smoother sweep (block-stencil
-             SpMV + node-block Jacobi), the dominant kernel, timed live with
-             CUDA events inside the timed region
+``e2e``    : the same through the public host-State API (``advance_batch``:
+             host States in, host States out; H2D of the inputs and D2H of
+             the results inside every timed step)
+``roofline``: the level-0 cell-patch Vanka solve (k_vanka_cell), the
+             largest HBM-class kernel of the step, timed with CUDA events
+             around every launch in a separate profiled step; ``traffic`` is
+             its DRAM bytes per launch from the committed ncu --set full
+             capture (profiles/r01_ncu_traffic.json)
 ``cpu_baseline``: the CPU oracle (numpy/scipy port of the same CN step,
              oracle/fsi_oracle.py) on a bounded sample of the same workload.
 
@@ -106,6 +109,18 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _traffic(config, kernel):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    --set full capture (tools/ncu_traffic.py), or None when there is none."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            e = json.load(f)[config]
+    except Exception:
+        return None
+    base = kernel.split(" ")[0]
+    return e["dram_bytes_per_launch"] if base.split("<")[0] in e["kernel"] else None
 
 
 def _dist():
@@ -267,18 +282,14 @@ def run_ours(args):
     prof_step_ms = pe0.elapsed_time(pe1)
     dev.profile(0)
 
-    # ---- e2e through the public host-State API (pinned H2D + D2H each step)
+    # ---- e2e through the public host-State API (H2D + D2H inside every step)
+    # the reference-facing call: advance_batch(host States, t_ends) -> host States
     host_states = [s0.with_values(v, time=t) for v, t in zip(dev.to_host(X0), t0)]
-    pinned_in = torch.from_numpy(np.stack([s.values for s in host_states])).pin_memory()
     e2e_times = []
     for it in range(1 + args.steps):
         torch.cuda.synchronize()
         a = time.perf_counter()
-        y = dev.empty(L)
-        y[:, :, :dev.nn].copy_(pinned_in.view(L, dev.C, dev.nn), non_blocking=True)
-        res = F.advance_device(y, t0, t1)
-        vals = res[:, :, :dev.nn].cpu()
-        outs = [s.with_values(vals[l].reshape(-1).numpy(), time=t1[l]) for l, s in enumerate(host_states)]
+        outs = F.advance_batch(host_states, t1)
         torch.cuda.synchronize()
         if it > 0:
             e2e_times.append(time.perf_counter() - a)
@@ -299,7 +310,7 @@ def run_ours(args):
     roofline = {
         "kernel": kname,
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "peak_kind": peak_kind, "traffic": None,
+        "peak_kind": peak_kind, "traffic": _traffic(args.config, kname),
         "avg_launch_us": 1e3 * prof["kernel_ms"] / max(1, prof["kernel_launches"]),
         "launches": prof["kernel_launches"],
         "share_of_step": prof["kernel_ms"] / prof_step_ms,
