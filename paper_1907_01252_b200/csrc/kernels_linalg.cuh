@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, cons
   constexpr int L = Cells<D>::L;
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
-  __shared__ double rc[L][CELLS];
+  __shared__ float rc[L][CELLS];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   if (work && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(work, 1ULL);
@@ -1234,16 +1234,17 @@ __global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, cons
     int nodes[A];
     cell_nodes<D>(g, cell, nodes);
     const int a = row / C, ca = row % C;
-    rc[row][threadIdx.x] = r[(size_t)s * C * np + (size_t)ca * np + nodes[a]];
+    rc[row][threadIdx.x] = (float)r[(size_t)s * C * np + (size_t)ca * np + nodes[a]];
   }
   __syncthreads();
   if (!live) return;
   const float* Vs = Vinv + (size_t)s * L * L * ncell + (size_t)row * L * ncell + cell;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // fp32 arithmetic: the inverse is fp32 storage and the product is a
+  // smoother correction inside the preconditioner (FGMRES absorbs the rounding)
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int j = 0; j < L; ++j)
-    acc[j & 3] = fma((double)__ldg(Vs + (size_t)j * ncell), rc[j][threadIdx.x], acc[j & 3]);
-  y[(size_t)s * L * ncell + (size_t)row * ncell + cell] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  for (int j = 0; j < L; ++j) acc[j & 3] = fmaf(__ldg(Vs + (size_t)j * ncell), rc[j][threadIdx.x], acc[j & 3]);
+  y[(size_t)s * L * ncell + (size_t)row * ncell + cell] = (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
 }
 
 // x_out = x_in + omega / count(n) * sum_{cells c containing n} y_c[local(n)]
@@ -1531,13 +1532,13 @@ __device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const 
     int nodes[A];
     cell_nodes<D>(L.g, cell, nodes);
     const float* Vs = L.vinv + (size_t)s * LL * LL * ncell + (size_t)row * LL * ncell + cell;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // fp32 as in k_vanka_cell
 #pragma unroll
     for (int j = 0; j < LL; ++j) {
-      const double rj = r[(size_t)s * C * np + (size_t)(j % C) * np + nodes[j / C]];
-      acc[j & 3] = fma((double)__ldg(Vs + (size_t)j * ncell), rj, acc[j & 3]);
+      const float rj = (float)r[(size_t)s * C * np + (size_t)(j % C) * np + nodes[j / C]];
+      acc[j & 3] = fmaf(__ldg(Vs + (size_t)j * ncell), rj, acc[j & 3]);
     }
-    L.ycell[(size_t)s * LL * ncell + (size_t)row * ncell + cell] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    L.ycell[(size_t)s * LL * ncell + (size_t)row * ncell + cell] = (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
   }
 }
 
