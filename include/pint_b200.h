@@ -76,7 +76,9 @@ typedef struct pint_krylov_opts {
   int32_t coarse_sweeps; /* smoothing sweeps when the coarsest level is too big for a dense inverse */
   int32_t smoother;      /* 0 node-block Jacobi, 1 cell-patch Vanka (default) */
   int32_t precond_reuse; /* k >= 1: rebuild a slice's multigrid hierarchy at its first Newton iteration
-                            every k steps; 0: every Newton iteration */
+                            every k steps, or earlier when the slice's first-iteration Krylov count
+                            grew past 1.5x (+2) the count right after its last build; 0: every
+                            Newton iteration */
   double rtol_first;     /* inexact-Newton forcing of the first Newton iteration of a step (0: use rtol);
                             later iterations use rtol, never below a tenth of the Newton target */
 } pint_krylov_opts;

@@ -120,6 +120,8 @@ struct pint_ctx {
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
+  std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
+  std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
   bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a cluster
@@ -929,21 +931,24 @@ struct Impl {
       if (nrun == 0) break;
       PINT_CHECK(cudaMemcpyAsync(ctx->d_active, running.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
       PINT_TRY(assemble(ctx, S, y, yo, ctx->d_active, st));
-      // the multigrid hierarchy is rebuilt at the first Newton iteration of every
-      // step (or every iteration with precond_reuse = 0) -- per-step policy, so a
-      // slice's preconditioner never depends on the batch
       // multigrid hierarchy per slice: rebuilt every Newton iteration
-      // (precond_reuse = 0) or at the first Newton iteration of every
-      // precond_reuse-th step since the slice's last build -- a per-slice rule,
-      // so a slice's preconditioner never depends on the batch
+      // (precond_reuse = 0), or at the first Newton iteration of a step when
+      // precond_reuse steps have passed since the slice's last build OR its
+      // previous first-iteration solve needed more than 1.5x (+2) the Krylov
+      // iterations of the first solve after that build (the operator drifted
+      // away from the preconditioner).  Per-slice rule from the slice's own
+      // counts, so a slice's preconditioner never depends on the batch.
+      std::vector<int> built_now(S, 0);
       {
         std::vector<int> need(S, 0);
         int nneed = 0;
         for (int s = 0; s < S; ++s) {
           if (!running[s]) continue;
           const int last = ctx->built_step[s];
-          need[s] = ko->precond_reuse <= 0 || last < 0 || (it == 0 && step - last >= ko->precond_reuse);
-          if (need[s]) { ctx->built_step[s] = step; ++nneed; }
+          const bool drift = ctx->base_its[s] >= 0 && 2 * ctx->first_its[s] > 3 * ctx->base_its[s] + 4;
+          need[s] = ko->precond_reuse <= 0 || last < 0 ||
+                    (it == 0 && (step - last >= ko->precond_reuse || drift));
+          if (need[s]) { ctx->built_step[s] = step; built_now[s] = it == 0; ++nneed; }
         }
         if (nneed) {
           PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, need.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
@@ -961,8 +966,14 @@ struct Impl {
       }
       PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, lin_rtol.data(), lin_atol.data(), klin.data(),
                      kres.data(), st));
-      for (int s = 0; s < S; ++s)
-        if (running[s]) kit[s] += klin[s];
+      for (int s = 0; s < S; ++s) {
+        if (!running[s]) continue;
+        kit[s] += klin[s];
+        if (it == 0) {
+          ctx->first_its[s] = klin[s];
+          if (built_now[s]) ctx->base_its[s] = klin[s];
+        }
+      }
       if (ctx->verbose)
         for (int s = 0; s < S; ++s)
           if (running[s])
@@ -1024,6 +1035,8 @@ struct Impl {
     std::vector<double> t(t0, t0 + S);
     std::vector<int> nit(S, 0), kit(S, 0), status(S, PINT_OK);
     ctx->built_step.assign(ctx->maxS, -1);
+    ctx->base_its.assign(ctx->maxS, -1);
+    ctx->first_its.assign(ctx->maxS, 0);
     std::vector<double> ft(S, 0.0);
     int nmax = 0;
     for (int s = 0; s < S; ++s) nmax = std::max(nmax, nsteps[s]);
