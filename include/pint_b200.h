@@ -90,6 +90,9 @@ int pint_destroy(pint_ctx* ctx);
 const char* pint_last_error(const pint_ctx* ctx);
 /* nn nodes, np padded stride, C dofs/node, number of multigrid levels */
 int pint_sizes(const pint_ctx* ctx, int32_t* nn, int32_t* np, int32_t* C, int32_t* levels);
+/* 1 when the V-cycle residuals read an fp32 copy of the level-0 operator (allocated at create
+ * when it fits next to the workspace; PINT_A32=0 disables it), else 0 */
+int pint_level0_fp32(const pint_ctx* ctx, int32_t* enabled);
 /* node flags (uint8 per node: 1 solid-touch, 2 fluid-touch, 4 Dirichlet v, 8 Dirichlet u)
  * and cell flags (1 solid, 2 outflow) into host buffers, for cross-checks */
 int pint_flags(const pint_ctx* ctx, uint8_t* node_flags, uint8_t* cell_flags);

@@ -32,7 +32,7 @@ STATUS_NAMES = {
 
 # every symbol include/pint_b200.h declares (tests check the export table)
 EXPORTS = (
-    "pint_create", "pint_destroy", "pint_last_error", "pint_sizes", "pint_flags",
+    "pint_create", "pint_destroy", "pint_last_error", "pint_sizes", "pint_level0_fp32", "pint_flags",
     "pint_propagate", "pint_residual", "pint_jvp", "pint_assemble", "pint_jacobian_blocks",
     "pint_spmv", "pint_precond_setup", "pint_precond_apply", "pint_linear_solve",
     "pint_parareal_precorrect", "pint_parareal_correct_one", "pint_profile", "pint_profile_read",
@@ -96,6 +96,7 @@ _SIGNATURES = {
     "pint_destroy": (_I, [_P]),
     "pint_last_error": (ctypes.c_char_p, [_P]),
     "pint_sizes": (_I, [_P, _IP, _IP, _IP, _IP]),
+    "pint_level0_fp32": (_I, [_P, _IP]),
     "pint_flags": (_I, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_uint8)]),
     "pint_propagate": (_I, [_P, _I, _P, _P, _DP, _DP, _IP, _D, _D, ctypes.POINTER(NewtonOpts),
                             ctypes.POINTER(KrylovOpts), _IP, _IP, _IP, _DP, _P]),

@@ -720,7 +720,8 @@ struct Impl {
     for (int l = from; l < nl; ++l) {
       const Level& L = ctx->lv[l];
       const unsigned long long V = (unsigned long long)C * 8 * L.g.nn;
-      const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * 8 * L.g.nn;
+      // the V-cycle residuals read the fp32 copy of level 0 when it exists
+      const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * (L.A32 ? 4 : 8) * L.g.nn;
       if (l == nl - 1 && ctx->coarse_dense) {
         total += (unsigned long long)ctx->dense_n * ctx->dense_n * 4 + 2 * V;  // fp32 inverse
         continue;
@@ -1315,6 +1316,12 @@ int pint_sizes(const pint_ctx* ctx, int32_t* nn, int32_t* np, int32_t* C, int32_
   if (np) *np = ctx->g.np;
   if (C) *C = ctx->C;
   if (levels) *levels = (int32_t)ctx->lv.size();
+  return PINT_OK;
+}
+
+int pint_level0_fp32(const pint_ctx* ctx, int32_t* enabled) {
+  if (!ctx || !enabled) return PINT_INVALID_ARG;
+  *enabled = ctx->lv.empty() || !ctx->lv[0].A32 ? 0 : 1;
   return PINT_OK;
 }
 

@@ -206,6 +206,9 @@ class FSIDevice:
         nn, np_, C, lv = (ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32())
         self.lib.pint_sizes(handle, ctypes.byref(nn), ctypes.byref(np_), ctypes.byref(C), ctypes.byref(lv))
         self.nn, self.np, self.C, self.levels = nn.value, np_.value, C.value, lv.value
+        f32 = ctypes.c_int32()
+        self.lib.pint_level0_fp32(handle, ctypes.byref(f32))
+        self.level0_fp32 = bool(f32.value)  # V-cycle residuals read the fp32 level-0 copy
         assert self.nn == problem.num_nodes and self.C == problem.dofs_per_node
 
     def __del__(self):

@@ -89,14 +89,17 @@ def main():
             dev.precond_setup(S, krylov)
             # V(1,1) level-0 traffic: first sweep (inverses + r + y) + residual SpMV + post sweep
             # (SpMV + inverses + gather) + restriction/prolongation; coarse levels add ~1/3
-            lvl0 = (ncell * (400 * 4 + 160) + V) * 2 + (Ablk + 2 * V) * 2 + 4 * V
+            # (the two V-cycle SpMVs read the fp32 level-0 copy when the context holds one)
+            Avc = Ablk // 2 if dev.level0_fp32 else Ablk
+            lvl0 = (ncell * (400 * 4 + 160) + V) * 2 + (Avc + 2 * V) * 2 + 4 * V
             res["vcycle"] = (timed(lambda: dev.precond_apply(w, out=out), flush), int(lvl0 * 4 / 3))
-            # one flexible-GMRES(1) solve = Arnoldi step (V-cycle + SpMV + CGS2/norm on 2 vectors)
+            # one flexible-GMRES(1) solve = Arnoldi step (V-cycle + fp64 SpMV + CGS2/norm on 2 vectors)
             # + x += Z y + the true-residual SpMV (no second V-cycle: z_j is stored)
             res["gmres_iteration"] = (timed(lambda: dev.linear_solve(w, krylov, out=out), flush),
                                       int(lvl0 * 4 / 3) + 2 * (Ablk + 2 * V) + 16 * V)
             line = {"config": "c5", "size": size, "mesh": list(C5_MESHES[size]), "slices": S,
                     "dofs_per_slice": P.num_dofs, "seed": a.seed, "peak_gbs": pk, "peak_kind": pk_kind,
+                    "level0_fp32": dev.level0_fp32,
                     "kernels": {}}
             for name, (ms, bytes_per_slice) in res.items():
                 gbs = S * bytes_per_slice / 1e9 / (ms / 1e3)
