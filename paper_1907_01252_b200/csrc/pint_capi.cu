@@ -122,6 +122,7 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
+  int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
   bool tail_cluster = true;  // PINT_TAIL_CLUSTER=0: one CTA per slice instead of a cluster
@@ -946,7 +947,8 @@ struct Impl {
         for (int s = 0; s < S; ++s) {
           if (!running[s]) continue;
           const int last = ctx->built_step[s];
-          const bool drift = ctx->base_its[s] >= 0 && 2 * ctx->first_its[s] > 3 * ctx->base_its[s] + 4;
+          const bool drift = ctx->drift_num > 0 && ctx->base_its[s] >= 0 &&
+                             2 * ctx->first_its[s] > ctx->drift_num * ctx->base_its[s] + 4;
           need[s] = ko->precond_reuse <= 0 || last < 0 ||
                     (it == 0 && (step - last >= ko->precond_reuse || drift));
           if (need[s]) { ctx->built_step[s] = step; built_now[s] = it == 0; ++nneed; }
@@ -1144,6 +1146,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
   ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
+  if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
