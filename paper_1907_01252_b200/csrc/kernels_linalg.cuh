@@ -398,61 +398,56 @@ __device__ __forceinline__ double pweight(int fine, int coarse) {
 
 // bc[c][I] = sum_i P(i, I) rf[c][i]
 template <int D>
-__global__ void k_restrict(Grid gf, Grid gc, const double* __restrict__ rf, double* __restrict__ bc,
-                           const int* __restrict__ active) {
-  constexpr int C = 2 * D + 1;
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
+                                                              double* __restrict__ bc,
+                                                              const int* __restrict__ active) {
+  // thread = (coarse node, component): block (32, C), so the 3^d fine loads of
+  // a thread are independent of its C-1 siblings' (more loads in flight)
   const int s = blockIdx.y;
   if (active && !active[s]) return;
-  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int I = blockIdx.x * 32 + threadIdx.x;
   if (I >= gc.nn) return;
+  const int c = threadIdx.y;
   int ci, cj, ck;
   node_coords(gc, I, ci, cj, ck);
-  double acc[C];
+  double acc = 0.0;
+  const double* rs = rf + (size_t)s * (2 * D + 1) * gf.np + (size_t)c * gf.np;
 #pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.0;
-  const double* rs = rf + (size_t)s * C * gf.np;
   for (int dk = (D == 3 ? -1 : 0); dk <= (D == 3 ? 1 : 0); ++dk)
+#pragma unroll
     for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
       for (int di = -1; di <= 1; ++di) {
         const int fi = 2 * ci + di, fj = 2 * cj + dj, fk = 2 * ck + dk;
         if (fi < 0 || fi >= gf.n[0] || fj < 0 || fj >= gf.n[1] || fk < 0 || fk >= gf.n[2]) continue;
         const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
-        const int f = node_index(gf, fi, fj, fk);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc[c] += w * rs[c * gf.np + f];
+        acc += w * rs[node_index(gf, fi, fj, fk)];
       }
-  double* bs = bc + (size_t)s * C * gc.np;
-#pragma unroll
-  for (int c = 0; c < C; ++c) bs[c * gc.np + I] = acc[c];
+  bc[(size_t)s * (2 * D + 1) * gc.np + (size_t)c * gc.np + I] = acc;
 }
 
-// xf[c][i] += sum_I P(i, I) ec[c][I]
+// xf[c][i] += sum_I P(i, I) ec[c][I]; thread = (fine node, component), block (32, C)
 template <int D>
-__global__ void k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec, double* __restrict__ xf,
-                              const int* __restrict__ active) {
-  constexpr int C = 2 * D + 1;
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec,
+                                                                 double* __restrict__ xf,
+                                                                 const int* __restrict__ active) {
   const int s = blockIdx.y;
   if (active && !active[s]) return;
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.x * 32 + threadIdx.x;
   if (f >= gf.nn) return;
+  const int c = threadIdx.y;
   int fi, fj, fk;
   node_coords(gf, f, fi, fj, fk);
-  double acc[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.0;
-  const double* es = ec + (size_t)s * C * gc.np;
+  double acc = 0.0;
+  const double* es = ec + (size_t)s * (2 * D + 1) * gc.np + (size_t)c * gc.np;
   const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
   for (int ck = k0; ck <= (D == 3 ? k0 + (fk & 1) : k0); ++ck)
     for (int cj = j0; cj <= j0 + (fj & 1); ++cj)
       for (int ci = i0; ci <= i0 + (fi & 1); ++ci) {
         const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
-        const int I = node_index(gc, ci, cj, ck);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc[c] += w * es[c * gc.np + I];
+        acc += w * es[node_index(gc, ci, cj, ck)];
       }
-  double* xs = xf + (size_t)s * C * gf.np;
-#pragma unroll
-  for (int c = 0; c < C; ++c) xs[c * gf.np + f] += acc[c];
+  xf[(size_t)s * (2 * D + 1) * gf.np + (size_t)c * gf.np + f] += acc;
 }
 
 // Galerkin coarse operator Ac = P^T Af P; thread = (coarse node, coarse offset, row comp)

@@ -662,10 +662,10 @@ struct Impl {
       std::swap(cur, nxt);
     }
     vc_resid(ctx, L, S, cur, b, L.res, mask, st);
-    k_restrict<D><<<node_grid(Lc.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
+    k_restrict<D><<<row_grid(Lc.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
-    k_prolong_add<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, Lc.g, xc, cur, mask);
+    k_prolong_add<D><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, Lc.g, xc, cur, mask);
     for (int i = 0; i < post; ++i) {
       double* out = (i == post - 1) ? x : nxt;
       smooth(ctx, L, S, b, cur, out, mask, st, false);
