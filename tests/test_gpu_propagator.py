@@ -105,3 +105,42 @@ def test_newton_counters(cuda):
     assert gpu.steps_taken == 10
     assert gpu.newton_iterations >= 10
     assert abs(gpu.newton_iterations - cpu.newton_iterations) <= 3
+
+
+def _c1_window(krylov=None, env=None):
+    """One c1 fine window (25 CN steps from rest) through a fresh context."""
+    import os
+    from paper_1907_01252_b200.propagator import KrylovSettings, NewtonSettings, ThetaSettings, make_propagator
+    P = CONFIGS["c1"].problem
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        gpu = make_propagator(P, ThetaSettings(step=0.002, theta0=1.0, newton=NewtonSettings(**NEWTON)),
+                              krylov=krylov or KrylovSettings(), max_slices=1)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return gpu, gpu.advance(O.initial_state(P), 0.05)
+
+
+def test_preconditioner_precision_and_refresh_do_not_move_the_solution(cuda):
+    """The mixed-precision pieces (fp32 level-0 V-cycle operator, fp32 Vanka
+    solves) and the refresh period live inside the FGMRES preconditioner: the
+    converged window must agree with the fp64-operator / rebuild-every-Newton
+    variants and with the oracle to the solver tolerance."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = CONFIGS["c1"].problem
+    g32, a = _c1_window()
+    g64, b = _c1_window(env={"PINT_A32": "0"})
+    _, c = _c1_window(krylov=KrylovSettings(precond_reuse=0))
+    assert g32.device.level0_fp32 and not g64.device.level0_fp32
+    ref = O.OracleFSIPropagator(P, 0.002, theta0=1.0, newton=O.OracleNewtonSettings(**NEWTON)).advance(
+        O.initial_state(P), 0.05)
+    for x in (a, b, c):
+        errs = block_errors(P, x.values, ref.values)
+        assert max(errs.values()) <= 1e-8, errs
+    errs = block_errors(P, a.values, b.values)
+    assert max(errs.values()) <= 1e-9, errs
