@@ -122,6 +122,7 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
+  int tail_rows = 2048;         // PINT_TAIL_ROWS: first level of the fused V-cycle tail has <= this many rows
   int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
   int64_t tail_slice_launches = 0;  // profiled tail launches x slices (tail_first == 0)
@@ -503,7 +504,7 @@ struct Impl {
     ctx->tail_first = -1;
     if (ctx->use_tail && ko->smoother == 1 && nl <= kMaxLevels) {
       for (int l = 0; l < nl; ++l)
-        if ((size_t)ctx->lv[l].g.nn * C <= 2048) { ctx->tail_first = l; break; }
+        if ((size_t)ctx->lv[l].g.nn * C <= (size_t)ctx->tail_rows) { ctx->tail_first = l; break; }
       if (ctx->tail_first >= 0) {
         TailArgs& t = ctx->tail;
         for (int l = 0; l < nl; ++l) {
@@ -1147,6 +1148,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
   ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
+  if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {

@@ -179,3 +179,59 @@ def test_dense_coarsest_inverse_matches_direct_solve(devices, name):
         err = np.linalg.norm(X[s] - ref) / np.linalg.norm(ref)
         assert err <= 1e-5, (name, s, err)
         assert its[s] <= 4, (name, s, its[s])
+
+
+def _device_with_env(P, env, S=3):
+    import os
+    from paper_1907_01252_b200.propagator import FSIDevice
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return FSIDevice(P, max_slices=S)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", ["c1", "small3d"])
+def test_jacobian_formulations_agree(cuda, name):
+    """K2 by pointwise linearisation (1 + d dual passes per column component,
+    default) and K2 by one dual pass per Jacobian column (PINT_JAC=columns)
+    assemble the same block-stencil operator up to round-off."""
+    P = PROBLEMS[name]
+    S = 3
+    Y = random_states(P, S, 51)
+    Yo = random_states(P, S, 52)
+    k, th, t1 = _step_args(S)
+    blocks = []
+    for env in ({}, {"PINT_JAC": "columns"}):
+        dev = _device_with_env(P, env)
+        dev.assemble(dev.to_device(Y), dev.to_device(Yo), k, th, t1)
+        blocks.append(dev.jacobian_blocks(S).cpu().numpy())
+    scale = np.abs(blocks[1]).max()
+    assert np.abs(blocks[0] - blocks[1]).max() <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("name", ["c1", "small3d"])
+def test_vanka_setup_variants_agree(cuda, name):
+    """Register-row Gauss-Jordan with implicit pivoting (default) and the
+    warp-per-cell shared-memory version (PINT_VANKA_SETUP=smem) store the same
+    fp32 cell inverses up to fp32 rounding: one V-cycle agrees to 1e-5."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 61, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 62, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs = []
+    for env in ({}, {"PINT_VANKA_SETUP": "smem"}):
+        dev = _device_with_env(P, env, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+    for s in range(S):
+        assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[1][s]), (name, s)
