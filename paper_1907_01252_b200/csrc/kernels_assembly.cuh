@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_residual_colour(Mesh
                                                         const double* __restrict__ y, const double* __restrict__ yo,
                                                         double* __restrict__ r, int* __restrict__ degen,
                                                         const int* __restrict__ active, int colour) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   const int s = blockIdx.y;
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jacobian_colour(Mesh
                                                         const double* __restrict__ y, const double* __restrict__ yo,
                                                         double* __restrict__ J, const int* __restrict__ active,
                                                         int colour) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   const int s = blockIdx.z;
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(M
                                                          const double* __restrict__ y, const double* __restrict__ yo,
                                                          double* __restrict__ J, const int* __restrict__ active,
                                                          int colour) {
+  pdl_wait();
   using L = JacLin<D>;
   constexpr int A = L::A, C = L::C, NS = L::NS, T = L::T;
   extern __shared__ double sm[];
@@ -505,6 +508,7 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m
                                                    const double* __restrict__ y, const double* __restrict__ yo,
                                                    const double* __restrict__ w, double* __restrict__ out,
                                                    const int* __restrict__ active, int colour) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   const int s = blockIdx.y;
@@ -534,6 +538,7 @@ __device__ __forceinline__ bool row_fixed(uint8_t f, int c, int D) {
 template <int D>
 __global__ void k_fix_residual(MeshDev m, const StepScalars* __restrict__ st, const double* __restrict__ y,
                                double* __restrict__ r, const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   const int s = blockIdx.y;
   if (active && !active[s]) return;
@@ -553,6 +558,7 @@ __global__ void k_fix_residual(MeshDev m, const StepScalars* __restrict__ st, co
 // Jacobian rows of fixed dofs = identity rows
 template <int D>
 __global__ void k_fix_jacobian(MeshDev m, double* __restrict__ J, const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   const int s = blockIdx.y;
   if (active && !active[s]) return;
@@ -575,6 +581,7 @@ __global__ void k_fix_jacobian(MeshDev m, double* __restrict__ J, const int* __r
 template <int D>
 __global__ void k_fix_jvp(MeshDev m, const double* __restrict__ w, double* __restrict__ out,
                           const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   const int s = blockIdx.y;
   if (active && !active[s]) return;

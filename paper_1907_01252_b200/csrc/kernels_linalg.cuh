@@ -102,6 +102,7 @@ __device__ __forceinline__ double stencil_row(const MT* __restrict__ Arow, const
 // fp32 copy of a block-stencil operator (preconditioner-side residuals only)
 __global__ void k_to_f32(const double* __restrict__ A, float* __restrict__ A32, size_t per_slice,
                          const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double2* src = reinterpret_cast<const double2*>(A + s * per_slice);
@@ -114,6 +115,7 @@ __global__ void k_to_f32(const double* __restrict__ A, float* __restrict__ A32, 
 
 // ---------------------------------------------------------------- generic vector kernels
 __global__ void k_zero_active(double* __restrict__ x, size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   double* xs = x + s * per_slice;
@@ -123,6 +125,7 @@ __global__ void k_zero_active(double* __restrict__ x, size_t per_slice, const in
 
 __global__ void k_copy_active(double* __restrict__ dst, const double* __restrict__ src, size_t per_slice,
                               const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
@@ -132,6 +135,7 @@ __global__ void k_copy_active(double* __restrict__ dst, const double* __restrict
 // y = a_s * x + y  (a per slice)
 __global__ void k_axpy_slice(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ a,
                              double sign, size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double al = sign * a[s];
@@ -142,6 +146,7 @@ __global__ void k_axpy_slice(double* __restrict__ y, const double* __restrict__ 
 // out = x + lam_s * d
 __global__ void k_trial(double* __restrict__ out, const double* __restrict__ x, const double* __restrict__ d,
                         const double* __restrict__ lam, size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double l = lam[s];
@@ -152,6 +157,7 @@ __global__ void k_trial(double* __restrict__ out, const double* __restrict__ x, 
 // out = -x
 __global__ void k_negate(double* __restrict__ out, const double* __restrict__ x, size_t per_slice,
                          const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
@@ -161,6 +167,7 @@ __global__ void k_negate(double* __restrict__ out, const double* __restrict__ x,
 // out = x / a_s  (a_s == 0 -> out = 0)
 __global__ void k_scale_inv(double* __restrict__ out, const double* __restrict__ x, const double* __restrict__ a,
                             size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double al = a[s];
@@ -174,6 +181,7 @@ __global__ void k_scale_inv(double* __restrict__ out, const double* __restrict__
 __global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __restrict__ x, const double* __restrict__ y,
                                                             size_t per_slice, double* __restrict__ partial, int nblk,
                                                             const int* __restrict__ active) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
@@ -193,6 +201,7 @@ __global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __res
 // +inf if the slice flagged a degenerate mesh
 __global__ void k_dot_final(const double* __restrict__ partial, int nblk, double* __restrict__ out, int S, int take_sqrt,
                             const int* __restrict__ degen, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   if (active && !active[s]) return;
@@ -208,6 +217,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_partial(const double* __re
                                                              const double* __restrict__ w, int nv, size_t per_slice,
                                                              double* __restrict__ partial, int nblk, int maxv,
                                                              const int* __restrict__ active) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.z;
   const int v = blockIdx.y;
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_partial(const double* __re
 // h[s][i] (+)= sum_b partial[s][i][b]
 __global__ void k_mdot_final(const double* __restrict__ partial, int nblk, int nv, int maxv, double* __restrict__ h,
                              int hstride, int accumulate, int S, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.x;
   if (s >= S) return;
   if (active && !active[s]) return;
@@ -243,6 +254,7 @@ __global__ void k_mdot_final(const double* __restrict__ partial, int nblk, int n
 __global__ void k_mupdate(double* __restrict__ w, const double* __restrict__ V, size_t vstride,
                           const double* __restrict__ coef, int cstride, int nv, size_t per_slice,
                           const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double* cs = coef + (size_t)s * cstride;
@@ -257,6 +269,7 @@ __global__ void k_mupdate(double* __restrict__ w, const double* __restrict__ V, 
 __global__ void k_mcombine(double* __restrict__ out, const double* __restrict__ V, size_t vstride,
                            const double* __restrict__ coef, int cstride, const int* __restrict__ nvs,
                            size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double* cs = coef + (size_t)s * cstride;
@@ -287,6 +300,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ y,
                                                           const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.y;
@@ -310,6 +324,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
 template <int D>
 __global__ void k_block_inverse(Grid g, const double* __restrict__ A, double* __restrict__ Dinv,
                                 const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.y;
@@ -355,6 +370,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
                                                             double* __restrict__ xout, double omega,
                                                             const int* __restrict__ active,
                                                             unsigned long long* __restrict__ work) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   __shared__ double rsh[C][32];
@@ -401,6 +417,7 @@ template <int D>
 __global__ void __launch_bounds__(32 * (2 * D + 1)) k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
                                                               double* __restrict__ bc,
                                                               const int* __restrict__ active) {
+  pdl_wait();
   // thread = (coarse node, component): block (32, C), so the 3^d fine loads of
   // a thread are independent of its C-1 siblings' (more loads in flight)
   const int s = blockIdx.y;
@@ -431,6 +448,7 @@ template <int D>
 __global__ void __launch_bounds__(32 * (2 * D + 1)) k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec,
                                                                  double* __restrict__ xf,
                                                                  const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const int f = blockIdx.x * 32 + threadIdx.x;
@@ -454,6 +472,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_prolong_add(Grid gf, Grid 
 template <int D>
 __global__ void k_rap(Grid gf, Grid gc, const double* __restrict__ Af, double* __restrict__ Ac,
                       const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.z;
@@ -503,6 +522,7 @@ __global__ void k_rap(Grid gf, Grid gc, const double* __restrict__ Af, double* _
 template <int D>
 __global__ void k_dense_build(Grid g, const double* __restrict__ A, double* __restrict__ M,
                               const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   const int s = blockIdx.y;
@@ -530,6 +550,7 @@ __global__ void k_dense_build(Grid g, const double* __restrict__ A, double* __re
 
 // in-place Gauss-Jordan with partial pivoting, one CTA per slice (grid.x = S)
 __global__ void k_gauss_jordan(double* __restrict__ M, int n, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.x;
   if (active && !active[s]) return;
   double* Ms = M + (size_t)s * n * 2 * n;
@@ -630,6 +651,7 @@ template <int D>
 __global__ void __cluster_dims__(kGJCluster, 1, 1) __launch_bounds__(kGJThreads, 1)
     k_dense_invert_cl(Grid g, const double* __restrict__ A, float* __restrict__ Minv, int n, int ld,
                       const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   cg::cluster_group cluster = cg::this_cluster();
@@ -862,6 +884,7 @@ __device__ __forceinline__ void dense_apply_warps(const Grid& g, const float* __
 // fp64 augmented [n][2n] inverse (single-CTA fallback) -> fp32 [n][ld]
 __global__ void k_dense_to_f32(const double* __restrict__ M, float* __restrict__ out, int n, int ld,
                                const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double* Ms = M + (size_t)s * n * 2 * n;
@@ -874,6 +897,7 @@ __global__ void k_dense_to_f32(const double* __restrict__ M, float* __restrict__
 template <int D>
 __global__ void k_dense_apply(Grid g, const float* __restrict__ M, int ld, const double* __restrict__ b,
                               double* __restrict__ x, const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = 2 * D + 1;
   const int s = blockIdx.x;
   if (active && !active[s]) return;
@@ -887,6 +911,7 @@ __global__ void k_gmres_givens(int j, int m, double* __restrict__ H, double* __r
                                double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
                                int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its,
                                double* __restrict__ resid, int S) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   if (!gm_active[s]) return;
@@ -920,6 +945,7 @@ __global__ void k_gmres_givens(int j, int m, double* __restrict__ H, double* __r
 __global__ void k_gmres_solve(int m, const double* __restrict__ H, const double* __restrict__ gv,
                               const int* __restrict__ gm_steps, double* __restrict__ y, const int* __restrict__ active,
                               int S) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   if (active && !active[s]) return;
@@ -943,6 +969,7 @@ namespace pint {
 // hcol[s][i] += add[s][i], i < nv
 __global__ void k_add_cols(double* __restrict__ hcol, int hstride, const double* __restrict__ add, int astride, int nv,
                            int S, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.x;
   if (s >= S || (active && !active[s])) return;
   for (int i = threadIdx.x; i < nv; i += blockDim.x) hcol[(size_t)s * hstride + i] += add[(size_t)s * astride + i];
@@ -951,6 +978,7 @@ __global__ void k_add_cols(double* __restrict__ hcol, int hstride, const double*
 // hcol[s][row] = sqrt(sum_b partial[s][b])
 __global__ void k_norm_to_h(const double* __restrict__ partial, int nblk, double* __restrict__ hcol, int hstride,
                             int row, int S, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S || (active && !active[s])) return;
   double acc = 0.0;
@@ -961,6 +989,7 @@ __global__ void k_norm_to_h(const double* __restrict__ partial, int nblk, double
 // vout = w / hcol[s][row]  (0 when the norm vanished: lucky breakdown)
 __global__ void k_scale_col(double* __restrict__ vout, const double* __restrict__ w, const double* __restrict__ hcol,
                             int hstride, int row, size_t per_slice, const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const double h = hcol[(size_t)s * hstride + row];
@@ -972,6 +1001,7 @@ __global__ void k_scale_col(double* __restrict__ vout, const double* __restrict_
 // x += z
 __global__ void k_axpy_one(double* __restrict__ x, const double* __restrict__ z, size_t per_slice,
                            const int* __restrict__ active) {
+  pdl_wait();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
@@ -1021,6 +1051,7 @@ __device__ __forceinline__ int num_cells(const Grid& g) {
 template <int D, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS) k_vanka_setup(Grid g, const double* __restrict__ Ast,
                                                           float* __restrict__ Vinv, const int* __restrict__ active) {
+  pdl_wait();
   constexpr int L = Cells<D>::L;
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
@@ -1121,6 +1152,7 @@ template <int D>
 __global__ void __launch_bounds__(VankaRows<D>::T) k_vanka_setup_rows(Grid g, const double* __restrict__ Ast,
                                                                      float* __restrict__ Vinv,
                                                                      const int* __restrict__ active) {
+  pdl_wait();
   using VR = VankaRows<D>;
   constexpr int L = VR::L, C = Cells<D>::C, A = Cells<D>::A, WPC = VR::WPC, CPB = VR::CPB;
   __shared__ double prow[2][CPB][L];
@@ -1213,6 +1245,7 @@ __global__ void __launch_bounds__(CELLS * Cells<D>::L) k_vanka_cell(Grid g, cons
                                                                    double* __restrict__ y,
                                                                    const int* __restrict__ active,
                                                                    unsigned long long* __restrict__ work) {
+  pdl_wait();
   constexpr int L = Cells<D>::L;
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
@@ -1249,6 +1282,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_gather(Grid g, const
                                                                   const double* __restrict__ xin,
                                                                   double* __restrict__ xout, double omega,
                                                                   const int* __restrict__ active) {
+  pdl_wait();
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
   constexpr int L = Cells<D>::L;
@@ -1338,6 +1372,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __rest
                                                            double* __restrict__ h2, int h2stride,
                                                            unsigned int* __restrict__ counters,
                                                            const int* __restrict__ active) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32][kMdotMax];
   const int s = blockIdx.y;
   if (active && !active[s]) return;  // uniform per slice: the ticket count stays consistent
@@ -1400,6 +1435,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused_v(const double* __re
                                                              double* __restrict__ h2, int h2stride,
                                                              unsigned int* __restrict__ counters,
                                                              const int* __restrict__ active) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.z;
   const int v = blockIdx.y;
@@ -1437,6 +1473,7 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
                                                             int* __restrict__ gm_steps, int* __restrict__ its,
                                                             double* __restrict__ resid, double* __restrict__ hnorm,
                                                             unsigned int* __restrict__ counters) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.y;
   if (!gm_active[s]) return;
@@ -1784,6 +1821,7 @@ __device__ __forceinline__ void vcycle_tail_body(const TailArgs& a, const double
 template <int D>
 __global__ void __launch_bounds__(1024) k_vcycle_tail(TailArgs a, const double* __restrict__ b_top,
                                                      double* __restrict__ x_top, const int* __restrict__ active) {
+  pdl_wait();
   vcycle_tail_body<D, 1>(a, b_top, x_top, active);
 }
 
@@ -1797,6 +1835,7 @@ template <int D, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kTailThreads)
     k_vcycle_tail_cl(TailArgs a, const double* __restrict__ b_top, double* __restrict__ x_top,
                      const int* __restrict__ active) {
+  pdl_wait();
   vcycle_tail_body<D, CL>(a, b_top, x_top, active);
 }
 
@@ -1951,6 +1990,7 @@ __device__ __forceinline__ void arnoldi_body(const ArnoldiArgs& a) {
 
 template <int D>
 __global__ void __cluster_dims__(kTailCluster, 1, 1) __launch_bounds__(kTailThreads) k_arnoldi_fused(ArnoldiArgs a) {
+  pdl_wait();
   arnoldi_body<D, kTailCluster>(a);
 }
 

@@ -9,6 +9,7 @@ namespace pint {
 // K8a: delta = f_old - c_old for S slices (one launch)
 __global__ void k_precorrect(const double* __restrict__ f, const double* __restrict__ c, double* __restrict__ d,
                              size_t total) {
+  pdl_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
     d[i] = f[i] - c[i];
 }
@@ -16,6 +17,7 @@ __global__ void k_precorrect(const double* __restrict__ f, const double* __restr
 // per-component partial dots: part[c][q][blk] for q in {<f,c>, <c,c>, <f,f>}
 __global__ void __launch_bounds__(kRedThreads) k_block_dots(const double* __restrict__ f, const double* __restrict__ cn,
                                                            int nn, int np, double* __restrict__ part, int nblk) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int comp = blockIdx.y;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
@@ -44,6 +46,7 @@ __global__ void __launch_bounds__(kRedThreads) k_block_dots(const double* __rest
 // theta (one thread): mirrors theta_weight (parareal.py:166-197)
 __global__ void k_theta(const double* __restrict__ part, int nblk, int C, int variant, double lo, double hi,
                         double* __restrict__ theta) {
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (variant == 0) { *theta = 1.0; return; }
   const double degenerate = 1e-28;
@@ -76,6 +79,7 @@ __global__ void __launch_bounds__(kRedThreads) k_update_norms(const double* __re
                                                              const double* __restrict__ co, const double* __restrict__ xp,
                                                              double* __restrict__ xn, const double* __restrict__ theta,
                                                              int nn, int np, double* __restrict__ part, int nblk) {
+  pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int comp = blockIdx.y;
   const double th = *theta;
@@ -101,6 +105,7 @@ __global__ void __launch_bounds__(kRedThreads) k_update_norms(const double* __re
 }
 
 __global__ void k_corr(const double* __restrict__ part, int nblk, int C, double* __restrict__ out) {
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double dd = 0.0, n2 = 0.0;
   for (int c = 0; c < C; ++c)

@@ -20,6 +20,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -122,6 +123,7 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
+  bool pdl = true;              // PINT_PDL=0: launch without programmatic stream serialization
   int tail_rows = 2048;         // PINT_TAIL_ROWS: first level of the fused V-cycle tail has <= this many rows
   int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
@@ -164,6 +166,26 @@ static inline cudaStream_t counted(pint_ctx* ctx, cudaStream_t st) {
 }
 
 namespace {
+
+
+// Every kernel launch of the library: counted (profiling), and launched with
+// programmatic stream serialization so it may start while its predecessor
+// drains (each kernel begins with pdl_wait(); PINT_PDL=0 turns it off).
+template <typename... KArgs, typename... Args>
+static inline void pint_launch(pint_ctx* ctx, cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                               size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = counted(ctx, st);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 cudaEvent_t next_event(pint_ctx* ctx) {
   if (ctx->ev_used == ctx->ev_pool.size()) {
@@ -346,15 +368,15 @@ struct Impl {
   static int residual(pint_ctx* ctx, int S, const double* y, const double* yo, double* r, const int* mask,
                       double* h_norms, cudaStream_t st) {
     MeshDev m = mesh(ctx);
-    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, counted(ctx, st)>>>(r, vs(ctx), mask);
+    pint_launch(ctx, st, k_zero_active, vec_grid(vs(ctx), S), 256, 0, r, vs(ctx), mask);
     cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_residual_colour<D><<<dim3((ne * (1 << D) + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
+      pint_launch(ctx, st, k_residual_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
                                                                       mask, c);
     }
-    k_fix_residual<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, ctx->d_st, y, r, mask);
+    pint_launch(ctx, st, k_fix_residual<D>, node_grid(ctx->g.nn, S), 128, 0, m, ctx->d_st, y, r, mask);
     PINT_LAUNCHED();
     return norms(ctx, S, r, r, mask, true, ctx->d_degen, h_norms, st);
   }
@@ -362,8 +384,8 @@ struct Impl {
   static int norms(pint_ctx* ctx, int S, const double* x, const double* y, const int* mask, bool take_sqrt,
                    const int* degen, double* h_out, cudaStream_t st) {
     const int nblk = ctx->nblk;
-    k_dot_partial<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(x, y, vs(ctx), ctx->partial, nblk, mask);
-    k_dot_final<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(ctx->partial, nblk, ctx->d_norms, S, take_sqrt ? 1 : 0, degen,
+    pint_launch(ctx, st, k_dot_partial, dim3(nblk, S), kRedThreads, 0, x, y, vs(ctx), ctx->partial, nblk, mask);
+    pint_launch(ctx, st, k_dot_final, (S + 127) / 128, 128, 0, ctx->partial, nblk, ctx->d_norms, S, take_sqrt ? 1 : 0, degen,
                                                 mask);
     PINT_LAUNCHED();
     if (h_out) {
@@ -379,7 +401,7 @@ struct Impl {
     MeshDev m = mesh(ctx);
     Level& L0 = ctx->lv[0];
     const size_t ms = (size_t)ctx->g.noff * C * C * ctx->g.np;
-    k_zero_active<<<vec_grid(ms, S), 256, 0, counted(ctx, st)>>>(L0.A, ms, mask);
+    pint_launch(ctx, st, k_zero_active, vec_grid(ms, S), 256, 0, L0.A, ms, mask);
     constexpr int A = 1 << D;
     if (!ctx->jac_columns) {
       using JL = JacLin<D>;
@@ -391,19 +413,19 @@ struct Impl {
       for (int c = 0; c < A; ++c) {
         const int ne = colour_count(ctx, c);
         if (ne == 0) continue;
-        k_jacobian_lin<D><<<dim3((ne + JL::EPB - 1) / JL::EPB, C, S), JL::T, JL::smem, counted(ctx, st)>>>(
+        pint_launch(ctx, st, k_jacobian_lin<D>, dim3((ne + JL::EPB - 1) / JL::EPB, C, S), JL::T, JL::smem, 
             m, ctx->ph, ctx->d_st, y, yo, L0.A, mask, c);
       }
     } else {
       for (int c = 0; c < A; ++c) {
         const int ne = colour_count(ctx, c);
         if (ne == 0) continue;
-        k_jacobian_colour<D><<<dim3((ne * A + 127) / 128, A * C, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
+        pint_launch(ctx, st, k_jacobian_colour<D>, dim3((ne * A + 127) / 128, A * C, S), 128, 0, m, ctx->ph, ctx->d_st, y, yo, L0.A, mask,
                                                                            c);
       }
     }
-    k_fix_jacobian<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, L0.A, mask);
-    if (L0.A32) k_to_f32<<<vec_grid(ms / 2, S), 256, 0, counted(ctx, st)>>>(L0.A, L0.A32, ms, mask);
+    pint_launch(ctx, st, k_fix_jacobian<D>, node_grid(ctx->g.nn, S), 128, 0, m, L0.A, mask);
+    if (L0.A32) pint_launch(ctx, st, k_to_f32, vec_grid(ms / 2, S), 256, 0, L0.A, L0.A32, ms, mask);
     PINT_LAUNCHED();
     return PINT_OK;
   }
@@ -413,24 +435,24 @@ struct Impl {
                        const int* mask, cudaStream_t st) {
     const bool w = wide(L.g.nn, S);
     if (L.A32) {
-      if (w) k_spmv<D, true, 3, float><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A32, x, b, r, mask);
-      else k_spmv<D, true, 9, float><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A32, x, b, r, mask);
+      if (w) pint_launch(ctx, st, k_spmv<D, true, 3, float>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A32, x, b, r, mask);
+      else pint_launch(ctx, st, k_spmv<D, true, 9, float>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A32, x, b, r, mask);
     } else {
-      if (w) k_spmv<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, b, r, mask);
-      else k_spmv<D, true, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, b, r, mask);
+      if (w) pint_launch(ctx, st, k_spmv<D, true, 3>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A, x, b, r, mask);
+      else pint_launch(ctx, st, k_spmv<D, true, 9>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A, x, b, r, mask);
     }
   }
 
   static int jvp(pint_ctx* ctx, int S, const double* y, const double* yo, const double* w, double* out,
                  cudaStream_t st) {
     MeshDev m = mesh(ctx);
-    k_zero_active<<<vec_grid(vs(ctx), S), 256, 0, counted(ctx, st)>>>(out, vs(ctx), nullptr);
+    pint_launch(ctx, st, k_zero_active, vec_grid(vs(ctx), S), 256, 0, out, vs(ctx), nullptr);
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      k_jvp_colour<D><<<dim3((ne * (1 << D) + 127) / 128, S), 128, 0, counted(ctx, st)>>>(m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
+      pint_launch(ctx, st, k_jvp_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
     }
-    k_fix_jvp<D><<<node_grid(ctx->g.nn, S), 128, 0, counted(ctx, st)>>>(m, w, out, nullptr);
+    pint_launch(ctx, st, k_fix_jvp<D>, node_grid(ctx->g.nn, S), 128, 0, m, w, out, nullptr);
     PINT_LAUNCHED();
     return PINT_OK;
   }
@@ -438,9 +460,9 @@ struct Impl {
   static void spmv(pint_ctx* ctx, int lvl, int S, const double* x, double* y, const int* mask, cudaStream_t st) {
     Level& L = ctx->lv[lvl];
     if (wide(L.g.nn, S))
-      k_spmv<D, false, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
+      pint_launch(ctx, st, k_spmv<D, false, 3>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A, x, nullptr, y, mask);
     else
-      k_spmv<D, false, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, x, nullptr, y, mask);
+      pint_launch(ctx, st, k_spmv<D, false, 9>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A, x, nullptr, y, mask);
   }
 
   // ---- multigrid setup: RAP on all levels, block inverses, dense coarsest
@@ -466,22 +488,22 @@ struct Impl {
       Level& L = ctx->lv[l];
       if (l > 0) {
         Level& F = ctx->lv[l - 1];
-        k_rap<D><<<dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, counted(ctx, st)>>>(F.g, L.g, F.A, L.A, mask);
+        pint_launch(ctx, st, k_rap<D>, dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, F.g, L.g, F.A, L.A, mask);
       }
       const bool last_dense = ctx->coarse_dense && l == nl - 1;
       if (ko->smoother == 1 && !last_dense && !ctx->vanka_smem) {
         using VR = VankaRows<D>;
-        k_vanka_setup_rows<D><<<dim3((L.ncell + VR::CPB - 1) / VR::CPB, S), VR::T, 0, counted(ctx, st)>>>(
+        pint_launch(ctx, st, k_vanka_setup_rows<D>, dim3((L.ncell + VR::CPB - 1) / VR::CPB, S), VR::T, 0, 
             L.g, L.A, L.vinv, mask);
       } else if (ko->smoother == 1 && !last_dense) {
         constexpr int W = D == 2 ? 4 : 2;
         constexpr int Lc = Cells<D>::L;
         const size_t smem = (size_t)W * (Lc * 2 * Lc + Lc) * sizeof(double);
         cudaFuncSetAttribute(k_vanka_setup<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vanka_setup<D, W><<<dim3((L.ncell + W - 1) / W, S), 32 * W, smem, counted(ctx, st)>>>(L.g, L.A, L.vinv,
+        pint_launch(ctx, st, k_vanka_setup<D, W>, dim3((L.ncell + W - 1) / W, S), 32 * W, smem, L.g, L.A, L.vinv,
                                                                                                 mask);
       } else {
-        k_block_inverse<D><<<node_grid(L.g.nn, S), 128, 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, mask);
+        pint_launch(ctx, st, k_block_inverse<D>, node_grid(L.g.nn, S), 128, 0, L.g, L.A, L.Dinv, mask);
       }
     }
     if (ctx->coarse_dense) {
@@ -491,12 +513,12 @@ struct Impl {
       const size_t smem = gj_smem_bytes(n);
       if (gj_fits(n)) {
         cudaFuncSetAttribute(k_dense_invert_cl<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_dense_invert_cl<D><<<S * kGJCluster, kGJThreads, smem, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense32, n,
+        pint_launch(ctx, st, k_dense_invert_cl<D>, S * kGJCluster, kGJThreads, smem, L.g, L.A, ctx->d_dense32, n,
                                                                                       ctx->dense_ld, mask);
       } else {
-        k_dense_build<D><<<dim3(1, S), 512, 0, counted(ctx, st)>>>(L.g, L.A, ctx->d_dense, mask);
-        k_gauss_jordan<<<S, 512, 0, counted(ctx, st)>>>(ctx->d_dense, n, mask);
-        k_dense_to_f32<<<dim3((n * n + 255) / 256, S), 256, 0, counted(ctx, st)>>>(ctx->d_dense, ctx->d_dense32, n,
+        pint_launch(ctx, st, k_dense_build<D>, dim3(1, S), 512, 0, L.g, L.A, ctx->d_dense, mask);
+        pint_launch(ctx, st, k_gauss_jordan, S, 512, 0, ctx->d_dense, n, mask);
+        pint_launch(ctx, st, k_dense_to_f32, dim3((n * n + 255) / 256, S), 256, 0, ctx->d_dense, ctx->d_dense32, n,
                                                                                  ctx->dense_ld, mask);
       }
     }
@@ -564,22 +586,22 @@ struct Impl {
         e1 = next_event(ctx);
         cudaEventRecord(e0, st);
       }
-      k_vanka_cell<D, CELLS><<<dim3((L.ncell + CELLS - 1) / CELLS, S), dim3(CELLS, Cells<D>::L), 0, counted(ctx, st)>>>(
+      pint_launch(ctx, st, k_vanka_cell<D, CELLS>, dim3((L.ncell + CELLS - 1) / CELLS, S), dim3(CELLS, Cells<D>::L), 0, 
           L.g, L.vinv, r, L.ycell, mask, prof ? ctx->d_work : nullptr);
       if (prof) {
         cudaEventRecord(e1, st);
         ctx->ev_pairs.emplace_back(e0, e1);
       }
       if (first)
-        k_vanka_gather<D, true><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.ycell, nullptr,
+        pint_launch(ctx, st, k_vanka_gather<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.ycell, nullptr,
                                                                                               xout, om, mask);
       else
-        k_vanka_gather<D, false><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.ycell, xin,
+        pint_launch(ctx, st, k_vanka_gather<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.ycell, xin,
                                                                                                xout, om, mask);
       return;
     }
     if (first) {
-      k_smooth<D, true, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, L.A, L.Dinv, b, nullptr,
+      pint_launch(ctx, st, k_smooth<D, true, 3>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A, L.Dinv, b, nullptr,
                                                                                     xout, om, mask, nullptr);
       return;
     }
@@ -591,10 +613,10 @@ struct Impl {
       cudaEventRecord(e0, st);
     }
     if (wide(L.g.nn, S))
-      k_smooth<D, false, 3><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(
+      pint_launch(ctx, st, k_smooth<D, false, 3>, row_grid(L.g.nn, S), row_block<D>(), 0, 
           L.g, L.A, L.Dinv, b, xin, xout, om, mask, prof ? ctx->d_work : nullptr);
     else
-      k_smooth<D, false, 9><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(
+      pint_launch(ctx, st, k_smooth<D, false, 9>, row_grid(L.g.nn, S), row_block<D>(), 0, 
           L.g, L.A, L.Dinv, b, xin, xout, om, mask, prof ? ctx->d_work : nullptr);
     if (prof) {
       cudaEventRecord(e1, st);
@@ -623,13 +645,13 @@ struct Impl {
       const TailArgs& ta = stage ? ctx->tail_cl : ctx->tail;
       const size_t sm = stage ? tsm : 0;
       if (cl == 8)
-        k_vcycle_tail_cl<D, 8><<<S * 8, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
+        pint_launch(ctx, st, k_vcycle_tail_cl<D, 8>, S * 8, kTailThreads, sm, ta, b, x, mask);
       else if (cl == 4)
-        k_vcycle_tail_cl<D, 4><<<S * 4, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
+        pint_launch(ctx, st, k_vcycle_tail_cl<D, 4>, S * 4, kTailThreads, sm, ta, b, x, mask);
       else if (cl == 2)
-        k_vcycle_tail_cl<D, 2><<<S * 2, kTailThreads, sm, counted(ctx, st)>>>(ta, b, x, mask);
+        pint_launch(ctx, st, k_vcycle_tail_cl<D, 2>, S * 2, kTailThreads, sm, ta, b, x, mask);
       else
-        k_vcycle_tail<D><<<S, 1024, 0, counted(ctx, st)>>>(ctx->tail, b, x, mask);
+        pint_launch(ctx, st, k_vcycle_tail<D>, S, 1024, 0, ctx->tail, b, x, mask);
       if (prof) {
         cudaEventRecord(e1, st);
         ctx->ev_pairs.emplace_back(e0, e1);
@@ -638,7 +660,7 @@ struct Impl {
     }
     if (l == nl - 1) {
       if (ctx->coarse_dense) {
-        k_dense_apply<D><<<S, 256, 0, counted(ctx, st)>>>(L.g, ctx->d_dense32, ctx->dense_ld, b, x, mask);
+        pint_launch(ctx, st, k_dense_apply<D>, S, 256, 0, L.g, ctx->d_dense32, ctx->dense_ld, b, x, mask);
       } else {
         const int sweeps = std::max(1, (int)ko.coarse_sweeps);
         double* cur = L.xa;
@@ -663,10 +685,10 @@ struct Impl {
       std::swap(cur, nxt);
     }
     vc_resid(ctx, L, S, cur, b, L.res, mask, st);
-    k_restrict<D><<<row_grid(Lc.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, Lc.g, L.res, Lc.rhs, mask);
+    pint_launch(ctx, st, k_restrict<D>, row_grid(Lc.g.nn, S), row_block<D>(), 0, L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
-    k_prolong_add<D><<<row_grid(L.g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(L.g, Lc.g, xc, cur, mask);
+    pint_launch(ctx, st, k_prolong_add<D>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, Lc.g, xc, cur, mask);
     for (int i = 0; i < post; ++i) {
       double* out = (i == post - 1) ? x : nxt;
       smooth(ctx, L, S, b, cur, out, mask, st, false);
@@ -696,22 +718,22 @@ struct Impl {
     for (int pass = 0; pass < 2; ++pass) {
       // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
       if ((size_t)nblk * S >= 2 * 148)
-        k_mdot_fused<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(
+        pint_launch(ctx, st, k_mdot_fused, dim3(nblk, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
             ctx->ctr_mdot, ctx->gm_active);
       else
-        k_mdot_fused_v<<<dim3(nblk, j + 1, S), kRedThreads, 0, counted(ctx, st)>>>(
+        pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
             ctx->ctr_mdot, ctx->gm_active);
-      k_mupdate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
+      pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
                                                              pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
     }
     // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
-    k_norm_givens<<<dim3(nblk, S), kRedThreads, 0, counted(ctx, st)>>>(
+    pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
         ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
         ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
     double* vj1 = ctx->V + (j + 1) * vstride;
-    k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
+    pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
   // algorithmic bytes of one V-cycle from level `from` down, for one slice
@@ -779,7 +801,7 @@ struct Impl {
       cudaEventRecord(e0, st);
       ctx->fused_used = true;
     }
-    k_arnoldi_fused<D><<<S * kTailCluster, kTailThreads, 0, counted(ctx, st)>>>(a);
+    pint_launch(ctx, st, k_arnoldi_fused<D>, S * kTailCluster, kTailThreads, 0, a);
     if (ctx->prof) {
       cudaEventRecord(e1, st);
       ctx->ev_pairs.emplace_back(e0, e1);
@@ -831,7 +853,7 @@ struct Impl {
       for (int s = 0; s < S; ++s) host_mask[s] = ctx->h_int[s];
     }
     // x = 0, r = b, beta = ||b||, tol = max(rtol beta0, atol)
-    k_zero_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, n, mask);
+    pint_launch(ctx, st, k_zero_active, vec_grid(n, S), 256, 0, x, n, mask);
     PINT_TRY(norms(ctx, S, b, b, mask, true, nullptr, nullptr, st));
     std::vector<double> beta(S, 0.0), tol(S, 0.0);
     PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
@@ -863,7 +885,7 @@ struct Impl {
       for (int s = 0; s < S; ++s) g0[(size_t)s * (m + 1)] = res[s];
       PINT_CHECK(cudaMemcpyAsync(ctx->gv, g0.data(), sizeof(double) * g0.size(), cudaMemcpyHostToDevice, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->gm_beta, res.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
-      k_scale_inv<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
+      pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
       int remaining_cap = m;
       for (int s = 0; s < S; ++s)
         if (cyc[s]) remaining_cap = std::min(remaining_cap, std::max(1, ko->max_iters - its[s]));
@@ -881,16 +903,16 @@ struct Impl {
         }
       }
       // x += Z y  (flexible GMRES: the preconditioned directions are stored)
-      k_gmres_solve<<<(S + 127) / 128, 128, 0, counted(ctx, st)>>>(m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
+      pint_launch(ctx, st, k_gmres_solve, (S + 127) / 128, 128, 0, m, ctx->H, ctx->gv, ctx->gm_steps, ctx->ybuf, ctx->cyc_active,
                                                     S);
-      k_mcombine<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->u, ctx->Z, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
+      pint_launch(ctx, st, k_mcombine, vec_grid(n, S), 256, 0, ctx->u, ctx->Z, vstride, ctx->ybuf, m + 1, ctx->gm_steps, n,
                                                  ctx->cyc_active);
-      k_axpy_one<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(x, ctx->u, n, ctx->cyc_active);
+      pint_launch(ctx, st, k_axpy_one, vec_grid(n, S), 256, 0, x, ctx->u, n, ctx->cyc_active);
       // true residual r = b - J x into ctx->u (reused as cycle start)
       if (wide(ctx->g.nn, S))
-        k_spmv<D, true, 3><<<row_grid(ctx->g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+        pint_launch(ctx, st, k_spmv<D, true, 3>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
       else
-        k_spmv<D, true, 9><<<row_grid(ctx->g.nn, S), row_block<D>(), 0, counted(ctx, st)>>>(ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
+        pint_launch(ctx, st, k_spmv<D, true, 9>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
       rvec = ctx->u;
       PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
@@ -918,7 +940,7 @@ struct Impl {
     std::vector<double> rnorm(S), target(S), tnorm(S), lam(S, 1.0);
     std::vector<int> running(S, 0), its(S, 0), ls(S, 0), accept(S, 0);
     PINT_CHECK(cudaMemcpyAsync(ctx->d_active, act.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-    k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(y, yo, n, ctx->d_active);  // Newton guess = previous state
+    pint_launch(ctx, st, k_copy_active, vec_grid(n, S), 256, 0, y, yo, n, ctx->d_active);  // Newton guess = previous state
     PINT_TRY(residual(ctx, S, y, yo, ctx->r, ctx->d_active, rnorm.data(), st));
     for (int s = 0; s < S; ++s) {
       if (!act[s]) continue;
@@ -959,7 +981,7 @@ struct Impl {
           PINT_TRY(precond_setup(ctx, S, ko, ctx->d_mask2, st));
         }
       }
-      k_negate<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->b, ctx->r, n, ctx->d_active);
+      pint_launch(ctx, st, k_negate, vec_grid(n, S), 256, 0, ctx->b, ctx->r, n, ctx->d_active);
       // inexact Newton forcing (per slice): the first Newton iteration of a step only
       // needs rtol_first (its update error is dominated by the nonlinearity); later
       // iterations solve to rtol, but never below a tenth of the Newton target
@@ -991,7 +1013,7 @@ struct Impl {
         if (nls == 0) break;
         PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ls.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
         PINT_CHECK(cudaMemcpyAsync(ctx->d_lam, lam.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
-        k_trial<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->ytrial, y, ctx->dx, ctx->d_lam, n, ctx->d_mask2);
+        pint_launch(ctx, st, k_trial, vec_grid(n, S), 256, 0, ctx->ytrial, y, ctx->dx, ctx->d_lam, n, ctx->d_mask2);
         std::vector<double> tn(S, 0.0);
         PINT_TRY(residual(ctx, S, ctx->ytrial, yo, ctx->rtrial, ctx->d_mask2, tn.data(), st));
         for (int s = 0; s < S; ++s) {
@@ -1012,8 +1034,8 @@ struct Impl {
         accept[s] = 1;
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, accept.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(y, ctx->ytrial, n, ctx->d_mask2);
-      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->r, ctx->rtrial, n, ctx->d_mask2);
+      pint_launch(ctx, st, k_copy_active, vec_grid(n, S), 256, 0, y, ctx->ytrial, n, ctx->d_mask2);
+      pint_launch(ctx, st, k_copy_active, vec_grid(n, S), 256, 0, ctx->r, ctx->rtrial, n, ctx->d_mask2);
       PINT_LAUNCHED();
       for (int s = 0; s < S; ++s) {
         if (!accept[s]) continue;
@@ -1066,7 +1088,7 @@ struct Impl {
         t[s] = t1[s];
       }
       PINT_CHECK(cudaMemcpyAsync(ctx->d_mask2, ok.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
-      k_copy_active<<<vec_grid(n, S), 256, 0, counted(ctx, st)>>>(ctx->ystate, ctx->ynew, n, ctx->d_mask2);
+      pint_launch(ctx, st, k_copy_active, vec_grid(n, S), 256, 0, ctx->ystate, ctx->ynew, n, ctx->d_mask2);
       PINT_LAUNCHED();
     }
     PINT_CHECK(cudaMemcpyAsync(y_out, ctx->ystate, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
@@ -1149,6 +1171,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
+  ctx->pdl = !(std::getenv("PINT_PDL") && std::getenv("PINT_PDL")[0] == '0');
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {

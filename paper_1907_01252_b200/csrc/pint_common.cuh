@@ -14,6 +14,11 @@
 
 namespace pint {
 
+// Programmatic dependent launch: every kernel of the library waits here for
+// the grid it depends on (a no-op when launched without the PDL attribute),
+// so the host may launch it while its predecessor drains (pint_launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr int kMaxDim = 3;
 
 struct Grid {
