@@ -123,6 +123,7 @@ struct pint_ctx {
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
+  int poll_every = 4;           // PINT_POLL: Arnoldi steps between host polls of the convergence mask
   bool pdl = true;              // PINT_PDL=0: launch without programmatic stream serialization
   int tail_rows = 2048;         // PINT_TAIL_ROWS: first level of the fused V-cycle tail has <= this many rows
   int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
@@ -894,7 +895,7 @@ struct Impl {
         PINT_LAUNCHED();
         if (j + 1 >= remaining_cap) break;
         // poll: any slice still iterating?
-        if ((j & 3) == 3 || j + 1 == m) {
+        if ((j + 1) % ctx->poll_every == 0 || j + 1 == m) {
           PINT_CHECK(cudaMemcpyAsync(ctx->h_int, ctx->gm_active, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
           PINT_CHECK(cudaStreamSynchronize(st));
           bool any = false;
@@ -1172,6 +1173,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
   ctx->pdl = !(std::getenv("PINT_PDL") && std::getenv("PINT_PDL")[0] == '0');
+  if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
