@@ -1538,18 +1538,49 @@ struct TailArgs {
 template <int D>
 __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const double* x, const double* b,
                                                 double* out, int tid, int nth) {
+  // P consecutive lanes share a row, each takes every P-th stencil offset with
+  // all its loads in flight; the partial sums meet in an xor butterfly (fixed
+  // order, independent of the cluster size).  One round of memory latency per
+  // row instead of NOFF/3 -- the tail's phases are latency-bound.
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
+  constexpr int P = D == 2 ? 4 : 8;
+  constexpr int OPL = (NOFF + P - 1) / P;
   const int np = L.g.np;
   const size_t vs = (size_t)C * np;
-  for (int idx = tid; idx < L.g.nn * C; idx += nth) {
-    const int ca = idx / L.g.nn, n = idx % L.g.nn;
-    int nbs[NOFF];
-    stencil_neighbours<D>(L.g, n, nbs);
+  const int total = L.g.nn * C * P;
+  const int part = tid % P;
+  for (int base = 0; base < total; base += nth) {
+    const int idx = base + tid;
+    const bool ok = idx < total;
+    const int row = ok ? idx / P : 0;
+    const int ca = row / L.g.nn, n = row % L.g.nn;
+    int i, j, k;
+    node_coords(L.g, n, i, j, k);
     const double* Arow = L.A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
-    const double acc = stencil_row<D, 3>(Arow, x + s * vs, np, nbs);
-    const size_t o = s * vs + (size_t)ca * np + n;
-    out[o] = b[o] - acc;
+    const double* xs = x + s * vs;
+    double a[OPL][C], xv[OPL][C];
+#pragma unroll
+    for (int q = 0; q < OPL; ++q) {
+      const int off = part + P * q;
+      const int nb = (ok && off < NOFF) ? neighbour(L.g, i, j, k, off) : -1;
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) {
+        a[q][cb] = nb >= 0 ? ld_nc(Arow + ((size_t)off * C * C + cb) * np) : 0.0;
+        xv[q][cb] = nb >= 0 ? ld_nc(xs + cb * np + nb) : 0.0;
+      }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < OPL; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) acc = fma(a[q][cb], xv[q][cb], acc);
+#pragma unroll
+    for (int o = P / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (ok && part == 0) {
+      const size_t o = s * vs + (size_t)ca * np + n;
+      out[o] = b[o] - acc;
+    }
   }
 }
 
