@@ -1312,6 +1312,77 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_gather(Grid g, const
   xout[o] = (FIRST ? 0.0 : xin[o]) + omega * z;
 }
 
+// Fused Vanka sweep (cell solves + gather in ONE pass, no y_c buffer):
+// thread (node n, comp c) owns row (a, c) of each of the <= 2^D cells that
+// have n as corner a, so every inverse row is still read exactly once.  The
+// block's residual neighbourhood (3^{D-1} node-row ranges of 34 nodes, all
+// components, converted to fp32 exactly as k_vanka_cell does) is staged in
+// shared memory; per cell the product uses the same fmaf order and 4-way
+// split as k_vanka_cell and the cells are summed in the same fixed corner
+// order as k_vanka_gather -> bitwise the same x_out as the two-kernel sweep.
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_apply(Grid g, const float* __restrict__ Vinv,
+                                                                 const double* __restrict__ r,
+                                                                 const double* __restrict__ xin,
+                                                                 double* __restrict__ xout, double omega,
+                                                                 const int* __restrict__ active,
+                                                                 unsigned long long* __restrict__ work) {
+  pdl_wait();
+  constexpr int C = Cells<D>::C;
+  constexpr int A = Cells<D>::A;
+  constexpr int L = Cells<D>::L;
+  constexpr int R = D == 2 ? 3 : 9;  // node-row ranges (dj, dk) in {-1,0,1}^{D-1}
+  constexpr int W = 34;              // 32 nodes + one halo node either side
+  __shared__ float rs[C][R][W];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  if (work && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(work, 1ULL);
+  const int n0 = blockIdx.x * 32;
+  const int nx = g.n[0], nxy = g.n[0] * g.n[1];
+  const double* rsl = r + (size_t)s * C * g.np;
+  for (int idx = threadIdx.y * 32 + threadIdx.x; idx < C * R * W; idx += 32 * C) {
+    const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
+    const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
+    const int m = n0 - 1 + w + dj * nx + dk * nxy;
+    rs[cb][q][w] = (m >= 0 && m < g.nn) ? (float)__ldg(rsl + (size_t)cb * g.np + m) : 0.0f;
+  }
+  __syncthreads();
+  const int n = n0 + threadIdx.x;
+  if (n >= g.nn) return;
+  const int c = threadIdx.y;
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+  const int cx = g.n[0] - 1, cy = g.n[1] - 1, cz = D == 3 ? g.n[2] - 1 : 1;
+  const int ncell = cx * cy * cz;
+  const float* Vs = Vinv + (size_t)s * L * L * ncell;
+  double acc = 0.0;
+  int cnt = 0;
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+    const int ax = a & 1, ay = (a >> 1) & 1, az = D == 3 ? (a >> 2) & 1 : 0;
+    const int ci = i - ax, cj = j - ay, ck = D == 3 ? k - az : 0;
+    if (ci < 0 || ci >= cx || cj < 0 || cj >= cy || ck < 0 || ck >= cz) continue;
+    const int cell = (ck * cy + cj) * cx + ci;
+    const float* Vr = Vs + (size_t)(a * C + c) * L * ncell + cell;
+    float v[L];
+#pragma unroll
+    for (int jj = 0; jj < L; ++jj) v[jj] = __ldg(Vr + (size_t)jj * ncell);
+    float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int jj = 0; jj < L; ++jj) {
+      const int b = jj / C, cb = jj % C;
+      const int dx = (b & 1) - ax, dy = ((b >> 1) & 1) - ay, dz = D == 3 ? ((b >> 2) & 1) - az : 0;
+      const int q = (dy + 1) + (D == 3 ? 3 * (dz + 1) : 0);
+      p[jj & 3] = fmaf(v[jj], rs[cb][q][threadIdx.x + 1 + dx], p[jj & 3]);
+    }
+    acc += (double)((p[0] + p[1]) + (p[2] + p[3]));
+    ++cnt;
+  }
+  const size_t o = (size_t)s * C * g.np + (size_t)c * g.np + n;
+  const double z = acc / cnt;
+  xout[o] = (FIRST ? 0.0 : xin[o]) + omega * z;
+}
+
 }  // namespace pint
 
 // ======================================================================
@@ -1584,36 +1655,20 @@ __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const 
   }
 }
 
+// fused tail sweep body: thread (node, comp) applies its row of each adjacent
+// cell inverse and sums the cells in corner order (same bits as
+// tail_vanka_cell + tail_vanka_gather, one cluster barrier fewer per sweep)
 template <int D>
-__device__ __forceinline__ void tail_vanka_cell(const LevelDev& L, int s, const double* r, int tid, int nth) {
+__device__ __forceinline__ void tail_vanka_apply(const LevelDev& L, int s, const double* r, const double* xin,
+                                                 double* xout, double omega, bool first, int tid, int nth) {
   constexpr int C = 2 * D + 1;
   constexpr int A = 1 << D;
   constexpr int LL = A * C;
-  const int ncell = L.ncell, np = L.g.np;
-  for (int idx = tid; idx < ncell * LL; idx += nth) {
-    const int row = idx / ncell, cell = idx % ncell;
-    int nodes[A];
-    cell_nodes<D>(L.g, cell, nodes);
-    const float* Vs = L.vinv + (size_t)s * LL * LL * ncell + (size_t)row * LL * ncell + cell;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // fp32 as in k_vanka_cell
-#pragma unroll
-    for (int j = 0; j < LL; ++j) {
-      const float rj = (float)r[(size_t)s * C * np + (size_t)(j % C) * np + nodes[j / C]];
-      acc[j & 3] = fmaf(__ldg(Vs + (size_t)j * ncell), rj, acc[j & 3]);
-    }
-    L.ycell[(size_t)s * LL * ncell + (size_t)row * ncell + cell] = (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
-  }
-}
-
-template <int D>
-__device__ __forceinline__ void tail_vanka_gather(const LevelDev& L, int s, const double* xin, double* xout,
-                                                  double omega, bool first, int tid, int nth) {
-  constexpr int C = 2 * D + 1;
-  constexpr int A = 1 << D;
-  constexpr int LL = A * C;
-  const int np = L.g.np;
+  const int np = L.g.np, ncell = L.ncell;
   const int cx = L.g.n[0] - 1, cy = L.g.n[1] - 1, cz = D == 3 ? L.g.n[2] - 1 : 1;
-  const double* ys = L.ycell + (size_t)s * LL * L.ncell;
+  const int nx = L.g.n[0], nxy = L.g.n[0] * L.g.n[1];
+  const double* rsl = r + (size_t)s * C * np;
+  const float* Vs = L.vinv + (size_t)s * LL * LL * ncell;
   for (int idx = tid; idx < L.g.nn * C; idx += nth) {
     const int c = idx / L.g.nn, n = idx % L.g.nn;
     int i, j, k;
@@ -1622,9 +1677,20 @@ __device__ __forceinline__ void tail_vanka_gather(const LevelDev& L, int s, cons
     int cnt = 0;
 #pragma unroll
     for (int a = 0; a < A; ++a) {
-      const int ci = i - (a & 1), cj = j - ((a >> 1) & 1), ck = D == 3 ? k - ((a >> 2) & 1) : 0;
+      const int ax = a & 1, ay = (a >> 1) & 1, az = D == 3 ? (a >> 2) & 1 : 0;
+      const int ci = i - ax, cj = j - ay, ck = D == 3 ? k - az : 0;
       if (ci < 0 || ci >= cx || cj < 0 || cj >= cy || ck < 0 || ck >= cz) continue;
-      acc += ys[(size_t)(a * C + c) * L.ncell + (ck * cy + cj) * cx + ci];
+      const int cell = (ck * cy + cj) * cx + ci;
+      const float* Vr = Vs + (size_t)(a * C + c) * LL * ncell + cell;
+      const int lower = n - ax - ay * nx - az * nxy;
+      float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int jj = 0; jj < LL; ++jj) {
+        const int b = jj / C, cb = jj % C;
+        const int m = lower + (b & 1) + ((b >> 1) & 1) * nx + (D == 3 ? ((b >> 2) & 1) * nxy : 0);
+        p[jj & 3] = fmaf(__ldg(Vr + (size_t)jj * ncell), (float)rsl[(size_t)cb * np + m], p[jj & 3]);
+      }
+      acc += (double)((p[0] + p[1]) + (p[2] + p[3]));
       ++cnt;
     }
     const size_t o = (size_t)s * C * np + (size_t)c * np + n;
@@ -1783,9 +1849,7 @@ __device__ __forceinline__ void tail_sweep(const LevelDev& L, int s, const doubl
     tail_sync<CL>();
     r = L.res;
   }
-  tail_vanka_cell<D>(L, s, r, tid, nth);
-  tail_sync<CL>();
-  tail_vanka_gather<D>(L, s, xin, xout, omega, first, tid, nth);
+  tail_vanka_apply<D>(L, s, r, xin, xout, omega, first, tid, nth);
   tail_sync<CL>();
 }
 

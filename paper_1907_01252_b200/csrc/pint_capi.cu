@@ -120,6 +120,7 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
+  bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
@@ -586,6 +587,20 @@ struct Impl {
         e0 = next_event(ctx);
         e1 = next_event(ctx);
         cudaEventRecord(e0, st);
+      }
+      if (!ctx->vanka_split) {
+        // fused cell solves + gather (bitwise the same as the split pair below)
+        if (first)
+          pint_launch(ctx, st, k_vanka_apply<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.vinv, r,
+                      nullptr, xout, om, mask, prof ? ctx->d_work : nullptr);
+        else
+          pint_launch(ctx, st, k_vanka_apply<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.vinv, r,
+                      xin, xout, om, mask, prof ? ctx->d_work : nullptr);
+        if (prof) {
+          cudaEventRecord(e1, st);
+          ctx->ev_pairs.emplace_back(e0, e1);
+        }
+        return;
       }
       pint_launch(ctx, st, k_vanka_cell<D, CELLS>, dim3((L.ncell + CELLS - 1) / CELLS, S), dim3(CELLS, Cells<D>::L), 0, 
           L.g, L.vinv, r, L.ycell, mask, prof ? ctx->d_work : nullptr);
@@ -1170,6 +1185,11 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
   ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
+  // level-0 Vanka sweep: fused (cell solves + gather, k_vanka_apply) in 2-d,
+  // split in 3-d, where the fused grid is 1.2 waves of (node, comp) threads
+  // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
+  ctx->vanka_split = ctx->D == 3;
+  if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
   ctx->pdl = !(std::getenv("PINT_PDL") && std::getenv("PINT_PDL")[0] == '0');
@@ -1384,8 +1404,11 @@ const char* pint_profile_kernel(const pint_ctx* ctx) {
   if (ctx->tail_first == 0)
     return ctx->D == 2 ? "k_vcycle_tail_cl<2> (whole V-cycle: mesh fits the cluster tail)"
                        : "k_vcycle_tail_cl<3> (whole V-cycle: mesh fits the cluster tail)";
-  if (ctx->kopt.smoother == 1) return ctx->D == 2 ? "k_vanka_cell<2,16> (level-0 cell-patch Vanka solves)"
-                                                  : "k_vanka_cell<3,8> (level-0 cell-patch Vanka solves)";
+  if (ctx->kopt.smoother == 1 && ctx->vanka_split)
+    return ctx->D == 2 ? "k_vanka_cell<2,16> (level-0 cell-patch Vanka solves)"
+                       : "k_vanka_cell<3,8> (level-0 cell-patch Vanka solves)";
+  if (ctx->kopt.smoother == 1) return ctx->D == 2 ? "k_vanka_apply<2> (level-0 Vanka sweep: cell solves + gather)"
+                                                  : "k_vanka_apply<3> (level-0 Vanka sweep: cell solves + gather)";
   return ctx->D == 2 ? "k_smooth<2,false> (level-0 node-block Jacobi sweep)" : "k_smooth<3,false>";
 }
 
@@ -1417,10 +1440,15 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   } else if (bytes_per_slice_launch) {
     const Grid& g = ctx->lv[0].g;
     const int64_t C = ctx->C;
-    if (ctx->kopt.smoother == 1) {
+    if (ctx->kopt.smoother == 1 && ctx->vanka_split) {
       // k_vanka_cell: cell inverses (L^2) + cell corrections (L) per cell, residual C per node
       const int64_t Lc = (int64_t)(1 << ctx->D) * C;
       *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * (4 * Lc * Lc + 8 * Lc) + (int64_t)g.nn * 8 * C;
+    } else if (ctx->kopt.smoother == 1) {
+      // k_vanka_apply: fp32 cell inverses (L^2 per cell) + residual in + x out (C per node each);
+      // the x_in read of the non-first sweeps is not counted (lower bound)
+      const int64_t Lc = (int64_t)(1 << ctx->D) * C;
+      *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * 4 * Lc * Lc + (int64_t)g.nn * 16 * C;
     } else {
       // k_smooth: A (noff C^2) + Dinv (C^2) + b + x_in + x_out (3 C), fp64, per node
       *bytes_per_slice_launch = (int64_t)g.nn * 8 * ((int64_t)g.noff * C * C + C * C + 3 * C);

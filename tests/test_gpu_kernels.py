@@ -235,3 +235,25 @@ def test_vanka_setup_variants_agree(cuda, name):
         outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
     for s in range(S):
         assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[1][s]), (name, s)
+
+
+@pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("small3d", "300")])
+def test_vanka_fused_sweep_bitwise(cuda, name, tail_rows):
+    """The fused level-0 Vanka sweep (k_vanka_apply: cell solves + gather in
+    one pass) and the split pair (k_vanka_cell + k_vanka_gather through the
+    y_c buffer) give the same V-cycle bit for bit (same fmaf order, same fixed
+    corner order).  PINT_TAIL_ROWS keeps level 0 out of the cluster tail."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 71, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 72, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs = []
+    for mode in ("fused", "split"):
+        dev = _device_with_env(P, {"PINT_VANKA": mode, "PINT_TAIL_ROWS": tail_rows}, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+    assert np.array_equal(outs[0], outs[1]), name
