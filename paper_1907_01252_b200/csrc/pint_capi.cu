@@ -120,6 +120,7 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
+  bool split_norm = false;   // PINT_SPLIT_NORM=1: second CGS update and the norm as two kernels
   bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
   std::vector<int> base_its;    // per slice: Krylov its of the first-Newton-iteration solve after that build
@@ -741,13 +742,19 @@ struct Impl {
         pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
             ctx->ctr_mdot, ctx->gm_active);
+      if (pass == 1 && !ctx->split_norm) break;
       pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
                                                              pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
     }
     // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
-    pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
-        ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
-        ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
+    if (ctx->split_norm)
+      pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
+          ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
+          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
+    else  // second CGS update fused with the norm + Givens (same bits)
+      pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride, ctx->ybuf,
+          j + 1, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
+          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
     double* vj1 = ctx->V + (j + 1) * vstride;
     pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
@@ -1188,6 +1195,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // level-0 Vanka sweep: fused (cell solves + gather, k_vanka_apply) in 2-d,
   // split in 3-d, where the fused grid is 1.2 waves of (node, comp) threads
   // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
+  ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;
   if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);

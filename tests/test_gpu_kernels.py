@@ -257,3 +257,28 @@ def test_vanka_fused_sweep_bitwise(cuda, name, tail_rows):
         dev.precond_setup(S, KrylovSettings())
         outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
     assert np.array_equal(outs[0], outs[1]), name
+
+
+@pytest.mark.parametrize("name", ["c1", "small3d"])
+def test_fused_cgs_norm_bitwise(cuda, name):
+    """The second CGS2 update fused with ||w|| and the Givens update
+    (k_mupdate_norm_givens, default) and the split pair (k_mupdate +
+    k_norm_givens, PINT_SPLIT_NORM=1) give the same flexible-GMRES solve bit
+    for bit: same solution, same iteration counts."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 81, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 82, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    res = []
+    for env in ({}, {"PINT_SPLIT_NORM": "1"}):
+        dev = _device_with_env(P, env, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        ks = KrylovSettings(rtol=1e-10)
+        dev.precond_setup(S, ks)
+        x, its, _ = dev.linear_solve(dev.to_device(B), ks)
+        res.append((dev.to_host(x), list(its)))
+    assert res[0][1] == res[1][1] and min(res[0][1]) > 3
+    assert np.array_equal(res[0][0], res[1][0]), name
