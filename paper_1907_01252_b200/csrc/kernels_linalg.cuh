@@ -1568,13 +1568,13 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
   }
 }
 
-// second CGS pass fused with the norm: w -= sum_v y_v V_v on this block's
+// last CGS pass fused with the norm: w -= sum_v y_v V_v on this block's
 // chunk (k_mupdate's order), then ||w||^2 partials in k_norm_givens' order
 // over the same chunk -> bitwise the same H, Givens and w as the two kernels,
 // one launch and one read of w fewer per Arnoldi step; grid (nblk, S)
 __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
-    double* __restrict__ w, const double* __restrict__ V, size_t vstride, const double* __restrict__ coef, int nv,
-    size_t per_slice, double* __restrict__ partial, int nblk, int j, int m, double* __restrict__ H,
+    double* __restrict__ w, const double* __restrict__ V, size_t vstride, const double* __restrict__ coef, int cstride,
+    int nv, size_t per_slice, double* __restrict__ partial, int nblk, int j, int m, double* __restrict__ H,
     double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
     int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its, double* __restrict__ resid,
     double* __restrict__ hnorm, unsigned int* __restrict__ counters) {
@@ -1584,7 +1584,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
   if (!gm_active[s]) return;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   double* ws = w + s * per_slice;
-  const double* cf = coef + (size_t)s * (m + 1);
+  const double* cf = coef + (size_t)s * cstride;
   const double* Vs = V + s * per_slice;
   double acc = 0.0;
   for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {

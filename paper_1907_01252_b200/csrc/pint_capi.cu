@@ -120,6 +120,7 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
+  int cgs_passes = 1;          // PINT_CGS=1|2: classical Gram-Schmidt passes per Arnoldi step (2 = CGS2)
   bool split_norm = false;   // PINT_SPLIT_NORM=1: second CGS update and the norm as two kernels
   bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
@@ -732,7 +733,8 @@ struct Impl {
     double* hcol = ctx->H + (size_t)j * (m + 1);
     const int hstride = (m + 1) * m;
     const int nblk = ctx->nblk;
-    for (int pass = 0; pass < 2; ++pass) {
+    const int npass = ctx->cgs_passes;
+    for (int pass = 0; pass < npass; ++pass) {
       // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
       if ((size_t)nblk * S >= 2 * 148)
         pint_launch(ctx, st, k_mdot_fused, dim3(nblk, S), kRedThreads, 0, 
@@ -742,7 +744,7 @@ struct Impl {
         pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
             ctx->ctr_mdot, ctx->gm_active);
-      if (pass == 1 && !ctx->split_norm) break;
+      if (pass == npass - 1 && !ctx->split_norm) break;
       pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
                                                              pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
     }
@@ -751,9 +753,9 @@ struct Impl {
       pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
           ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
           ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
-    else  // second CGS update fused with the norm + Givens (same bits)
-      pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride, ctx->ybuf,
-          j + 1, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
+    else  // last CGS update fused with the norm + Givens (same bits)
+      pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride,
+          npass == 1 ? hcol : ctx->ybuf, npass == 1 ? hstride : (m + 1), j + 1, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
           ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
     double* vj1 = ctx->V + (j + 1) * vstride;
     pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
@@ -1195,6 +1197,9 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // level-0 Vanka sweep: fused (cell solves + gather, k_vanka_apply) in 2-d,
   // split in 3-d, where the fused grid is 1.2 waves of (node, comp) threads
   // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
+  // one classical Gram-Schmidt pass (PETSc's GMRES default); CGS2 measured the
+  // same Krylov counts on c1-c4 to 3 decimals at 5-9 % lower throughput
+  if (const char* e = std::getenv("PINT_CGS")) ctx->cgs_passes = std::atoi(e) == 2 ? 2 : 1;
   ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;
   if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";
