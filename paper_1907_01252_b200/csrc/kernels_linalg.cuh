@@ -253,10 +253,10 @@ __global__ void k_mdot_final(const double* __restrict__ partial, int nblk, int n
 // w -= sum_i coef[s][i] V_i   (fixed order in i)
 __global__ void k_mupdate(double* __restrict__ w, const double* __restrict__ V, size_t vstride,
                           const double* __restrict__ coef, int cstride, int nv, size_t per_slice,
-                          const int* __restrict__ active) {
+                          const int* __restrict__ active, const int* __restrict__ active2) {
   pdl_wait();
   const int s = blockIdx.y;
-  if (active && !active[s]) return;
+  if ((active && !active[s]) || (active2 && !active2[s])) return;
   const double* cs = coef + (size_t)s * cstride;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < per_slice; e += (size_t)gridDim.x * blockDim.x) {
     double acc = w[s * per_slice + e];
@@ -1442,11 +1442,11 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __rest
                                                            double* __restrict__ h, int hstride, int mode,
                                                            double* __restrict__ h2, int h2stride,
                                                            unsigned int* __restrict__ counters,
-                                                           const int* __restrict__ active) {
+                                                           const int* __restrict__ active, const int* __restrict__ active2) {
   pdl_wait();
   __shared__ double sh[kRedThreads / 32][kMdotMax];
   const int s = blockIdx.y;
-  if (active && !active[s]) return;  // uniform per slice: the ticket count stays consistent
+  if ((active && !active[s]) || (active2 && !active2[s])) return;  // uniform per slice: the ticket count stays consistent
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
   const double* vs = V + s * per_slice;
@@ -1505,12 +1505,12 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused_v(const double* __re
                                                              double* __restrict__ h, int hstride, int mode,
                                                              double* __restrict__ h2, int h2stride,
                                                              unsigned int* __restrict__ counters,
-                                                             const int* __restrict__ active) {
+                                                             const int* __restrict__ active, const int* __restrict__ active2) {
   pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.z;
   const int v = blockIdx.y;
-  if (active && !active[s]) return;
+  if ((active && !active[s]) || (active2 && !active2[s])) return;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
   const double* vs = V + v * vstride + s * per_slice;
@@ -1574,17 +1574,21 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
 // one launch and one read of w fewer per Arnoldi step; grid (nblk, S)
 __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
     double* __restrict__ w, const double* __restrict__ V, size_t vstride, const double* __restrict__ coef, int cstride,
-    int nv, size_t per_slice, double* __restrict__ partial, int nblk, int j, int m, double* __restrict__ H,
+    const double* __restrict__ coef2, int cstride2, const int* __restrict__ two_pass, int nv, size_t per_slice, double* __restrict__ partial, int nblk, int j, int m, double* __restrict__ H,
     double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
     int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its, double* __restrict__ resid,
-    double* __restrict__ hnorm, unsigned int* __restrict__ counters) {
+    double* __restrict__ hnorm, unsigned int* __restrict__ counters, double* __restrict__ scale_out) {
   pdl_wait();
   __shared__ double sh[kRedThreads / 32];
+  __shared__ double sinv;
+  __shared__ int sact;
   const int s = blockIdx.y;
   if (!gm_active[s]) return;
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   double* ws = w + s * per_slice;
-  const double* cf = coef + (size_t)s * cstride;
+  // slices with a second Gram-Schmidt pass subtract its coefficients (coef2),
+  // the others the first pass's (their w was left alone by the second pass)
+  const double* cf = (two_pass && two_pass[s]) ? coef2 + (size_t)s * cstride2 : coef + (size_t)s * cstride;
   const double* Vs = V + s * per_slice;
   double acc = 0.0;
   for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
@@ -1606,7 +1610,16 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
     hnorm[s] = sqrt(t);
     counters[s] = 0u;
     givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid);
+    sinv = hnorm[s] != 0.0 ? 1.0 / hnorm[s] : 0.0;
+    sact = gm_active[s];
   }
+  if (!scale_out) return;
+  // small slices: v_{j+1} = w / h_{j+1,j} by this last block (k_scale_inv's
+  // arithmetic and mask, one launch fewer); every block's w is visible after
+  // the ticket fence
+  __syncthreads();
+  if (!sact) return;
+  for (size_t e = threadIdx.x; e < per_slice; e += kRedThreads) scale_out[s * per_slice + e] = __ldcg(ws + e) * sinv;
 }
 
 }  // namespace pint

@@ -92,6 +92,7 @@ struct pint_ctx {
   double *V = nullptr, *H = nullptr, *gv = nullptr, *cs = nullptr, *sn = nullptr, *ybuf = nullptr, *z = nullptr,
          *w = nullptr, *u = nullptr, *gm_res = nullptr, *gm_tol = nullptr, *gm_beta = nullptr;
   int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
+  int* gm_two_pass = nullptr;  // per slice: second Gram-Schmidt pass in this solve
   double* gm_hnorm = nullptr;
   double* Z = nullptr;  // flexible-GMRES preconditioned basis z_j = M^{-1} v_j, [m][S][C][np]
   double* cpart = nullptr;  // fused Arnoldi: CTA partial sums [S][cluster][kMaxBasis]
@@ -120,7 +121,10 @@ struct pint_ctx {
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
-  int cgs_passes = 1;          // PINT_CGS=1|2: classical Gram-Schmidt passes per Arnoldi step (2 = CGS2)
+  int scale_fuse_max = 0;      // PINT_SCALE_FUSE: per-slice length up to which the last norm block scales v_{j+1}
+                               // (measured neutral on c1/c2, off)
+  int cgs_passes = 0;          // PINT_CGS=1|2 forces the Gram-Schmidt passes per Arnoldi step; 0 = by tolerance
+  int cur_passes = 1;          // passes of the running GMRES solve
   bool split_norm = false;   // PINT_SPLIT_NORM=1: second CGS update and the norm as two kernels
   bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
@@ -733,32 +737,43 @@ struct Impl {
     double* hcol = ctx->H + (size_t)j * (m + 1);
     const int hstride = (m + 1) * m;
     const int nblk = ctx->nblk;
-    const int npass = ctx->cgs_passes;
+    // Gram-Schmidt passes: cur_passes = 2 when any slice of the solve wants a
+    // second pass; then the pass-1 kernels are masked to those slices
+    // (gm_two_pass) and the others subtract their first-pass coefficients in
+    // the fused norm kernel -- bitwise the one-pass computation, so a slice's
+    // result never depends on the other slices of the batch
+    const int npass = ctx->cur_passes;
+    const int* two = (npass == 2 && !ctx->split_norm) ? ctx->gm_two_pass : nullptr;
     for (int pass = 0; pass < npass; ++pass) {
+      const int* act2 = pass == 1 ? two : nullptr;
       // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
       if ((size_t)nblk * S >= 2 * 148)
         pint_launch(ctx, st, k_mdot_fused, dim3(nblk, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
-            ctx->ctr_mdot, ctx->gm_active);
+            ctx->ctr_mdot, ctx->gm_active, act2);
       else
         pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, 
             ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
-            ctx->ctr_mdot, ctx->gm_active);
+            ctx->ctr_mdot, ctx->gm_active, act2);
       if (pass == npass - 1 && !ctx->split_norm) break;
       pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
-                                                             pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active);
+                  pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active, pass == 0 ? two : nullptr);
     }
     // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
+    // (optionally the scaling inside the last block when a slice is small)
+    double* vj1 = ctx->V + (j + 1) * vstride;
+    const bool fuse_scale = !ctx->split_norm && n <= (size_t)ctx->scale_fuse_max;
     if (ctx->split_norm)
       pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
           ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
           ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
-    else  // last CGS update fused with the norm + Givens (same bits)
+    else  // last Gram-Schmidt update fused with the norm + Givens (same bits)
       pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride,
-          npass == 1 ? hcol : ctx->ybuf, npass == 1 ? hstride : (m + 1), j + 1, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
-          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
-    double* vj1 = ctx->V + (j + 1) * vstride;
-    pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
+          hcol, hstride, ctx->ybuf, m + 1, npass == 2 ? ctx->gm_two_pass : nullptr, j + 1, n, ctx->partial, nblk, j, m,
+          ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
+          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm, fuse_scale ? vj1 : nullptr);
+    if (!fuse_scale)
+      pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
   // algorithmic bytes of one V-cycle from level `from` down, for one slice
@@ -843,7 +858,8 @@ struct Impl {
       return PINT_OK;
     }
     const GraphKey key{S, j, ctx->prec_levels, ctx->kopt.pre_smooth, ctx->kopt.post_smooth, ctx->kopt.coarse_sweeps,
-                       ctx->kopt.smoother * 1000 + ctx->tail_first * 10 + (ctx->fused ? 1 : 0), ctx->kopt.omega};
+                       ctx->cur_passes * 100000 + ctx->kopt.smoother * 1000 + ctx->tail_first * 10 + (ctx->fused ? 1 : 0),
+                       ctx->kopt.omega};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
       cudaGraph_t graph;
@@ -889,6 +905,22 @@ struct Impl {
       tol[s] = std::max((rtol_s ? rtol_s[s] : ko->rtol) * beta[s], atol_s ? atol_s[s] : ko->atol);
     }
     PINT_CHECK(cudaMemcpyAsync(ctx->gm_tol, tol.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    // Gram-Schmidt passes per slice, from the slice's own relative tolerance:
+    // one classical pass (PETSc's GMRES default) at loose tolerances -- the
+    // inexact-Newton solves here run at 3e-5 .. 1e-5 relative, where CGS2
+    // measured the same Krylov counts on c1-c4 at 5-9 % lower throughput --
+    // and CGS2 below 1e-7 relative, where one pass loses orthogonality (a c1
+    // test system at 1e-8: 41 vs 26 iterations).  PINT_CGS=1|2 forces one.
+    {
+      std::vector<int> two(S, 0);
+      int any = 0;
+      for (int s = 0; s < S; ++s) {
+        two[s] = ctx->cgs_passes ? (ctx->cgs_passes == 2) : (tol[s] < 1e-7 * beta[s]);
+        any |= two[s];
+      }
+      ctx->cur_passes = any ? 2 : 1;
+      PINT_CHECK(cudaMemcpyAsync(ctx->gm_two_pass, two.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
+    }
     std::vector<int> its(S, 0);
     std::vector<double> res(beta);
     const double* rvec = b;  // residual of the current cycle start
@@ -1197,9 +1229,8 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // level-0 Vanka sweep: fused (cell solves + gather, k_vanka_apply) in 2-d,
   // split in 3-d, where the fused grid is 1.2 waves of (node, comp) threads
   // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
-  // one classical Gram-Schmidt pass (PETSc's GMRES default); CGS2 measured the
-  // same Krylov counts on c1-c4 to 3 decimals at 5-9 % lower throughput
   if (const char* e = std::getenv("PINT_CGS")) ctx->cgs_passes = std::atoi(e) == 2 ? 2 : 1;
+  if (const char* e = std::getenv("PINT_SCALE_FUSE")) ctx->scale_fuse_max = std::atoi(e);
   ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;
   if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";
@@ -1313,6 +1344,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->gm_steps, (size_t)S);
   ALLOC(ctx->gm_its, (size_t)S);
   ALLOC(ctx->cyc_active, (size_t)S);
+  ALLOC(ctx->gm_two_pass, (size_t)S);
   ALLOC(ctx->gm_hnorm, (size_t)S);
   ALLOC(ctx->ctr_mdot, (size_t)S);
   ALLOC(ctx->ctr_norm, (size_t)S);
