@@ -125,6 +125,7 @@ struct pint_ctx {
                                // (measured neutral on c1/c2, off)
   int cgs_passes = 0;          // PINT_CGS=1|2 forces the Gram-Schmidt passes per Arnoldi step; 0 = by tolerance
   int cur_passes = 1;          // passes of the running GMRES solve
+  bool host_beta = true;       // PINT_HOST_BETA=0: GMRES recomputes ||b|| on the device (one more sync)
   bool split_norm = false;   // PINT_SPLIT_NORM=1: second CGS update and the norm as two kernels
   bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
   std::vector<int> built_step;  // per slice: step of the last multigrid build in this propagate call
@@ -883,24 +884,32 @@ struct Impl {
   // ---- GMRES(m), right preconditioned:  J x = b  for slices in mask
   static int gmres(pint_ctx* ctx, int S, const double* b, double* x, const int* mask, const pint_krylov_opts* ko,
                    const double* rtol_s, const double* atol_s,
-                   int* h_its, double* h_res, cudaStream_t st) {
+                   int* h_its, double* h_res, cudaStream_t st,
+                   const int* h_mask = nullptr, const double* h_beta = nullptr) {
     const int m = ctx->restart;
     const size_t n = vs(ctx);
     const size_t vstride = (size_t)ctx->maxS * n;
+    // h_mask / h_beta: the caller's host copy of the mask and of ||b|| (the
+    // Newton loop knows both: b = -r, and ||-r|| is bitwise its ||r||), which
+    // saves two host round trips per solve
     std::vector<int> host_mask(S, 1);
-    if (mask) {
+    if (mask && h_mask) {
+      for (int s = 0; s < S; ++s) host_mask[s] = h_mask[s];
+    } else if (mask) {
       PINT_CHECK(cudaMemcpyAsync(ctx->h_int, mask, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
       PINT_CHECK(cudaStreamSynchronize(st));
       for (int s = 0; s < S; ++s) host_mask[s] = ctx->h_int[s];
     }
     // x = 0, r = b, beta = ||b||, tol = max(rtol beta0, atol)
     pint_launch(ctx, st, k_zero_active, vec_grid(n, S), 256, 0, x, n, mask);
-    PINT_TRY(norms(ctx, S, b, b, mask, true, nullptr, nullptr, st));
+    if (!h_beta) {
+      PINT_TRY(norms(ctx, S, b, b, mask, true, nullptr, nullptr, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+      PINT_CHECK(cudaStreamSynchronize(st));
+    }
     std::vector<double> beta(S, 0.0), tol(S, 0.0);
-    PINT_CHECK(cudaMemcpyAsync(ctx->h_dbl, ctx->d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
-    PINT_CHECK(cudaStreamSynchronize(st));
     for (int s = 0; s < S; ++s) {
-      beta[s] = ctx->h_dbl[s];
+      beta[s] = h_beta ? (host_mask[s] ? h_beta[s] : 0.0) : ctx->h_dbl[s];
       // per-slice stopping test: ||r|| <= max(rtol_s beta, atol_s) (defaults: the options)
       tol[s] = std::max((rtol_s ? rtol_s[s] : ko->rtol) * beta[s], atol_s ? atol_s[s] : ko->atol);
     }
@@ -1048,7 +1057,7 @@ struct Impl {
         lin_atol[s] = std::max(ko->atol, 0.1 * target[s]);
       }
       PINT_TRY(gmres(ctx, S, ctx->b, ctx->dx, ctx->d_active, ko, lin_rtol.data(), lin_atol.data(), klin.data(),
-                     kres.data(), st));
+                     kres.data(), st, running.data(), ctx->host_beta ? rnorm.data() : nullptr));
       for (int s = 0; s < S; ++s) {
         if (!running[s]) continue;
         kit[s] += klin[s];
@@ -1231,6 +1240,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
   if (const char* e = std::getenv("PINT_CGS")) ctx->cgs_passes = std::atoi(e) == 2 ? 2 : 1;
   if (const char* e = std::getenv("PINT_SCALE_FUSE")) ctx->scale_fuse_max = std::atoi(e);
+  ctx->host_beta = !(std::getenv("PINT_HOST_BETA") && std::getenv("PINT_HOST_BETA")[0] == '0');
   ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;
   if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";

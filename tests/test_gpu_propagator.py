@@ -144,3 +144,21 @@ def test_preconditioner_precision_and_refresh_do_not_move_the_solution(cuda):
         assert max(errs.values()) <= 1e-8, errs
     errs = block_errors(P, a.values, b.values)
     assert max(errs.values()) <= 1e-9, errs
+
+
+def test_host_beta_bitwise(cuda, monkeypatch):
+    """GMRES takes ||b|| = ||-r|| from the Newton loop's own residual norm
+    (default) instead of recomputing it on the device (PINT_HOST_BETA=0): the
+    same kernel computed both, so the propagation is bitwise unchanged."""
+    P = CONFIGS["c1"].problem
+    s0 = O.initial_state(P)
+    cpu = make_pair(P, 0.002)[1]
+    starts = [s0, cpu.advance(s0, 0.02)]
+    ends = [s.time + 0.02 for s in starts]
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("PINT_HOST_BETA", v)
+        gpu, _ = make_pair(P, 0.002)
+        outs.append(gpu.advance_batch(starts, ends))
+    for a, b in zip(*outs):
+        assert a.values.tobytes() == b.values.tobytes()
