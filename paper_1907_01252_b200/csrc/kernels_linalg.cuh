@@ -1634,6 +1634,12 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
 // ======================================================================
 namespace pint {
 
+#ifndef PINT_TAIL_P2
+#define PINT_TAIL_P2 4  // lanes per row of the tail residual (2-d)
+#endif
+#ifndef PINT_TAIL_P3
+#define PINT_TAIL_P3 8  // (3-d)
+#endif
 constexpr int kMaxLevels = 12;
 
 struct LevelDev {
@@ -1669,7 +1675,7 @@ __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const 
   // row instead of NOFF/3 -- the tail's phases are latency-bound.
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
-  constexpr int P = D == 2 ? 4 : 8;
+  constexpr int P = D == 2 ? PINT_TAIL_P2 : PINT_TAIL_P3;
   constexpr int OPL = (NOFF + P - 1) / P;
   const int np = L.g.np;
   const size_t vs = (size_t)C * np;
