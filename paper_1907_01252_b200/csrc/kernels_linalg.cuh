@@ -1590,14 +1590,31 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
   // the others the first pass's (their w was left alone by the second pass)
   const double* cf = (two_pass && two_pass[s]) ? coef2 + (size_t)s * cstride2 : coef + (size_t)s * cstride;
   const double* Vs = V + s * per_slice;
+  // basis vectors outer, this thread's chunk elements inner: the element
+  // loads of one vector are all in flight (same per-element operation order)
+  constexpr int PT = kRedChunk / kRedThreads;
+  double x[PT];
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const size_t e = base + threadIdx.x + t * kRedThreads;
+    x[t] = e < per_slice ? ws[e] : 0.0;
+  }
+  for (int v = 0; v < nv; ++v) {
+    const double c = cf[v];
+    const double* Vv = Vs + v * vstride;
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const size_t e = base + threadIdx.x + t * kRedThreads;
+      if (e < per_slice) x[t] -= c * __ldg(Vv + e);
+    }
+  }
   double acc = 0.0;
-  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
-    const size_t e = base + i;
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const size_t e = base + threadIdx.x + t * kRedThreads;
     if (e < per_slice) {
-      double x = ws[e];
-      for (int v = 0; v < nv; ++v) x -= cf[v] * Vs[v * vstride + e];
-      ws[e] = x;
-      acc += x * x;
+      ws[e] = x[t];
+      acc += x[t] * x[t];
     }
   }
   acc = block_sum(acc, sh);
