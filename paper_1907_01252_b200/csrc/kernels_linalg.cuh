@@ -23,6 +23,26 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// this thread's share of a chunk dot product: all element loads issued before
+// the first FMA (a rolled loop waits one memory round trip per element), the
+// products accumulated in element order
+__device__ __forceinline__ double chunk_dot(const double* __restrict__ x, const double* __restrict__ y, size_t base,
+                                            size_t per_slice) {
+  constexpr int PT = kRedChunk / kRedThreads;
+  double a[PT], b[PT];
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const size_t e = base + threadIdx.x + t * kRedThreads;
+    a[t] = e < per_slice ? x[e] : 0.0;
+    b[t] = e < per_slice ? y[e] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int t = 0; t < PT; ++t)
+    if (base + threadIdx.x + t * kRedThreads < per_slice) acc = fma(a[t], b[t], acc);
+  return acc;
+}
+
 // fixed-order block reduction; result valid in thread 0
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   v = warp_sum(v);
@@ -188,12 +208,7 @@ __global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __res
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* xs = x + s * per_slice;
   const double* ys = y + s * per_slice;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
-    const size_t e = base + i;
-    if (e < per_slice) acc += xs[e] * ys[e];
-  }
-  acc = block_sum(acc, sh);
+  const double acc = block_sum(chunk_dot(xs, ys, base, per_slice), sh);
   if (threadIdx.x == 0) partial[(size_t)s * nblk + blockIdx.x] = acc;
 }
 
@@ -1514,12 +1529,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused_v(const double* __re
   const size_t base = (size_t)blockIdx.x * kRedChunk;
   const double* ws = w + s * per_slice;
   const double* vs = V + v * vstride + s * per_slice;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < kRedChunk; i += kRedThreads) {
-    const size_t e = base + i;
-    if (e < per_slice) acc += vs[e] * ws[e];
-  }
-  acc = block_sum(acc, sh);
+  const double acc = block_sum(chunk_dot(vs, ws, base, per_slice), sh);
   if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
   if (!last_block_of_slice(counters + s, (unsigned)(nblk * nv))) return;
   for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) {
