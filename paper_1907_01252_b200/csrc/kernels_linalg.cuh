@@ -458,6 +458,37 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_restrict(Grid gf, Grid gc,
   bc[(size_t)s * (2 * D + 1) * gc.np + (size_t)c * gc.np + I] = acc;
 }
 
+// sum_I P(i, I) e[I] over the <= 2^d coarse parents of fine node (fi, fj, fk):
+// all parent loads issued first (predicated), then summed in ascending
+// (k, j, i) parent order
+template <int D>
+__device__ __forceinline__ double prolong_sum(const Grid& gc, const double* es, int fi, int fj, int fk) {
+  constexpr int KK = D == 3 ? 2 : 1;
+  const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
+  double e[KK][2][2];
+#pragma unroll
+  for (int dk = 0; dk < KK; ++dk)
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int di = 0; di < 2; ++di) {
+        const bool ok = di <= (fi & 1) && dj <= (fj & 1) && (D == 2 || dk <= (fk & 1));
+        e[dk][dj][di] = ok ? es[node_index(gc, i0 + di, j0 + dj, k0 + dk)] : 0.0;
+      }
+  double acc = 0.0;
+#pragma unroll
+  for (int dk = 0; dk < KK; ++dk)
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int di = 0; di < 2; ++di) {
+        if (!(di <= (fi & 1) && dj <= (fj & 1) && (D == 2 || dk <= (fk & 1)))) continue;
+        const double w = pweight(fi, i0 + di) * pweight(fj, j0 + dj) * (D == 3 ? pweight(fk, k0 + dk) : 1.0);
+        acc += w * e[dk][dj][di];
+      }
+  return acc;
+}
+
 // xf[c][i] += sum_I P(i, I) ec[c][I]; thread = (fine node, component), block (32, C)
 template <int D>
 __global__ void __launch_bounds__(32 * (2 * D + 1)) k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec,
@@ -471,16 +502,11 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_prolong_add(Grid gf, Grid 
   const int c = threadIdx.y;
   int fi, fj, fk;
   node_coords(gf, f, fi, fj, fk);
-  double acc = 0.0;
   const double* es = ec + (size_t)s * (2 * D + 1) * gc.np + (size_t)c * gc.np;
-  const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
-  for (int ck = k0; ck <= (D == 3 ? k0 + (fk & 1) : k0); ++ck)
-    for (int cj = j0; cj <= j0 + (fj & 1); ++cj)
-      for (int ci = i0; ci <= i0 + (fi & 1); ++ci) {
-        const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
-        acc += w * es[node_index(gc, ci, cj, ck)];
-      }
-  xf[(size_t)s * (2 * D + 1) * gf.np + (size_t)c * gf.np + f] += acc;
+  const size_t o = (size_t)s * (2 * D + 1) * gf.np + (size_t)c * gf.np + f;
+  const double xo = xf[o];
+  const double acc = prolong_sum<D>(gc, es, fi, fj, fk);
+  xf[o] = xo + acc;
 }
 
 // Galerkin coarse operator Ac = P^T Af P; thread = (coarse node, coarse offset, row comp)
@@ -1816,15 +1842,9 @@ __device__ __forceinline__ void tail_prolong(const LevelDev& F, const LevelDev& 
     const int c = idx / gf.nn, f = idx % gf.nn;
     int fi, fj, fk;
     node_coords(gf, f, fi, fj, fk);
-    double acc = 0.0;
-    const int i0 = fi >> 1, j0 = fj >> 1, k0 = fk >> 1;
-    for (int ck = k0; ck <= (D == 3 ? k0 + (fk & 1) : k0); ++ck)
-      for (int cj = j0; cj <= j0 + (fj & 1); ++cj)
-        for (int ci = i0; ci <= i0 + (fi & 1); ++ci) {
-          const double w = pweight(fi, ci) * pweight(fj, cj) * (D == 3 ? pweight(fk, ck) : 1.0);
-          acc += w * Cc.sol[(size_t)s * C * gc.np + (size_t)c * gc.np + node_index(gc, ci, cj, ck)];
-        }
-    xf[(size_t)s * C * gf.np + (size_t)c * gf.np + f] += acc;
+    const size_t o = (size_t)s * C * gf.np + (size_t)c * gf.np + f;
+    const double xo = xf[o];
+    xf[o] = xo + prolong_sum<D>(gc, Cc.sol + (size_t)s * C * gc.np + (size_t)c * gc.np, fi, fj, fk);
   }
 }
 
