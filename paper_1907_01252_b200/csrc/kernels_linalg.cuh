@@ -1367,11 +1367,25 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_apply(Grid g, const 
                                                                  const double* __restrict__ xin,
                                                                  double* __restrict__ xout, double omega,
                                                                  const int* __restrict__ active,
-                                                                 unsigned long long* __restrict__ work) {
+                                                                 unsigned long long* __restrict__ work,
+                                                                 const double* __restrict__ wsrc = nullptr,
+                                                                 const double* __restrict__ hn = nullptr,
+                                                                 double* __restrict__ vout = nullptr) {
   pdl_wait();
   constexpr int C = Cells<D>::C;
   constexpr int A = Cells<D>::A;
   constexpr int L = Cells<D>::L;
+  // wsrc != nullptr (first sweep of an Arnoldi step's V-cycle): the right-hand
+  // side is the basis vector v_j = w / h_{j,j-1} that the previous step left
+  // unscaled; it is formed here with k_scale_inv's arithmetic (x * (1/h)),
+  // staged, and written to vout by each (node, comp) owner -- bitwise the
+  // separate scaling launch, one launch fewer per Arnoldi step
+  double inv = 1.0;
+  if (wsrc) {
+    const double al = hn[blockIdx.y];
+    inv = al != 0.0 ? 1.0 / al : 0.0;
+    r = wsrc;
+  }
   constexpr int R = D == 2 ? 3 : 9;  // node-row ranges (dj, dk) in {-1,0,1}^{D-1}
   constexpr int W = 34;              // 32 nodes + one halo node either side
   __shared__ float rs[C][R][W];
@@ -1385,12 +1399,18 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_apply(Grid g, const 
     const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
     const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
     const int m = n0 - 1 + w + dj * nx + dk * nxy;
-    rs[cb][q][w] = (m >= 0 && m < g.nn) ? (float)__ldg(rsl + (size_t)cb * g.np + m) : 0.0f;
+    rs[cb][q][w] = (m >= 0 && m < g.nn) ? (float)(wsrc ? rsl[(size_t)cb * g.np + m] * inv
+                                                         : __ldg(rsl + (size_t)cb * g.np + m))
+                                        : 0.0f;
   }
   __syncthreads();
   const int n = n0 + threadIdx.x;
   if (n >= g.nn) return;
   const int c = threadIdx.y;
+  if (wsrc) {
+    const size_t ov = (size_t)s * C * g.np + (size_t)c * g.np + n;
+    vout[ov] = wsrc[ov] * inv;
+  }
   int i, j, k;
   node_coords(g, n, i, j, k);
   const int cx = g.n[0] - 1, cy = g.n[1] - 1, cz = D == 3 ? g.n[2] - 1 : 1;

@@ -125,6 +125,8 @@ struct pint_ctx {
                                // (measured neutral on c1/c2, off)
   int cgs_passes = 0;          // PINT_CGS=1|2 forces the Gram-Schmidt passes per Arnoldi step; 0 = by tolerance
   int cur_passes = 1;          // passes of the running GMRES solve
+  bool defer_scale = true;     // PINT_DEFER_SCALE=0: v_{j+1} = w / h by its own launch
+  double* defer_w = nullptr;   // set while the V-cycle's first sweep forms v_j from w
   bool host_beta = true;       // PINT_HOST_BETA=0: GMRES recomputes ||b|| on the device (one more sync)
   bool split_norm = false;   // PINT_SPLIT_NORM=1: second CGS update and the norm as two kernels
   bool vanka_split = false;  // PINT_VANKA=split|fused (default split in 3-d): separate k_vanka_cell + k_vanka_gather (y_c buffer)
@@ -597,12 +599,18 @@ struct Impl {
       }
       if (!ctx->vanka_split) {
         // fused cell solves + gather (bitwise the same as the split pair below)
-        if (first)
+        if (first && ctx->defer_w && &L == &ctx->lv[0]) {
+          // b = v_j is formed from the previous step's unscaled w inside the sweep
+          pint_launch(ctx, st, k_vanka_apply<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.vinv,
+                      (const double*)ctx->defer_w, nullptr, xout, om, mask, prof ? ctx->d_work : nullptr,
+                      (const double*)ctx->defer_w, (const double*)ctx->gm_hnorm, const_cast<double*>(b));
+          ctx->defer_w = nullptr;
+        } else if (first)
           pint_launch(ctx, st, k_vanka_apply<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.vinv, r,
-                      nullptr, xout, om, mask, prof ? ctx->d_work : nullptr);
+                      nullptr, xout, om, mask, prof ? ctx->d_work : nullptr, nullptr, nullptr, nullptr);
         else
           pint_launch(ctx, st, k_vanka_apply<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.vinv, r,
-                      xin, xout, om, mask, prof ? ctx->d_work : nullptr);
+                      xin, xout, om, mask, prof ? ctx->d_work : nullptr, nullptr, nullptr, nullptr);
         if (prof) {
           cudaEventRecord(e1, st);
           ctx->ev_pairs.emplace_back(e0, e1);
@@ -732,7 +740,13 @@ struct Impl {
     // z = M^{-1} v_j ; w = J z
     // flexible GMRES: keep z_j = M^{-1} v_j, so the update x += Z y needs no extra V-cycle
     double* zj = ctx->Z + j * vstride;
+    // v_j = w / h_{j,j-1} deferred into the first smoothing sweep of this
+    // step's V-cycle (level 0 outside the tail, fused 2-d Vanka sweep)
+    const bool defer = ctx->defer_scale && ctx->kopt.smoother == 1 && !ctx->vanka_split && ctx->tail_first != 0 &&
+                       !(ctx->prec_levels == 1 && ctx->coarse_dense) && ctx->scale_fuse_max == 0;
+    ctx->defer_w = (defer && j >= 1) ? ctx->w : nullptr;
     vcycle(ctx, 0, S, vj, zj, ctx->gm_active, st);
+    ctx->defer_w = nullptr;
     spmv(ctx, 0, S, zj, ctx->w, ctx->gm_active, st);
     // CGS2 against v_0..v_j (fused partial + last-block reductions)
     double* hcol = ctx->H + (size_t)j * (m + 1);
@@ -773,7 +787,7 @@ struct Impl {
           hcol, hstride, ctx->ybuf, m + 1, npass == 2 ? ctx->gm_two_pass : nullptr, j + 1, n, ctx->partial, nblk, j, m,
           ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
           ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm, fuse_scale ? vj1 : nullptr);
-    if (!fuse_scale)
+    if (!fuse_scale && !defer)  // deferred: step j+1 forms v_{j+1} (unused when j+1 == m)
       pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
   }
 
@@ -1240,6 +1254,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // (c4: fused 86.6 us vs split 82.9 + gather per sweep; c3: fused 212 vs 261)
   if (const char* e = std::getenv("PINT_CGS")) ctx->cgs_passes = std::atoi(e) == 2 ? 2 : 1;
   if (const char* e = std::getenv("PINT_SCALE_FUSE")) ctx->scale_fuse_max = std::atoi(e);
+  ctx->defer_scale = !(std::getenv("PINT_DEFER_SCALE") && std::getenv("PINT_DEFER_SCALE")[0] == '0');
   ctx->host_beta = !(std::getenv("PINT_HOST_BETA") && std::getenv("PINT_HOST_BETA")[0] == '0');
   ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;

@@ -162,3 +162,25 @@ def test_host_beta_bitwise(cuda, monkeypatch):
         outs.append(gpu.advance_batch(starts, ends))
     for a, b in zip(*outs):
         assert a.values.tobytes() == b.values.tobytes()
+
+
+@pytest.mark.parametrize("env", [{}, {"PINT_TAIL_ROWS": "1000"}])
+def test_deferred_basis_scaling_bitwise(cuda, monkeypatch, env):
+    """v_{j+1} = w / h formed inside the next Arnoldi step's first Vanka sweep
+    (default) or by its own launch (PINT_DEFER_SCALE=0): bitwise the same
+    propagation (PINT_TAIL_ROWS=1000 keeps c1's level 0 out of the tail, so
+    the deferred path runs)."""
+    P = CONFIGS["c1"].problem
+    s0 = O.initial_state(P)
+    cpu = make_pair(P, 0.002)[1]
+    starts = [s0, cpu.advance(s0, 0.02)]
+    ends = [s.time + 0.02 for s in starts]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("PINT_DEFER_SCALE", v)
+        gpu, _ = make_pair(P, 0.002)
+        outs.append(gpu.advance_batch(starts, ends))
+    for a, b in zip(*outs):
+        assert a.values.tobytes() == b.values.tobytes()
