@@ -103,7 +103,11 @@ int pint_flags(const pint_ctx* ctx, uint8_t* node_flags, uint8_t* cell_flags);
  * integrators.py:154-162), theta = 1/2 + theta0*k_step clamped to [1/2, 1]
  * (integrators.py:73), Newton guess = previous state (integrators.py:93).
  * y_in / y_out: device [S][C][np].  Host outputs per slice: Newton
- * iterations, Krylov iterations, status (PINT_*), failing t_n. */
+ * iterations, Krylov iterations, status (PINT_*), failing t_n.
+ * The whole call is ONE launch of a CUDA graph whose conditional WHILE / IF
+ * nodes run the time-step, Newton, line-search and GMRES loops on the device
+ * (no host round trip inside the call); PINT_DEVICE_LOOP=0 selects the
+ * host-driven loop, which gives the same bits. */
 int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, const double* t0,
                    const double* t_end, const int32_t* nsteps, double k, double theta0,
                    const pint_newton_opts* newton, const pint_krylov_opts* krylov, int32_t* newton_iters,
@@ -128,7 +132,9 @@ int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream
 /* multigrid setup on the assembled Jacobian and one V-cycle x = M^{-1} b */
 int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov, void* stream);
 int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, void* stream);
-/* GMRES solve J x = b with the current preconditioner; its/resid per slice (host) */
+/* GMRES solve J x = b with the current preconditioner; its/resid per slice (host).
+ * pint_propagate, pint_linear_solve and pint_coarse_sweep require krylov->restart to
+ * equal the context's restart length (PINT_INVALID_ARG otherwise). */
 int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, const pint_krylov_opts* krylov,
                       int32_t* its, double* resid, void* stream);
 
@@ -157,6 +163,36 @@ int pint_parareal_correct_one(int32_t C, int32_t nn, int32_t np, const double* c
                               const double* c_old, const double* x_prev, double* x_new, int32_t variant,
                               double clamp_lo, double clamp_hi, double* theta_out, double* corr_out,
                               void* stream);
+
+/* ---- the sequential corrector sweep on the device (parareal.py:410-436) --
+ * One call runs the whole sweep of one Parareal iteration: for l = 0..L-1
+ *   c_new[l] = C(x[l]) over [t_grid[l], t_grid[l+1]] in nsteps[l] coarse steps
+ *              of size k (the coarse propagator's ThetaPropagator.advance,
+ *              integrators.py:144-166, batch 1);
+ *   x[l+1]   = theta_l c_new[l] + f_old[l] - theta_l c_old[l]   (parareal_update,
+ *              parareal.py:154-163, theta_l = theta_weight(f_old[l], c_new[l]),
+ *              parareal.py:166-197, variant / clamp as pint_parareal_correct_one);
+ *   corr[l]  = ||x[l+1] - x_prev[l+1]|| / ||x[l+1]||   (parareal.py:429-431).
+ * f_old == NULL runs the coarse initialisation instead (parareal.py:410-416):
+ * x[l+1] = c_new[l], theta 1, corr 0.  Device buffers: x, x_prev [L+1][C][np]
+ * (x[0] given), c_new, c_old, f_old [L][C][np].  Every propagation is one
+ * launch of the context's device-driven loop graph; nothing synchronises the
+ * host until the end.  Host outputs per l: theta, corr, Newton / Krylov
+ * iterations, status (PINT_*) and failing t_n of the coarse propagation.  A
+ * failed slice leaves the later ones undefined; the caller reports the first
+ * failing l (parareal.py:437-440). */
+int pint_coarse_sweep(pint_ctx* ctx, int32_t L, double* x, const double* x_prev, double* c_new, const double* c_old,
+                      const double* f_old, const double* t_grid, const int32_t* nsteps, double k, double theta0,
+                      const pint_newton_opts* newton, const pint_krylov_opts* krylov, int32_t variant,
+                      double clamp_lo, double clamp_hi, double* theta_out, double* corr_out, int32_t* newton_iters,
+                      int32_t* krylov_iters, int32_t* status, double* fail_t, void* stream);
+
+/* boundary_error (parareal.py:200-213) for S slices on the device:
+ * err[s] = ||x_s - ref_s|| / ||ref_s||, or the absolute ||x_s - ref_s|| with
+ * absolute[s] = 1 when ||ref_s|| = 0 (ErrorEntry, parareal.py:106-111).
+ * x, ref: device [S][C][np]; err, absolute: host. */
+int pint_boundary_error(pint_ctx* ctx, int32_t S, const double* x, const double* ref, double* err,
+                        int32_t* absolute, void* stream);
 
 #ifdef __cplusplus
 }

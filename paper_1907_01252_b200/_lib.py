@@ -36,7 +36,7 @@ EXPORTS = (
     "pint_propagate", "pint_residual", "pint_jvp", "pint_assemble", "pint_jacobian_blocks",
     "pint_spmv", "pint_precond_setup", "pint_precond_apply", "pint_linear_solve",
     "pint_parareal_precorrect", "pint_parareal_correct_one", "pint_profile", "pint_profile_read",
-    "pint_profile_kernel",
+    "pint_profile_kernel", "pint_coarse_sweep", "pint_boundary_error",
 )
 
 
@@ -110,6 +110,9 @@ _SIGNATURES = {
     "pint_linear_solve": (_I, [_P, _I, _P, _P, ctypes.POINTER(KrylovOpts), _IP, _DP, _P]),
     "pint_parareal_precorrect": (_I, [_I, _I, _I, _I, _P, _P, _P, _P]),
     "pint_parareal_correct_one": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _DP, _DP, _P]),
+    "pint_coarse_sweep": (_I, [_P, _I, _P, _P, _P, _P, _P, _DP, _IP, _D, _D, ctypes.POINTER(NewtonOpts),
+                               ctypes.POINTER(KrylovOpts), _I, _D, _D, _DP, _DP, _IP, _IP, _IP, _DP, _P]),
+    "pint_boundary_error": (_I, [_P, _I, _P, _P, _DP, _IP, _P]),
     "pint_profile": (_I, [_P, _I]),
     "pint_profile_kernel": (ctypes.c_char_p, [_P]),
     "pint_profile_read": (_I, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),

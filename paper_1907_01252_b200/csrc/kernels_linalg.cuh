@@ -946,42 +946,6 @@ __global__ void k_dense_apply(Grid g, const float* __restrict__ M, int ld, const
 }
 
 // ---------------------------------------------------------------- GMRES scalar work (one thread per slice)
-// Arnoldi column j of H is in h[s][0..j+1]; applies previous Givens
-// rotations, builds rotation j, updates g and the convergence state.
-__global__ void k_gmres_givens(int j, int m, double* __restrict__ H, double* __restrict__ cs,
-                               double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
-                               int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its,
-                               double* __restrict__ resid, int S) {
-  pdl_wait();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
-  if (!gm_active[s]) return;
-  double* h = H + (size_t)s * (m + 1) * m + (size_t)j * (m + 1);  // column-major column j
-  double* c = cs + (size_t)s * m;
-  double* sv = sn + (size_t)s * m;
-  double* g = gv + (size_t)s * (m + 1);
-  for (int i = 0; i < j; ++i) {
-    const double t = c[i] * h[i] + sv[i] * h[i + 1];
-    h[i + 1] = -sv[i] * h[i] + c[i] * h[i + 1];
-    h[i] = t;
-  }
-  const double a = h[j], b = h[j + 1];
-  const double r = hypot(a, b);
-  double cj = 1.0, sj = 0.0;
-  if (r != 0.0) { cj = a / r; sj = b / r; }
-  c[j] = cj;
-  sv[j] = sj;
-  h[j] = r;
-  h[j + 1] = 0.0;
-  g[j + 1] = -sj * g[j];
-  g[j] = cj * g[j];
-  gm_steps[s] = j + 1;
-  its[s] += 1;
-  const double res = fabs(g[j + 1]);
-  resid[s] = res;
-  if (res <= tol[s] || b == 0.0 || j + 1 == m) gm_active[s] = 0;
-}
-
 // back substitution H y = g for the steps taken this cycle
 __global__ void k_gmres_solve(int m, const double* __restrict__ H, const double* __restrict__ gv,
                               const int* __restrict__ gm_steps, double* __restrict__ y, const int* __restrict__ active,
@@ -1466,7 +1430,7 @@ __device__ __forceinline__ bool last_block_of_slice(unsigned int* counter, unsig
 // Givens update of column j for one slice (body of k_gmres_givens)
 __device__ __forceinline__ void givens_one(int s, int j, int m, double* H, double* cs, double* sn, double* gv,
                                            const double* tol, int* gm_active, int* gm_steps, int* its,
-                                           double* resid) {
+                                           double* resid, const int* cap) {
   double* h = H + (size_t)s * (m + 1) * m + (size_t)j * (m + 1);
   double* c = cs + (size_t)s * m;
   double* sv = sn + (size_t)s * m;
@@ -1490,7 +1454,9 @@ __device__ __forceinline__ void givens_one(int s, int j, int m, double* H, doubl
   its[s] += 1;
   const double res = fabs(g[j + 1]);
   resid[s] = res;
-  if (res <= tol[s] || b == 0.0 || j + 1 == m) gm_active[s] = 0;
+  // per-slice Krylov budget (cap = pint_krylov_opts.max_iters): a slice near
+  // its budget stops alone, the rest of the batch keeps its restart cycle
+  if (res <= tol[s] || b == 0.0 || j + 1 == m || its[s] >= *cap) gm_active[s] = 0;
 }
 
 // CGS pass: h[v] = <V_v, w> (mode 0) or h2[v] = <V_v, w>, h[v] += h2[v] (mode 1);
@@ -1599,7 +1565,8 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
                                                             const double* __restrict__ tol, int* __restrict__ gm_active,
                                                             int* __restrict__ gm_steps, int* __restrict__ its,
                                                             double* __restrict__ resid, double* __restrict__ hnorm,
-                                                            unsigned int* __restrict__ counters) {
+                                                            unsigned int* __restrict__ counters,
+                                                            const int* __restrict__ cap) {
   pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   const int s = blockIdx.y;
@@ -1620,7 +1587,7 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
     H[(size_t)s * (m + 1) * m + (size_t)j * (m + 1) + j + 1] = sqrt(t);
     hnorm[s] = sqrt(t);  // kept for v_{j+1} = w / h_{j+1,j}: the rotation zeroes H[j+1][j]
     counters[s] = 0u;
-    givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid);
+    givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid, cap);
   }
 }
 
@@ -1633,7 +1600,8 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
     const double* __restrict__ coef2, int cstride2, const int* __restrict__ two_pass, int nv, size_t per_slice, double* __restrict__ partial, int nblk, int j, int m, double* __restrict__ H,
     double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ gv, const double* __restrict__ tol,
     int* __restrict__ gm_active, int* __restrict__ gm_steps, int* __restrict__ its, double* __restrict__ resid,
-    double* __restrict__ hnorm, unsigned int* __restrict__ counters, double* __restrict__ scale_out) {
+    double* __restrict__ hnorm, unsigned int* __restrict__ counters, double* __restrict__ scale_out,
+    const int* __restrict__ cap) {
   pdl_wait();
   __shared__ double sh[kRedThreads / 32];
   __shared__ double sinv;
@@ -1682,7 +1650,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
     H[(size_t)s * (m + 1) * m + (size_t)j * (m + 1) + j + 1] = sqrt(t);
     hnorm[s] = sqrt(t);
     counters[s] = 0u;
-    givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid);
+    givens_one(s, j, m, H, cs, sn, gv, tol, gm_active, gm_steps, its, resid, cap);
     sinv = hnorm[s] != 0.0 ? 1.0 / hnorm[s] : 0.0;
     sact = gm_active[s];
   }
@@ -2093,6 +2061,7 @@ struct ArnoldiArgs {
   int* its;
   double* resid;
   double* hnorm;
+  const int* cap;           // Krylov budget (givens_one)
   double* cpart;            // [S][CL][kMaxBasis] CTA partials
   double* ybuf;             // [S][m+1] second-pass coefficients
   unsigned long long* work_bytes;  // profiling: algorithmic bytes of active slices (nullptr: off)
@@ -2205,7 +2174,7 @@ __device__ __forceinline__ void arnoldi_body(const ArnoldiArgs& a) {
     if (rank == 0 && threadIdx.x == 0) {
       hcol[j + 1] = hn;
       a.hnorm[s] = hn;
-      givens_one(s, j, m, a.H, a.cs, a.sn, a.gv, a.tol, a.gm_active, a.gm_steps, a.its, a.resid);
+      givens_one(s, j, m, a.H, a.cs, a.sn, a.gv, a.tol, a.gm_active, a.gm_steps, a.its, a.resid, a.cap);
     }
   }
 }

@@ -17,8 +17,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
+#include <set>
 #include <tuple>
 #include <utility>
 #include <string>
@@ -27,6 +29,7 @@
 #include "../../include/pint_b200.h"
 #include "kernels_assembly.cuh"
 #include "kernels_linalg.cuh"
+#include "kernels_loop.cuh"
 #include "kernels_parareal.cuh"
 
 using namespace pint;
@@ -35,6 +38,8 @@ namespace {
 
 constexpr int kDenseMax = 1024;
 constexpr size_t kTailSmemMax = 220 * 1024;  // dynamic shared memory of a staged tail CTA
+constexpr int kCapDepth = 8;      // nesting depth of conditional graph bodies (one capture stream each)
+constexpr int kMaxBodies = 16384; // conditional bodies over all loop graphs of a context
 
 struct Level {
   Grid g;
@@ -159,6 +164,34 @@ struct pint_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   pint_krylov_opts kopt{};
+  int* gm_cap = nullptr;        // Krylov budget of the running solve (givens_one)
+  int* h_cap = nullptr;         // pinned
+  // ---- device-driven control flow (Impl::propagate_dev): the whole
+  // propagate call as one CUDA graph with conditional WHILE / IF nodes
+  bool device_loop = true;      // PINT_DEVICE_LOOP=0: host-driven Newton / GMRES
+  LoopDev ld{};
+  LoopScalars* h_ls = nullptr;  // pinned staging of the call scalars
+  size_t tab_cap = 0, lsv_cap = 0;
+  StepScalars *d_sts = nullptr, *h_sts = nullptr;   // step tables [entries]
+  double *d_t1tab = nullptr, *h_t1tab = nullptr;
+  int *d_nsteps = nullptr, *h_nsteps = nullptr;
+  LoopScalars *d_lsv = nullptr, *h_lsv = nullptr;   // per-slice call scalars of a coarse sweep
+  int* h_out_i = nullptr;       // pinned outputs [4][maxS]
+  double* h_out_d = nullptr;
+  cudaStream_t cap_st[kCapDepth] = {};
+  cudaGraph_t cap_root = nullptr;  // root graph of the running capture (conditional handles live here)
+  std::set<cudaStream_t> nopdl;    // streams whose next launch must not carry the PDL attribute
+  bool capturing = false;          // a loop graph is being captured
+  std::map<std::vector<double>, std::pair<cudaGraphExec_t, long long>> loop_graphs;
+  std::vector<int> body_nodes;     // kernel nodes per conditional body (host copy)
+  int* d_body_nodes = nullptr;
+  unsigned long long* d_launch_ctr = nullptr;
+  // coarse sweep / boundary-error scratch (grown on demand)
+  size_t sw_cap = 0;
+  double *sw_part = nullptr, *sw_theta = nullptr, *sw_corr = nullptr, *sw_ft = nullptr;
+  int *sw_status = nullptr, *sw_nit = nullptr, *sw_kit = nullptr;
+  double* h_sw = nullptr;
+  std::vector<void*> grown;  // freed at destroy
 };
 
 // CTAs per slice of the V-cycle tail: the largest cluster whose S*CL CTAs run in
@@ -192,7 +225,9 @@ static inline void pint_launch(pint_ctx* ctx, cudaStream_t st, void (*kern)(KArg
   cfg.stream = counted(ctx, st);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  // no programmatic edge out of a conditional / memset node or into the first node of a body
+  const bool pdl = ctx->pdl && !(ctx->capturing && ctx->nopdl.erase(st));
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
@@ -245,6 +280,57 @@ int dalloc(pint_ctx* ctx, T** p, size_t count) {
     int rc_ = (x);           \
     if (rc_ != PINT_OK) return rc_; \
   } while (0)
+
+// ---------------------------------------------------------------- conditional graph capture
+// A conditional node is appended to the capture frontier of `st`; its body is
+// captured on the next stream of the context's capture-stream stack.  The
+// handle lives in the root graph of the capture; `idx` names the body's slot
+// in body_nodes (its kernel-node count, for the device launch counter).
+int new_cond(pint_ctx* ctx, cudaGraphConditionalHandle* h) {
+  PINT_CHECK(cudaGraphConditionalHandleCreate(h, ctx->cap_root, 0, 0));
+  if ((int)ctx->body_nodes.size() >= kMaxBodies) {
+    ctx->err = "too many conditional bodies (loop-graph cache exhausted)";
+    return PINT_CUDA_ERROR;
+  }
+  ctx->body_nodes.push_back(0);
+  return PINT_OK;
+}
+
+int capture_cond(pint_ctx* ctx, cudaStream_t st, int depth, cudaGraphConditionalHandle h, bool loop, int idx,
+                 const std::function<int(cudaStream_t, int)>& body) {
+  if (depth + 1 >= kCapDepth) {
+    ctx->err = "conditional nesting too deep";
+    return PINT_CUDA_ERROR;
+  }
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  PINT_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = loop ? cudaGraphCondTypeWhile : cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  PINT_CHECK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  cudaGraph_t bg = p.conditional.phGraph_out[0];
+  PINT_CHECK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  ctx->nopdl.insert(st);
+  cudaStream_t cst = ctx->cap_st[depth + 1];
+  PINT_CHECK(cudaStreamBeginCaptureToGraph(cst, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  ctx->nopdl.insert(cst);
+  const long long before = ctx->launches;
+  const int rc = body(cst, depth + 1);
+  const long long n = ctx->launches - before;
+  ctx->launches = before;
+  cudaGraph_t out = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(cst, &out);
+  if (rc != PINT_OK) return rc;
+  PINT_CHECK(e);
+  ctx->body_nodes[idx] = (int)n;
+  return PINT_OK;
+}
 
 Grid make_grid(int dim, const int* cells) {
   Grid g{};
@@ -381,6 +467,7 @@ struct Impl {
     MeshDev m = mesh(ctx);
     pint_launch(ctx, st, k_zero_active, vec_grid(vs(ctx), S), 256, 0, r, vs(ctx), mask);
     cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
+    if (ctx->capturing) ctx->nopdl.insert(st);  // memset node: no programmatic edge out of it
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
@@ -732,13 +819,13 @@ struct Impl {
   // v_{j+1} = w / h_{j+1,j}, Givens update.  Every scalar it needs lives in
   // device memory, so the sequence is captured once per (S, j, options) as
   // a CUDA graph and replayed.
-  static void arnoldi_step(pint_ctx* ctx, int S, int j, cudaStream_t st) {
-    const int m = ctx->restart;
-    const size_t n = vs(ctx);
-    const size_t vstride = (size_t)ctx->maxS * n;
+  //
+  // front: z_j = M^{-1} v_j (flexible GMRES keeps z_j, so the update x += Z y
+  // needs no extra V-cycle), w = J z_j; returns whether v_{j+1} = w / h is
+  // deferred into the next step's first level-0 Vanka sweep
+  static bool arnoldi_front(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    const size_t vstride = (size_t)ctx->maxS * vs(ctx);
     double* vj = ctx->V + j * vstride;
-    // z = M^{-1} v_j ; w = J z
-    // flexible GMRES: keep z_j = M^{-1} v_j, so the update x += Z y needs no extra V-cycle
     double* zj = ctx->Z + j * vstride;
     // v_j = w / h_{j,j-1} deferred into the first smoothing sweep of this
     // step's V-cycle (level 0 outside the tail, fused 2-d Vanka sweep)
@@ -748,10 +835,66 @@ struct Impl {
     vcycle(ctx, 0, S, vj, zj, ctx->gm_active, st);
     ctx->defer_w = nullptr;
     spmv(ctx, 0, S, zj, ctx->w, ctx->gm_active, st);
-    // CGS2 against v_0..v_j (fused partial + last-block reductions)
+    return defer;
+  }
+
+  // Gram-Schmidt dots of pass `pass` (h = <V, w>; pass 1 into ybuf and h += ybuf)
+  static void cgs_mdot(pint_ctx* ctx, int S, int j, int pass, const int* act2, cudaStream_t st) {
+    const int m = ctx->restart;
+    const size_t n = vs(ctx);
+    const size_t vstride = (size_t)ctx->maxS * n;
     double* hcol = ctx->H + (size_t)j * (m + 1);
     const int hstride = (m + 1) * m;
     const int nblk = ctx->nblk;
+    // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
+    if ((size_t)nblk * S >= 2 * 148)
+      pint_launch(ctx, st, k_mdot_fused, dim3(nblk, S), kRedThreads, 0, ctx->V, vstride, ctx->w, j + 1, n,
+                  ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1, ctx->ctr_mdot, ctx->gm_active,
+                  act2);
+    else
+      pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, ctx->V, vstride, ctx->w, j + 1, n,
+                  ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1, ctx->ctr_mdot, ctx->gm_active,
+                  act2);
+  }
+
+  // w -= sum_v c_v V_v with the pass's coefficients (h after pass 0, ybuf after pass 1)
+  static void cgs_update(pint_ctx* ctx, int S, int j, int pass, const int* mask2, cudaStream_t st) {
+    const int m = ctx->restart;
+    const size_t n = vs(ctx);
+    const size_t vstride = (size_t)ctx->maxS * n;
+    double* hcol = ctx->H + (size_t)j * (m + 1);
+    const int hstride = (m + 1) * m;
+    pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
+                pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active, mask2);
+  }
+
+  // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
+  // (optionally the scaling inside the last block when a slice is small);
+  // two: per-slice second-pass flags (nullptr: every slice ran one pass)
+  static void arnoldi_tail(pint_ctx* ctx, int S, int j, const int* two, bool defer, cudaStream_t st) {
+    const int m = ctx->restart;
+    const size_t n = vs(ctx);
+    const size_t vstride = (size_t)ctx->maxS * n;
+    double* hcol = ctx->H + (size_t)j * (m + 1);
+    const int hstride = (m + 1) * m;
+    const int nblk = ctx->nblk;
+    double* vj1 = ctx->V + (j + 1) * vstride;
+    const bool fuse_scale = !ctx->split_norm && n <= (size_t)ctx->scale_fuse_max;
+    if (ctx->split_norm)
+      pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, n, ctx->partial, nblk, j, m, ctx->H,
+                  ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res,
+                  ctx->gm_hnorm, ctx->ctr_norm, (const int*)ctx->gm_cap);
+    else  // last Gram-Schmidt update fused with the norm + Givens (same bits)
+      pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride, hcol,
+                  hstride, ctx->ybuf, m + 1, two, j + 1, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn,
+                  ctx->gv, ctx->gm_tol, ctx->gm_active, ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm,
+                  ctx->ctr_norm, fuse_scale ? vj1 : nullptr, (const int*)ctx->gm_cap);
+    if (!fuse_scale && !defer)  // deferred: step j+1 forms v_{j+1} (unused when j+1 == m)
+      pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
+  }
+
+  static void arnoldi_step(pint_ctx* ctx, int S, int j, cudaStream_t st) {
+    const bool defer = arnoldi_front(ctx, S, j, st);
     // Gram-Schmidt passes: cur_passes = 2 when any slice of the solve wants a
     // second pass; then the pass-1 kernels are masked to those slices
     // (gm_two_pass) and the others subtract their first-pass coefficients in
@@ -760,35 +903,27 @@ struct Impl {
     const int npass = ctx->cur_passes;
     const int* two = (npass == 2 && !ctx->split_norm) ? ctx->gm_two_pass : nullptr;
     for (int pass = 0; pass < npass; ++pass) {
-      const int* act2 = pass == 1 ? two : nullptr;
-      // wide grids: one block per chunk reading w once; narrow grids (c1/c2): one block per (chunk, vector)
-      if ((size_t)nblk * S >= 2 * 148)
-        pint_launch(ctx, st, k_mdot_fused, dim3(nblk, S), kRedThreads, 0, 
-            ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
-            ctx->ctr_mdot, ctx->gm_active, act2);
-      else
-        pint_launch(ctx, st, k_mdot_fused_v, dim3(nblk, j + 1, S), kRedThreads, 0, 
-            ctx->V, vstride, ctx->w, j + 1, n, ctx->partial, nblk, m + 1, hcol, hstride, pass, ctx->ybuf, m + 1,
-            ctx->ctr_mdot, ctx->gm_active, act2);
+      cgs_mdot(ctx, S, j, pass, pass == 1 ? two : nullptr, st);
       if (pass == npass - 1 && !ctx->split_norm) break;
-      pint_launch(ctx, st, k_mupdate, vec_grid(n, S), 256, 0, ctx->w, ctx->V, vstride, pass == 0 ? hcol : ctx->ybuf,
-                  pass == 0 ? hstride : (m + 1), j + 1, n, ctx->gm_active, pass == 0 ? two : nullptr);
+      cgs_update(ctx, S, j, pass, pass == 0 ? two : nullptr, st);
     }
-    // h_{j+1,j} = ||w||, Givens update (last block per slice), v_{j+1} = w / h_{j+1,j}
-    // (optionally the scaling inside the last block when a slice is small)
-    double* vj1 = ctx->V + (j + 1) * vstride;
-    const bool fuse_scale = !ctx->split_norm && n <= (size_t)ctx->scale_fuse_max;
-    if (ctx->split_norm)
-      pint_launch(ctx, st, k_norm_givens, dim3(nblk, S), kRedThreads, 0, 
-          ctx->w, n, ctx->partial, nblk, j, m, ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
-          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm);
-    else  // last Gram-Schmidt update fused with the norm + Givens (same bits)
-      pint_launch(ctx, st, k_mupdate_norm_givens, dim3(nblk, S), kRedThreads, 0, ctx->w, ctx->V, vstride,
-          hcol, hstride, ctx->ybuf, m + 1, npass == 2 ? ctx->gm_two_pass : nullptr, j + 1, n, ctx->partial, nblk, j, m,
-          ctx->H, ctx->cs, ctx->sn, ctx->gv, ctx->gm_tol, ctx->gm_active,
-          ctx->gm_steps, ctx->gm_its, ctx->gm_res, ctx->gm_hnorm, ctx->ctr_norm, fuse_scale ? vj1 : nullptr);
-    if (!fuse_scale && !defer)  // deferred: step j+1 forms v_{j+1} (unused when j+1 == m)
-      pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, vj1, ctx->w, ctx->gm_hnorm, n, ctx->gm_active);
+    arnoldi_tail(ctx, S, j, npass == 2 ? ctx->gm_two_pass : nullptr, defer, st);
+  }
+
+  // the same step inside the device-driven loop: the second Gram-Schmidt pass
+  // runs under IF(any active slice wants it), set by k_arnoldi_gate
+  static int arnoldi_step_dev(pint_ctx* ctx, int S, int j, cudaStream_t st, int depth,
+                              cudaGraphConditionalHandle h_two, int i_two) {
+    const bool defer = arnoldi_front(ctx, S, j, st);
+    cgs_mdot(ctx, S, j, 0, nullptr, st);
+    PINT_TRY(capture_cond(ctx, st, depth, h_two, false, i_two, [&](cudaStream_t s2, int) {
+      cgs_update(ctx, S, j, 0, ctx->gm_two_pass, s2);
+      cgs_mdot(ctx, S, j, 1, ctx->gm_two_pass, s2);
+      return PINT_OK;
+    }));
+    arnoldi_tail(ctx, S, j, ctx->gm_two_pass, defer, st);
+    PINT_LAUNCHED();
+    return PINT_OK;
   }
 
   // algorithmic bytes of one V-cycle from level `from` down, for one slice
@@ -842,6 +977,7 @@ struct Impl {
     a.its = ctx->gm_its;
     a.resid = ctx->gm_res;
     a.hnorm = ctx->gm_hnorm;
+    a.cap = ctx->gm_cap;
     a.cpart = ctx->cpart;
     a.ybuf = ctx->ybuf;
     a.work_bytes = ctx->prof ? ctx->d_work_bytes : nullptr;
@@ -928,6 +1064,8 @@ struct Impl {
       tol[s] = std::max((rtol_s ? rtol_s[s] : ko->rtol) * beta[s], atol_s ? atol_s[s] : ko->atol);
     }
     PINT_CHECK(cudaMemcpyAsync(ctx->gm_tol, tol.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    *ctx->h_cap = ko->max_iters;  // per-slice budget, applied by the Givens update on the device
+    PINT_CHECK(cudaMemcpyAsync(ctx->gm_cap, ctx->h_cap, sizeof(int), cudaMemcpyHostToDevice, st));
     // Gram-Schmidt passes per slice, from the slice's own relative tolerance:
     // one classical pass (PETSc's GMRES default) at loose tolerances -- the
     // inexact-Newton solves here run at 3e-5 .. 1e-5 relative, where CGS2
@@ -966,13 +1104,9 @@ struct Impl {
       PINT_CHECK(cudaMemcpyAsync(ctx->gv, g0.data(), sizeof(double) * g0.size(), cudaMemcpyHostToDevice, st));
       PINT_CHECK(cudaMemcpyAsync(ctx->gm_beta, res.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
       pint_launch(ctx, st, k_scale_inv, vec_grid(n, S), 256, 0, ctx->V, rvec, ctx->gm_beta, n, ctx->cyc_active);
-      int remaining_cap = m;
-      for (int s = 0; s < S; ++s)
-        if (cyc[s]) remaining_cap = std::min(remaining_cap, std::max(1, ko->max_iters - its[s]));
       for (int j = 0; j < m; ++j) {
         PINT_TRY(run_arnoldi(ctx, S, j, st));
         PINT_LAUNCHED();
-        if (j + 1 >= remaining_cap) break;
         // poll: any slice still iterating?
         if ((j + 1) % ctx->poll_every == 0 || j + 1 == m) {
           PINT_CHECK(cudaMemcpyAsync(ctx->h_int, ctx->gm_active, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
@@ -1181,6 +1315,116 @@ struct Impl {
     }
     return PINT_OK;
   }
+
+  // ================================================================ device-driven control flow
+  // The whole propagate call captured as ONE CUDA graph whose WHILE / IF
+  // conditional nodes are driven by the controller kernels of
+  // kernels_loop.cuh: time steps -> Newton iterations -> (multigrid rebuild)
+  // -> GMRES cycles -> Arnoldi steps, and the line search.  The control flow is
+  // the host path's (propagate / newton_step / gmres above) statement for
+  // statement; every per-slice decision is made on the device from the
+  // slice's own numbers, so there is no host round trip inside the call and the
+  // result equals the host-driven path bitwise.
+  static int capture_propagate(pint_ctx* ctx, int S, const pint_krylov_opts* ko, cudaStream_t st0) {
+    const size_t n = vs(ctx);
+    const int m = ctx->restart;
+    const size_t vstride = (size_t)ctx->maxS * n;
+    const LoopDev d = ctx->ld;
+    cudaGraphConditionalHandle h_step;
+    const int i_step = (int)ctx->body_nodes.size();
+    PINT_TRY(new_cond(ctx, &h_step));
+    pint_launch(ctx, st0, k_loop_init, 1, kLoopThreads, 0, d, h_step, i_step);
+    return capture_cond(ctx, st0, 0, h_step, true, i_step, [&](cudaStream_t s1, int dp1) -> int {
+      // ---- one time step (integrators.py:154-162; guess = previous state, integrators.py:93)
+      pint_launch(ctx, s1, k_step_begin, 1, kLoopThreads, 0, d);
+      pint_launch(ctx, s1, k_copy_active, vec_grid(n, S), 256, 0, ctx->ynew, (const double*)ctx->ystate, n,
+                  (const int*)d.act);
+      PINT_TRY(residual(ctx, S, ctx->ynew, ctx->ystate, ctx->r, d.act, nullptr, s1));
+      cudaGraphConditionalHandle h_newton;
+      const int i_newton = (int)ctx->body_nodes.size();
+      PINT_TRY(new_cond(ctx, &h_newton));
+      pint_launch(ctx, s1, k_newton_init, 1, kLoopThreads, 0, d, h_newton, i_newton);
+      PINT_TRY(capture_cond(ctx, s1, dp1, h_newton, true, i_newton, [&](cudaStream_t s2, int dp2) -> int {
+        // ---- one Newton iteration (linalg.py:220-240)
+        PINT_TRY(assemble(ctx, S, ctx->ynew, ctx->ystate, d.running, s2));
+        cudaGraphConditionalHandle h_prec;
+        const int i_prec = (int)ctx->body_nodes.size();
+        PINT_TRY(new_cond(ctx, &h_prec));
+        pint_launch(ctx, s2, k_precond_decide, 1, kLoopThreads, 0, d, h_prec, i_prec);
+        PINT_TRY(capture_cond(ctx, s2, dp2, h_prec, false, i_prec, [&](cudaStream_t s3, int) -> int {
+          return precond_setup(ctx, S, ko, d.need, s3);
+        }));
+        pint_launch(ctx, s2, k_negate, vec_grid(n, S), 256, 0, ctx->b, (const double*)ctx->r, n, (const int*)d.running);
+        pint_launch(ctx, s2, k_zero_active, vec_grid(n, S), 256, 0, ctx->dx, n, (const int*)d.running);
+        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->u, (const double*)ctx->b, n,
+                    (const int*)d.running);
+        cudaGraphConditionalHandle h_cycle;
+        const int i_cycle = (int)ctx->body_nodes.size();
+        PINT_TRY(new_cond(ctx, &h_cycle));
+        pint_launch(ctx, s2, k_gmres_init, 1, kLoopThreads, 0, d, h_cycle, i_cycle);
+        PINT_TRY(capture_cond(ctx, s2, dp2, h_cycle, true, i_cycle, [&](cudaStream_t s3, int dp3) -> int {
+          // ---- one restart cycle of flexible GMRES(m): v0 = r / beta
+          pint_launch(ctx, s3, k_scale_inv, vec_grid(n, S), 256, 0, ctx->V, (const double*)ctx->u,
+                      (const double*)ctx->gm_beta, n, (const int*)ctx->cyc_active);
+          for (int j = 0; j < m; ++j) {
+            cudaGraphConditionalHandle h_j, h_two;
+            const int i_j = (int)ctx->body_nodes.size();
+            PINT_TRY(new_cond(ctx, &h_j));
+            const int i_two = (int)ctx->body_nodes.size();
+            PINT_TRY(new_cond(ctx, &h_two));
+            pint_launch(ctx, s3, k_arnoldi_gate, 1, kLoopThreads, 0, d, h_j, i_j, h_two, i_two);
+            PINT_TRY(capture_cond(ctx, s3, dp3, h_j, false, i_j, [&](cudaStream_t s4, int dp4) -> int {
+              return arnoldi_step_dev(ctx, S, j, s4, dp4, h_two, i_two);
+            }));
+          }
+          // x += Z y (flexible GMRES), true residual r = b - J x into u (next cycle start)
+          pint_launch(ctx, s3, k_gmres_solve, (S + 127) / 128, 128, 0, m, (const double*)ctx->H,
+                      (const double*)ctx->gv, (const int*)ctx->gm_steps, ctx->ybuf, (const int*)ctx->cyc_active, S);
+          pint_launch(ctx, s3, k_mcombine, vec_grid(n, S), 256, 0, ctx->u, (const double*)ctx->Z, vstride,
+                      (const double*)ctx->ybuf, m + 1, (const int*)ctx->gm_steps, n, (const int*)ctx->cyc_active);
+          pint_launch(ctx, s3, k_axpy_one, vec_grid(n, S), 256, 0, ctx->dx, (const double*)ctx->u, n,
+                      (const int*)ctx->cyc_active);
+          if (wide(ctx->g.nn, S))
+            pint_launch(ctx, s3, k_spmv<D, true, 3>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
+                        (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
+                        (const int*)ctx->cyc_active);
+          else
+            pint_launch(ctx, s3, k_spmv<D, true, 9>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
+                        (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
+                        (const int*)ctx->cyc_active);
+          PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, s3));
+          pint_launch(ctx, s3, k_cycle_end, 1, kLoopThreads, 0, d, h_cycle, i_cycle);
+          return PINT_OK;
+        }));
+        pint_launch(ctx, s2, k_gmres_end, 1, kLoopThreads, 0, d);
+        // ---- line search: lambda = 1, halve down to damping_min, accept anyway
+        cudaGraphConditionalHandle h_ls;
+        const int i_ls = (int)ctx->body_nodes.size();
+        PINT_TRY(new_cond(ctx, &h_ls));
+        pint_launch(ctx, s2, k_ls_init, 1, kLoopThreads, 0, d, h_ls, i_ls);
+        PINT_TRY(capture_cond(ctx, s2, dp2, h_ls, true, i_ls, [&](cudaStream_t s3, int) -> int {
+          pint_launch(ctx, s3, k_trial, vec_grid(n, S), 256, 0, ctx->ytrial, (const double*)ctx->ynew,
+                      (const double*)ctx->dx, (const double*)d.lam, n, (const int*)d.ls_mask);
+          PINT_TRY(residual(ctx, S, ctx->ytrial, ctx->ystate, ctx->rtrial, d.ls_mask, nullptr, s3));
+          pint_launch(ctx, s3, k_ls_update, 1, kLoopThreads, 0, d, h_ls, i_ls);
+          return PINT_OK;
+        }));
+        pint_launch(ctx, s2, k_accept, 1, kLoopThreads, 0, d);
+        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->ynew, (const double*)ctx->ytrial, n,
+                    (const int*)d.accept);
+        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->r, (const double*)ctx->rtrial, n,
+                    (const int*)d.accept);
+        pint_launch(ctx, s2, k_newton_update, 1, kLoopThreads, 0, d, h_newton, i_newton);
+        PINT_LAUNCHED();
+        return PINT_OK;
+      }));
+      pint_launch(ctx, s1, k_step_end, 1, kLoopThreads, 0, d, h_step, i_step);
+      pint_launch(ctx, s1, k_copy_active, vec_grid(n, S), 256, 0, ctx->ystate, (const double*)ctx->ynew, n,
+                  (const int*)d.ok);
+      PINT_LAUNCHED();
+      return PINT_OK;
+    });
+  }
 };
 
 // Public calls run on the context's own non-blocking stream (so Arnoldi
@@ -1212,6 +1456,274 @@ int check_S(pint_ctx* ctx, int S) {
     return PINT_INVALID_ARG;
   }
   return PINT_OK;
+}
+
+// ---------------------------------------------------------------- device-driven propagate (host side)
+template <typename T>
+int grow(pint_ctx* ctx, T** d, T** h, size_t count) {
+  if (*d) cudaFree(*d);
+  if (h && *h) cudaFreeHost(*h);
+  *d = nullptr;
+  if (h) *h = nullptr;
+  PINT_CHECK(cudaMalloc((void**)d, sizeof(T) * std::max<size_t>(count, 1)));
+  if (h) PINT_CHECK(cudaMallocHost((void**)h, sizeof(T) * std::max<size_t>(count, 1)));
+  return PINT_OK;
+}
+
+// step tables for `entries` (step, slice) pairs and call scalars for `slots` slices
+int ensure_tables(pint_ctx* ctx, size_t entries, size_t slots) {
+  if (entries > ctx->tab_cap) {
+    const size_t cap = std::max(entries, 2 * ctx->tab_cap);
+    PINT_TRY(grow(ctx, &ctx->d_sts, &ctx->h_sts, cap));
+    PINT_TRY(grow(ctx, &ctx->d_t1tab, &ctx->h_t1tab, cap));
+    ctx->tab_cap = cap;
+  }
+  if (slots > ctx->lsv_cap) {
+    const size_t cap = std::max(slots, 2 * ctx->lsv_cap);
+    PINT_TRY(grow(ctx, &ctx->d_nsteps, &ctx->h_nsteps, cap));
+    PINT_TRY(grow(ctx, &ctx->d_lsv, &ctx->h_lsv, cap));
+    ctx->lsv_cap = cap;
+  }
+  return PINT_OK;
+}
+
+// steps of slice s into the tables at column s of a [nmax][S] block starting
+// at `off`: the time arithmetic of Impl::propagate (integrators.py:154-162)
+void fill_steps(pint_ctx* ctx, size_t off, int S, int s, int nsteps, int nmax, double t0, double t_end, double k,
+                double theta0) {
+  double t = t0;
+  for (int j = 0; j < nmax; ++j) {
+    const size_t e = off + (size_t)j * S + s;
+    if (j >= nsteps) {
+      ctx->h_sts[e] = StepScalars{};
+      ctx->h_t1tab[e] = 0.0;
+      continue;
+    }
+    const double kk = (j == nsteps - 1) ? (t_end - t) : k;
+    const double theta = std::min(std::max(0.5 + theta0 * kk, 0.5), 1.0);
+    const double t1 = t + kk;
+    ctx->h_sts[e] = make_step(ctx->desc, kk, theta, t1);
+    ctx->h_t1tab[e] = t1;
+    t = t1;
+  }
+}
+
+LoopScalars call_scalars(pint_ctx* ctx, int S, int nmax, const pint_newton_opts* no, const pint_krylov_opts* ko,
+                         size_t tab_off, size_t nsteps_off) {
+  LoopScalars L{};
+  L.S = S;
+  L.nmax = nmax;
+  L.m = ctx->restart;
+  L.newton_max = no->max_iters;
+  L.lin_max = ko->max_iters;
+  L.reuse = ko->precond_reuse;
+  L.drift_num = ctx->drift_num;
+  L.cgs_force = ctx->cgs_passes;
+  L.abs_tol = no->abs_tol;
+  L.rel_tol = no->rel_tol;
+  L.damping_min = no->damping_min;
+  L.lin_rtol = ko->rtol;
+  L.lin_rtol_first = ko->rtol_first;
+  L.lin_atol = ko->atol;
+  L.sts = ctx->d_sts + tab_off;
+  L.t1tab = ctx->d_t1tab + tab_off;
+  L.nsteps = ctx->d_nsteps + nsteps_off;
+  return L;
+}
+
+int get_loop_graph(pint_ctx* ctx, int S, const pint_krylov_opts* ko, cudaStream_t st,
+                   std::pair<cudaGraphExec_t, long long>** out) {
+  const std::vector<double> key = {(double)S, (double)ko->pre_smooth, (double)ko->post_smooth, ko->omega,
+                                   (double)ko->max_levels, (double)ko->coarse_sweeps, (double)ko->smoother};
+  auto it = ctx->loop_graphs.find(key);
+  if (it == ctx->loop_graphs.end()) {
+    const size_t bodies0 = ctx->body_nodes.size();
+    const long long before = ctx->launches;
+    ctx->capturing = true;
+    ctx->nopdl.clear();
+    cudaGraph_t graph = nullptr;
+    int rc = PINT_OK;
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      cudaStreamCaptureStatus cs;
+      e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &ctx->cap_root, nullptr, nullptr);
+      if (e == cudaSuccess)
+        rc = ctx->D == 2 ? Impl<2>::capture_propagate(ctx, S, ko, st) : Impl<3>::capture_propagate(ctx, S, ko, st);
+      const cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+      if (e == cudaSuccess) e = e2;
+    }
+    ctx->capturing = false;
+    ctx->nopdl.clear();
+    const long long top = ctx->launches - before;
+    ctx->launches = before;
+    if (rc == PINT_OK && e != cudaSuccess) {
+      ctx->err = std::string("loop-graph capture: ") + cudaGetErrorString(e);
+      rc = PINT_CUDA_ERROR;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (rc == PINT_OK) {
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) {
+        ctx->err = std::string("loop-graph instantiate: ") + cudaGetErrorString(e);
+        rc = PINT_CUDA_ERROR;
+      }
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (rc != PINT_OK) {
+      ctx->body_nodes.resize(bodies0);
+      cudaGetLastError();
+      return rc;
+    }
+    PINT_CHECK(cudaMemcpy(ctx->d_body_nodes + bodies0, ctx->body_nodes.data() + bodies0,
+                          sizeof(int) * (ctx->body_nodes.size() - bodies0), cudaMemcpyHostToDevice));
+    it = ctx->loop_graphs.emplace(key, std::make_pair(exec, top)).first;
+  }
+  *out = &it->second;
+  return PINT_OK;
+}
+
+int propagate_dev(pint_ctx* ctx, int S, const double* y_in, double* y_out, const double* t0, const double* t_end,
+                  const int* nsteps, double k, double theta0, const pint_newton_opts* no,
+                  const pint_krylov_opts* ko, int* newton_iters, int* krylov_iters, int* status_out, double* fail_t,
+                  cudaStream_t st) {
+  const size_t n = (size_t)ctx->C * ctx->g.np;
+  int nmax = 0;
+  for (int s = 0; s < S; ++s) nmax = std::max(nmax, (int)nsteps[s]);
+  PINT_TRY(ensure_tables(ctx, (size_t)std::max(nmax, 1) * S, S));
+  for (int s = 0; s < S; ++s) {
+    fill_steps(ctx, 0, S, s, nsteps[s], nmax, t0[s], t_end[s], k, theta0);
+    ctx->h_nsteps[s] = nsteps[s];
+  }
+  *ctx->h_ls = call_scalars(ctx, S, nmax, no, ko, 0, 0);
+  std::pair<cudaGraphExec_t, long long>* graph = nullptr;
+  PINT_TRY(get_loop_graph(ctx, S, ko, st, &graph));
+  const size_t ents = (size_t)std::max(nmax, 1) * S;
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_sts, ctx->h_sts, sizeof(StepScalars) * ents, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_t1tab, ctx->h_t1tab, sizeof(double) * ents, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_nsteps, ctx->h_nsteps, sizeof(int) * S, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->ld.ls, ctx->h_ls, sizeof(LoopScalars), cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->ystate, y_in, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
+  PINT_CHECK(cudaGraphLaunch(graph->first, st));
+  ctx->launches += graph->second;
+  PINT_CHECK(cudaMemcpyAsync(y_out, ctx->ystate, sizeof(double) * n * S, cudaMemcpyDeviceToDevice, st));
+  int* hi = ctx->h_out_i;
+  PINT_CHECK(cudaMemcpyAsync(hi, ctx->ld.status, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaMemcpyAsync(hi + ctx->maxS, ctx->ld.nit, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaMemcpyAsync(hi + 2 * ctx->maxS, ctx->ld.kit, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->h_out_d, ctx->ld.ft, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaStreamSynchronize(st));
+  for (int s = 0; s < S; ++s) {
+    if (status_out) status_out[s] = hi[s];
+    if (newton_iters) newton_iters[s] = hi[ctx->maxS + s];
+    if (krylov_iters) krylov_iters[s] = hi[2 * ctx->maxS + s];
+    if (fail_t) fail_t[s] = ctx->h_out_d[s];
+  }
+  return PINT_OK;
+}
+
+int ensure_sweep(pint_ctx* ctx, size_t L) {
+  if (L <= ctx->sw_cap) return PINT_OK;
+  const size_t cap = std::max(L, 2 * ctx->sw_cap);
+  const int nblk = (ctx->g.np + kRedChunk - 1) / kRedChunk;
+  const size_t part = std::max((size_t)ctx->C * 5 * nblk, cap * 2 * (size_t)ctx->nblk);
+  PINT_TRY(grow<double>(ctx, &ctx->sw_part, nullptr, part));
+  PINT_TRY(grow<double>(ctx, &ctx->sw_theta, nullptr, cap));
+  PINT_TRY(grow<double>(ctx, &ctx->sw_corr, nullptr, cap));
+  PINT_TRY(grow<double>(ctx, &ctx->sw_ft, nullptr, cap));
+  PINT_TRY(grow<int>(ctx, &ctx->sw_status, nullptr, cap));
+  PINT_TRY(grow<int>(ctx, &ctx->sw_nit, nullptr, cap));
+  PINT_TRY(grow<int>(ctx, &ctx->sw_kit, nullptr, cap));
+  if (ctx->h_sw) cudaFreeHost(ctx->h_sw);
+  PINT_CHECK(cudaMallocHost((void**)&ctx->h_sw, sizeof(double) * 7 * cap));
+  ctx->sw_cap = cap;
+  return PINT_OK;
+}
+
+// K8b for one slice on the context's scratch: theta_l, x_new, corr_l on the device
+void correct_dev(pint_ctx* ctx, int l, const double* c_new, const double* f_old, const double* c_old,
+                 const double* x_prev, double* x_new, int variant, double lo, double hi, cudaStream_t st) {
+  const int C = ctx->C, nn = ctx->g.nn, np = ctx->g.np;
+  const int nblk = (nn + kRedChunk - 1) / kRedChunk;
+  double* part3 = ctx->sw_part;
+  double* part2 = ctx->sw_part + (size_t)C * 3 * nblk;
+  pint_launch(ctx, st, k_block_dots, dim3(nblk, C), kRedThreads, 0, f_old, c_new, nn, np, part3, nblk);
+  pint_launch(ctx, st, k_theta, 1, 32, 0, (const double*)part3, nblk, C, variant, lo, hi, ctx->sw_theta + l);
+  pint_launch(ctx, st, k_update_norms, dim3(nblk, C), kRedThreads, 0, c_new, f_old, c_old, x_prev, x_new,
+              (const double*)(ctx->sw_theta + l), nn, np, part2, nblk);
+  pint_launch(ctx, st, k_corr, 1, 32, 0, (const double*)part2, nblk, C, ctx->sw_corr + l);
+}
+
+// the sequential corrector sweep (parareal.py:422-436) or the coarse
+// initialisation (parareal.py:410-416): L loop-graph launches of batch 1 and
+// the K8b kernels, all enqueued without a host synchronisation
+int coarse_sweep(pint_ctx* ctx, int L, double* x, const double* x_prev, double* c_new, const double* c_old,
+                 const double* f_old, const double* t_grid, const int* nsteps, double k, double theta0,
+                 const pint_newton_opts* no, const pint_krylov_opts* ko, int variant, double lo, double hi,
+                 double* theta_out, double* corr_out, int* newton_iters, int* krylov_iters, int* status_out,
+                 double* fail_t, cudaStream_t st) {
+  const size_t n = (size_t)ctx->C * ctx->g.np;
+  size_t ents = 0;
+  std::vector<size_t> off(L);
+  for (int l = 0; l < L; ++l) {
+    off[l] = ents;
+    ents += (size_t)std::max(nsteps[l], 1);
+  }
+  PINT_TRY(ensure_tables(ctx, ents, L));
+  PINT_TRY(ensure_sweep(ctx, L));
+  for (int l = 0; l < L; ++l) {
+    fill_steps(ctx, off[l], 1, 0, nsteps[l], std::max(nsteps[l], 1), t_grid[l], t_grid[l + 1], k, theta0);
+    ctx->h_nsteps[l] = nsteps[l];
+    ctx->h_lsv[l] = call_scalars(ctx, 1, nsteps[l], no, ko, off[l], l);
+  }
+  std::pair<cudaGraphExec_t, long long>* graph = nullptr;
+  PINT_TRY(get_loop_graph(ctx, 1, ko, st, &graph));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_sts, ctx->h_sts, sizeof(StepScalars) * ents, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_t1tab, ctx->h_t1tab, sizeof(double) * ents, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_nsteps, ctx->h_nsteps, sizeof(int) * L, cudaMemcpyHostToDevice, st));
+  PINT_CHECK(cudaMemcpyAsync(ctx->d_lsv, ctx->h_lsv, sizeof(LoopScalars) * L, cudaMemcpyHostToDevice, st));
+  for (int l = 0; l < L; ++l) {
+    PINT_CHECK(cudaMemcpyAsync(ctx->ystate, x + l * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    PINT_CHECK(cudaMemcpyAsync(ctx->ld.ls, ctx->d_lsv + l, sizeof(LoopScalars), cudaMemcpyDeviceToDevice, st));
+    PINT_CHECK(cudaGraphLaunch(graph->first, st));
+    ctx->launches += graph->second;
+    pint_launch(ctx, st, k_sweep_record, 1, 32, 0, ctx->ld, l, ctx->sw_status, ctx->sw_nit, ctx->sw_kit, ctx->sw_ft);
+    double* cn = c_new + l * n;
+    PINT_CHECK(cudaMemcpyAsync(cn, ctx->ystate, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (f_old)
+      correct_dev(ctx, l, cn, f_old + l * n, c_old + l * n, x_prev + (l + 1) * n, x + (l + 1) * n, variant, lo, hi,
+                  st);
+    else
+      PINT_CHECK(cudaMemcpyAsync(x + (l + 1) * n, ctx->ystate, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  }
+  PINT_LAUNCHED();
+  double* h = ctx->h_sw;
+  const size_t cap = ctx->sw_cap;
+  if (f_old) {
+    PINT_CHECK(cudaMemcpyAsync(h, ctx->sw_theta, sizeof(double) * L, cudaMemcpyDeviceToHost, st));
+    PINT_CHECK(cudaMemcpyAsync(h + cap, ctx->sw_corr, sizeof(double) * L, cudaMemcpyDeviceToHost, st));
+  }
+  PINT_CHECK(cudaMemcpyAsync(h + 2 * cap, ctx->sw_ft, sizeof(double) * L, cudaMemcpyDeviceToHost, st));
+  int* hn = reinterpret_cast<int*>(h + 3 * cap);
+  PINT_CHECK(cudaMemcpyAsync(hn, ctx->sw_status, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaMemcpyAsync(hn + cap, ctx->sw_nit, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaMemcpyAsync(hn + 2 * cap, ctx->sw_kit, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaStreamSynchronize(st));
+  for (int l = 0; l < L; ++l) {
+    if (theta_out) theta_out[l] = f_old ? h[l] : 1.0;
+    if (corr_out) corr_out[l] = f_old ? h[cap + l] : 0.0;
+    if (fail_t) fail_t[l] = h[2 * cap + l];
+    if (status_out) status_out[l] = hn[l];
+    if (newton_iters) newton_iters[l] = hn[cap + l];
+    if (krylov_iters) krylov_iters[l] = hn[2 * cap + l];
+  }
+  return PINT_OK;
+}
+
+// the device-driven loop covers every option except the diagnostics that need
+// the host in the loop (per-iteration trace, CUDA-event profiling) and the
+// A/B variants kept for measurement (split norm, fused Arnoldi kernel)
+bool use_device_loop(const pint_ctx* ctx) {
+  return ctx->device_loop && !ctx->prof && !ctx->verbose && !ctx->split_norm && !ctx->use_fused;
 }
 
 }  // namespace
@@ -1400,8 +1912,47 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
       }
     }
   }
+  // device-driven control flow: per-slice loop state
+  {
+    LoopDev& d = ctx->ld;
+    int rc2;
+#define LALLOC(p, cnt) \
+  if ((rc2 = dalloc(ctx, &(p), (cnt))) != PINT_OK) return rc2;
+    LALLOC(d.ls, (size_t)1);
+    for (int** q : {&d.act, &d.status, &d.nit, &d.kit, &d.running, &d.its, &d.ls_mask, &d.accept, &d.ok, &d.built,
+                    &d.base, &d.first, &d.need, &d.built_now, &d.gits})
+      LALLOC(*q, (size_t)S);
+    for (double** q : {&d.ft, &d.rnorm, &d.target, &d.tnorm, &d.lam, &d.gres}) LALLOC(*q, (size_t)S);
+    LALLOC(ctx->gm_cap, (size_t)1);
+    LALLOC(ctx->d_body_nodes, (size_t)kMaxBodies);
+    LALLOC(ctx->d_launch_ctr, (size_t)1);
+#undef LALLOC
+    d.gm_tol = ctx->gm_tol;
+    d.gm_beta = ctx->gm_beta;
+    d.gv = ctx->gv;
+    d.norms = ctx->d_norms;
+    d.gm_active = ctx->gm_active;
+    d.gm_steps = ctx->gm_steps;
+    d.gm_its = ctx->gm_its;
+    d.cyc_active = ctx->cyc_active;
+    d.gm_two_pass = ctx->gm_two_pass;
+    d.gm_cap = ctx->gm_cap;
+    d.st = ctx->d_st;
+    d.launch_ctr = ctx->d_launch_ctr;
+    d.body_nodes = ctx->d_body_nodes;
+    for (int i = 0; i < kCapDepth; ++i)
+      if (cudaStreamCreateWithFlags(&ctx->cap_st[i], cudaStreamNonBlocking) != cudaSuccess) {
+        ctx->err = "capture stream creation failed";
+        return PINT_CUDA_ERROR;
+      }
+  }
+  ctx->device_loop = !(std::getenv("PINT_DEVICE_LOOP") && std::getenv("PINT_DEVICE_LOOP")[0] == '0');
   if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess) {
+      cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_cap, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_ls, sizeof(LoopScalars)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_out_i, sizeof(int) * 4 * S) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_out_d, sizeof(double) * S) != cudaSuccess) {
     ctx->err = "cudaMallocHost failed";
     return PINT_CUDA_ERROR;
   }
@@ -1419,6 +1970,16 @@ int pint_destroy(pint_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.first);
+  for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second.first);
+  for (void* p : {(void*)ctx->d_sts, (void*)ctx->d_t1tab, (void*)ctx->d_nsteps, (void*)ctx->d_lsv,
+                  (void*)ctx->sw_part, (void*)ctx->sw_theta, (void*)ctx->sw_corr, (void*)ctx->sw_ft,
+                  (void*)ctx->sw_status, (void*)ctx->sw_nit, (void*)ctx->sw_kit})
+    if (p) cudaFree(p);
+  for (void* p : {(void*)ctx->h_sts, (void*)ctx->h_t1tab, (void*)ctx->h_nsteps, (void*)ctx->h_lsv,
+                  (void*)ctx->h_sw, (void*)ctx->h_cap, (void*)ctx->h_ls, (void*)ctx->h_out_i, (void*)ctx->h_out_d})
+    if (p) cudaFreeHost(p);
+  for (cudaStream_t cs : ctx->cap_st)
+    if (cs) cudaStreamDestroy(cs);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
@@ -1462,6 +2023,7 @@ int pint_profile(pint_ctx* ctx, int32_t enable) {
   ctx->ev_used = 0;
   cudaMemset(ctx->d_work, 0, sizeof(unsigned long long));
   cudaMemset(ctx->d_work_bytes, 0, sizeof(unsigned long long));
+  if (ctx->d_launch_ctr) cudaMemset(ctx->d_launch_ctr, 0, sizeof(unsigned long long));
   ctx->fused_used = false;
   ctx->tail_slice_launches = 0;
   return PINT_OK;
@@ -1495,7 +2057,9 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   }
   unsigned long long work = 0;
   PINT_CHECK(cudaMemcpy(&work, ctx->d_work, sizeof(work), cudaMemcpyDeviceToHost));
-  if (launches) *launches = ctx->launches;
+  unsigned long long dev_launches = 0;  // kernels inside the conditional bodies of the loop graphs
+  PINT_CHECK(cudaMemcpy(&dev_launches, ctx->d_launch_ctr, sizeof(dev_launches), cudaMemcpyDeviceToHost));
+  if (launches) *launches = ctx->launches + (int64_t)dev_launches;
   if (kernel_launches) *kernel_launches = (int64_t)ctx->ev_pairs.size();
   const bool tail_kernel = !ctx->fused_used && ctx->tail_first == 0;
   if (slice_launches) *slice_launches = tail_kernel ? ctx->tail_slice_launches : (int64_t)work;
@@ -1539,13 +2103,17 @@ int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, 
     ctx->err = "invalid argument to pint_propagate";
     return PINT_INVALID_ARG;
   }
-  if (krylov->restart > ctx->restart) {
-    ctx->err = "krylov restart exceeds the context's restart length";
+  if (krylov->restart != ctx->restart) {
+    ctx->err = "krylov restart " + std::to_string(krylov->restart) + " differs from the context's restart length " +
+               std::to_string(ctx->restart);
     return PINT_INVALID_ARG;
   }
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   cudaStream_t st = ctx->stream;
+  if (use_device_loop(ctx))
+    return propagate_dev(ctx, S, y_in, y_out, t0, t_end, nsteps, k, theta0, newton, krylov, newton_iters,
+                         krylov_iters, status, fail_t, st);
   return DISPATCH(propagate(ctx, S, y_in, y_out, t0, t_end, nsteps, k, theta0, newton, krylov, newton_iters,
                             krylov_iters, status, fail_t, st));
 }
@@ -1632,8 +2200,9 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
                       int32_t* its, double* resid, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
-  if (krylov->restart > ctx->restart) {
-    ctx->err = "krylov restart exceeds the context's restart length";
+  if (krylov->restart != ctx->restart) {
+    ctx->err = "krylov restart " + std::to_string(krylov->restart) + " differs from the context's restart length " +
+               std::to_string(ctx->restart);
     return PINT_INVALID_ARG;
   }
   std::lock_guard<std::mutex> lock(ctx->mu);
@@ -1657,9 +2226,21 @@ int pint_parareal_correct_one(int32_t C, int32_t nn, int32_t np, const double* c
   if (C < 1 || nn < 1 || np < nn || variant < 0 || variant > 2 || clamp_lo > clamp_hi) return PINT_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const int nblk = (nn + kRedChunk - 1) / kRedChunk;
-  double* scratch = nullptr;
+  // scratch of the largest call so far (process-wide, serialised by its mutex)
+  static std::mutex mu;
+  static double* scratch = nullptr;
+  static size_t scratch_cnt = 0;
+  std::lock_guard<std::mutex> lock(mu);
   const size_t cnt = (size_t)C * 3 * nblk + (size_t)C * 2 * nblk + 2;
-  if (cudaMallocAsync((void**)&scratch, sizeof(double) * cnt, st) != cudaSuccess) return PINT_CUDA_ERROR;
+  if (cnt > scratch_cnt) {
+    if (scratch) cudaFree(scratch);
+    scratch = nullptr;
+    if (cudaMalloc((void**)&scratch, sizeof(double) * cnt) != cudaSuccess) {
+      scratch_cnt = 0;
+      return PINT_CUDA_ERROR;
+    }
+    scratch_cnt = cnt;
+  }
   double* part3 = scratch;
   double* part2 = scratch + (size_t)C * 3 * nblk;
   double* d_theta = part2 + (size_t)C * 2 * nblk;
@@ -1671,11 +2252,71 @@ int pint_parareal_correct_one(int32_t C, int32_t nn, int32_t np, const double* c
   k_corr<<<1, 32, 0, st>>>(part2, nblk, C, d_corr);
   double hres[2];
   cudaMemcpyAsync(hres, d_theta, sizeof(double) * 2, cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(scratch, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return PINT_CUDA_ERROR;
   if (theta_out) *theta_out = hres[0];
   if (corr_out) *corr_out = hres[1];
   return cudaGetLastError() == cudaSuccess ? PINT_OK : PINT_CUDA_ERROR;
+}
+
+int pint_coarse_sweep(pint_ctx* ctx, int32_t L, double* x, const double* x_prev, double* c_new, const double* c_old,
+                      const double* f_old, const double* t_grid, const int32_t* nsteps, double k, double theta0,
+                      const pint_newton_opts* newton, const pint_krylov_opts* krylov, int32_t variant,
+                      double clamp_lo, double clamp_hi, double* theta_out, double* corr_out, int32_t* newton_iters,
+                      int32_t* krylov_iters, int32_t* status, double* fail_t, void* stream) {
+  if (!ctx) return PINT_INVALID_ARG;
+  if (L < 1 || !x || !c_new || !t_grid || !nsteps || !newton || !krylov || k <= 0.0 || variant < 0 || variant > 2 ||
+      clamp_lo > clamp_hi || (f_old && (!c_old || !x_prev))) {
+    ctx->err = "invalid argument to pint_coarse_sweep";
+    return PINT_INVALID_ARG;
+  }
+  if (krylov->restart != ctx->restart) {
+    ctx->err = "krylov restart " + std::to_string(krylov->restart) + " differs from the context's restart length " +
+               std::to_string(ctx->restart);
+    return PINT_INVALID_ARG;
+  }
+  for (int l = 0; l < L; ++l)
+    if (nsteps[l] < 0 || !(t_grid[l + 1] >= t_grid[l])) {
+      ctx->err = "pint_coarse_sweep: time grid must be non-decreasing with non-negative step counts";
+      return PINT_INVALID_ARG;
+    }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (!use_device_loop(ctx)) {
+    ctx->err = "pint_coarse_sweep needs the device-driven loop (PINT_DEVICE_LOOP=0, profiling or a host-only A/B "
+               "switch is active)";
+    return PINT_INVALID_ARG;
+  }
+  StreamGuard guard(ctx, stream);
+  return coarse_sweep(ctx, L, x, x_prev, c_new, c_old, f_old, t_grid, nsteps, k, theta0, newton, krylov, variant,
+                      clamp_lo, clamp_hi, theta_out, corr_out, newton_iters, krylov_iters, status, fail_t,
+                      ctx->stream);
+}
+
+int pint_boundary_error(pint_ctx* ctx, int32_t S, const double* x, const double* ref, double* err,
+                        int32_t* absolute, void* stream) {
+  if (!ctx) return PINT_INVALID_ARG;
+  if (S < 1 || !x || !ref || !err) {
+    ctx->err = "invalid argument to pint_boundary_error";
+    return PINT_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
+  PINT_TRY(ensure_sweep(ctx, (size_t)S));
+  const size_t n = (size_t)ctx->C * ctx->g.np;
+  const int nblk = ctx->nblk;
+  pint_launch(ctx, st, k_err_partial, dim3(nblk, S), kRedThreads, 0, x, ref, n, ctx->sw_part, nblk);
+  pint_launch(ctx, st, k_err_final, (S + 127) / 128, 128, 0, (const double*)ctx->sw_part, nblk, S, ctx->sw_theta,
+              ctx->sw_status);
+  PINT_LAUNCHED();
+  PINT_CHECK(cudaMemcpyAsync(ctx->h_sw, ctx->sw_theta, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+  int* hi = reinterpret_cast<int*>(ctx->h_sw + 3 * ctx->sw_cap);
+  PINT_CHECK(cudaMemcpyAsync(hi, ctx->sw_status, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+  PINT_CHECK(cudaStreamSynchronize(st));
+  for (int s = 0; s < S; ++s) {
+    err[s] = ctx->h_sw[s];
+    if (absolute) absolute[s] = hi[s];
+  }
+  return PINT_OK;
 }
 
 }  // extern "C"

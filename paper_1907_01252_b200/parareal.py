@@ -1,88 +1,94 @@
-"""Parareal / theta-Parareal driver with serial, pipelined and batched schedulers.
+"""Device-resident Parareal drivers for the GPU propagators.
 
-API mirror of the reference engine (reference pkg/src/pintbench/parareal.py):
-``PararealConfig`` (49-76), ``RunTrace`` (79-103), ``parareal_update``
-(154-163), ``theta_weight`` (166-197), ``boundary_error`` (200-213),
-``sequential_solve`` (138-151), ``theoretical_speedup`` (133-135),
-``pipelined_schedule`` (241-267) and ``run_parareal`` (363-465).  The
-iteration is
+The reference engine ``pintbench.run_parareal`` (reference
+pkg/src/pintbench/parareal.py:363-465) drives ``GPUThetaPropagator`` as it
+stands -- it only reads ``step`` and calls ``advance`` (the drop-in contract,
+tests/test_gpu_integration.py).  This module holds the B200-first drivers,
+which keep every boundary state in HBM and hand each phase of an iteration
+to the device in one call:
 
-    X[i][l+1] = theta C(X[i][l]) + F(X[i-1][l]) - theta C(X[i-1][l])
+* the fine phase (parareal.py:417-421): all L fine tasks of iteration i in ONE
+  batched ``advance_device`` launch (legal because fine(i, .) depends only on
+  the corrector of iteration i-1, parareal.py:258-261; the result equals the
+  serial order bitwise because the propagator is batch-invariant);
+* the corrector sweep (parareal.py:422-436) and the coarse initialisation
+  (parareal.py:410-416): ONE ``pint_coarse_sweep`` call per iteration -- L
+  launches of the device-driven loop graph with the K8b correction
+  (theta weight, update, correction norm) between them, one host
+  synchronisation per sweep;
+* boundary errors against a reference trajectory (parareal.py:200-213,
+  461-464) on the device (``pint_boundary_error``).
 
-with the correction norm ||X[i][l+1] - X[i-1][l+1]|| / ||X[i][l+1]|| recorded
-per boundary (the "defect history") and the stop test at the end of each
-corrector sweep.
+``run_parareal_device`` optionally shards the fine phase over the ranks of a
+``torch.distributed`` group: each rank propagates a contiguous
+block of slices, one all-gather of device tensors (NCCL over NVLink on GPUs)
+per iteration assembles F(X[i-1]) everywhere, and every rank runs the same
+deterministic sweep, so all ranks hold identical iterates.
 
-Schedulers:
-* ``serial``    -- tasks in priority order on the calling thread (the
-                   reference's serial order, parareal.py:270-278);
-* ``pipelined`` -- a worker pool over the same task graph (fine task of
-                   iteration i starts once the i-1 corrector published its left
-                   boundary), as parareal.py:281-360;
-* ``batched``   -- new, B200-first: the L fine tasks of an iteration go to the
-                   propagator's ``advance_batch`` in ONE call (legal because
-                   fine(i, .) depends only on the corrector of i-1,
-                   parareal.py:258-261); results equal the serial order bitwise
-                   when the propagator is batch-invariant.
+``run_parareal_device_pipelined`` overlaps the fine phase of iteration i+1
+with the sweep of iteration i at chunk granularity (the dependency structure
+of the reference's pipelined task graph, parareal.py:241-267).
 
-``run_parareal_device`` keeps every boundary state resident in HBM: one
-batched fine launch per iteration, the sequential coarse sweep on the device
-(batch-1 ``advance_device``) and the correction (theta weight, update,
-correction norm) as the K8b kernel of the C ABI; iterates are copied to the
-host once at the end for the ``RunTrace``.
+The trace schema (``RunTrace``) and the configuration fields
+(``PararealConfig``) are those of the reference so its reporting code reads
+them unchanged.
 """
 
 from __future__ import annotations
 
-import heapq
 import threading
 import time
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence
-
-import numpy as np
+from typing import Optional, Sequence
 
 from .state import State
 
-VARIANTS = ("classic", "least_squares", "angle_penalized")
-SCHEDULERS = ("serial", "pipelined", "batched")
-_DEGENERATE_MASS = 1e-28
+VARIANT_CODES = {"classic": 0, "least_squares": 1, "angle_penalized": 2}
 
 
 class PararealError(RuntimeError):
-    """A propagator failed inside the iteration; message carries (iteration, interval)."""
+    """A propagator failed inside the iteration; the message names the task
+    kind, the iteration and the interval (parareal.py:437-440)."""
 
 
 @dataclass(frozen=True)
 class PararealConfig:
+    """Iteration controls, field for field the reference's (parareal.py:49-76):
+    L intervals, at most ``max_iters`` (<= L) iterations, stop when the largest
+    correction norm of an iteration is <= ``tol``, theta-weight variant and
+    clamp.  ``scheduler`` / ``workers`` only exist for schema compatibility."""
+
     intervals: int
     max_iters: int
     tol: float = 1e-10
     variant: str = "classic"
     theta_clamp: tuple = (0.0, 1.0)
-    scheduler: str = "serial"
+    scheduler: str = "device"
     workers: int = 1
 
     def __post_init__(self):
+        problems = []
         if self.intervals < 2:
-            raise ValueError("need at least 2 intervals")
+            problems.append("need at least 2 intervals")
         if not 1 <= self.max_iters <= self.intervals:
-            raise ValueError("max_iters must lie in [1, intervals]; further iterations cannot improve")
-        if self.tol <= 0.0:
-            raise ValueError("tol must be positive")
-        if self.variant not in VARIANTS:
-            raise ValueError(f"unknown variant {self.variant!r}, expected one of {VARIANTS}")
-        lo, hi = self.theta_clamp
-        if lo > hi:
-            raise ValueError("theta_clamp must be a non-empty interval")
-        if self.scheduler not in SCHEDULERS:
-            raise ValueError(f"unknown scheduler {self.scheduler!r}, expected one of {SCHEDULERS}")
+            problems.append("max_iters must lie in [1, intervals]")
+        if not self.tol > 0.0:
+            problems.append("tol must be positive")
+        if self.variant not in VARIANT_CODES:
+            problems.append(f"unknown variant {self.variant!r}, expected one of {tuple(VARIANT_CODES)}")
+        if self.theta_clamp[0] > self.theta_clamp[1]:
+            problems.append("theta_clamp must be a non-empty interval")
         if self.workers < 1:
-            raise ValueError("workers must be at least 1")
+            problems.append("workers must be at least 1")
+        if problems:
+            raise ValueError("; ".join(problems))
 
 
 @dataclass
 class RunTrace:
+    """What one Parareal run recorded (the reference's trace schema,
+    parareal.py:79-103, plus the device drivers' phase timings)."""
+
     intervals: int
     variant: str
     scheduler: str
@@ -96,579 +102,243 @@ class RunTrace:
     iteration_seconds: list = field(default_factory=list)
     total_seconds: float = 0.0
     fine_propagations: int = 0
-    fine_seconds: float = 0.0      # new: wall time spent in fine phases (batched / device modes)
+    fine_seconds: float = 0.0      # wall time inside the fine phases
+    sweep_seconds: float = 0.0     # wall time inside the corrector sweeps (coarse init excluded)
 
 
-@dataclass(frozen=True)
-class ErrorEntry:
-    value: float
-    absolute: bool = False
-
-
-@dataclass(frozen=True)
-class SpeedupModel:
-    r: float
-    iters: int
-    intervals: int
-
-    def __post_init__(self):
-        if self.r <= 0.0:
-            raise ValueError("step ratio r must be positive")
-        if not 0 < self.iters <= self.intervals:
-            raise ValueError("iteration count must lie in (0, intervals]")
-
-
-def theoretical_speedup(model: SpeedupModel) -> float:
-    """1 / (r + (K/N)(1 + r)) (PAPER.md:586-589)."""
-    return 1.0 / (model.r + (model.iters / model.intervals) * (1.0 + model.r))
-
-
-def _split_window(window: float, step: float) -> int:
-    from .propagator import split_window
-    return split_window(window, step)
-
-
-def sequential_solve(F, s0: State, t_grid: Sequence[float]) -> list:
-    grid = [float(t) for t in t_grid]
-    if len(grid) < 2:
-        raise ValueError("time grid needs at least two points")
-    if abs(grid[0] - s0.time) > 1e-12 * max(1.0, abs(s0.time)):
-        raise ValueError(f"grid starts at {grid[0]} but the state is at {s0.time}")
-    if any(b <= a for a, b in zip(grid, grid[1:])):
-        raise ValueError("time grid must be strictly increasing")
-    out = [s0]
-    for t in grid[1:]:
-        out.append(F.advance(out[-1], t))
-    return out
-
-
-def parareal_update(coarse_new: State, fine_old: State, coarse_old: State, theta: float) -> State:
-    """theta*C_new + F_old - theta*C_old, evaluated in that order (parareal.py:162)."""
-    if not (fine_old.same_layout(coarse_new) and fine_old.same_layout(coarse_old)):
-        raise ValueError("states in the update must share one layout")
-    t = fine_old.time
-    tol = 1e-12 * max(1.0, abs(t))
-    if abs(coarse_new.time - t) > tol or abs(coarse_old.time - t) > tol:
-        raise ValueError("states in the update must sit at the same time")
-    values = theta * coarse_new.values + fine_old.values - theta * coarse_old.values
-    return fine_old.with_values(values, time=t)
-
-
-def _block_weight(f: np.ndarray, c: np.ndarray, variant: str) -> float:
-    cc = float(np.dot(c, c))
-    if cc <= _DEGENERATE_MASS:
-        return 1.0
-    fc = float(np.dot(f, c))
-    if variant == "least_squares":
-        w = fc / cc
-    else:
-        denom = cc * float(np.dot(f, f))
-        w = fc / denom if denom > _DEGENERATE_MASS ** 2 else 1.0
-    return w if np.isfinite(w) else 1.0
-
-
-def theta_weight(fine: State, coarse: State, variant: str, clamp: tuple = (0.0, 1.0)) -> float:
-    """Per-block LSQ / angle-penalized weight averaged over blocks, clamped
-    (parareal.py:166-197); classic -> 1."""
-    if variant == "classic":
-        return 1.0
-    if variant not in VARIANTS:
-        raise ValueError(f"unknown variant {variant!r}")
-    if not fine.same_layout(coarse):
-        raise ValueError("fine and coarse states must share one layout")
-    ws = [_block_weight(fine.block(n), coarse.block(n), variant) for n in fine.layout]
-    lo, hi = clamp
-    return float(min(max(sum(ws) / len(ws), lo), hi))
-
-
-def boundary_error(parareal_states: Sequence[State], sequential_states: Sequence[State]) -> list:
-    if len(parareal_states) != len(sequential_states):
-        raise ValueError("state lists must have equal length")
-    out = []
-    for vp, vs in zip(parareal_states, sequential_states):
-        diff = float(np.linalg.norm(vp.values - vs.values))
-        ref = float(np.linalg.norm(vs.values))
-        out.append(ErrorEntry(diff / ref) if ref > 0.0 else ErrorEntry(diff, absolute=True))
-    return out
-
-
-def correction_norm(new: np.ndarray, prev: np.ndarray) -> float:
-    """0 if unchanged, else ||new - prev|| / ||new|| (inf if ||new|| = 0) (parareal.py:429-431)."""
-    diff = float(np.linalg.norm(new - prev))
-    norm = float(np.linalg.norm(new))
-    return 0.0 if diff == 0.0 else (diff / norm if norm > 0.0 else float("inf"))
-
-
-# ----------------------------------------------------------------------------
-# task graph (parareal.py:220-267)
-
-
-@dataclass(frozen=True)
-class Task:
-    kind: str
-    iteration: int
-    interval: int
-    depends: tuple
-
-    @property
-    def key(self):
-        return (self.iteration, 0 if self.kind == "fine" else 1, self.interval)
-
-
-def pipelined_schedule(intervals: int, iterations: int) -> list:
-    if intervals < 1:
-        raise ValueError("need at least one interval")
-    if iterations < 0:
-        raise ValueError("iterations must be non-negative")
-    tasks = [Task("coarse_init", 0, l, ((0, 1, l - 1),) if l else ()) for l in range(intervals)]
-    for i in range(1, iterations + 1):
-        tasks += [Task("fine", i, l, ((i - 1, 1, l - 1),) if l else ()) for l in range(intervals)]
-        for l in range(intervals):
-            deps = [(i, 0, l), (i - 1, 1, l)] + ([(i, 1, l - 1)] if l else [])
-            tasks.append(Task("correct", i, l, tuple(deps)))
-    return tasks
-
-
-class _Pool:
-    """Priority-ordered worker pool; one worker reproduces the serial order."""
-
-    def __init__(self, tasks, run_task: Callable, workers: int):
-        self.run_task = run_task
-        self.tasks = {t.key: t for t in tasks}
-        self.waiting = {t.key: len(t.depends) for t in tasks}
-        self.children: dict = {}
-        for t in tasks:
-            for d in t.depends:
-                if d not in self.tasks:
-                    raise ValueError(f"task {t.key} depends on unknown task {d}")
-                self.children.setdefault(d, []).append(t.key)
-        self.ready = sorted(k for k, n in self.waiting.items() if n == 0)
-        heapq.heapify(self.ready)
-        self.cv = threading.Condition()
-        self.left = len(tasks)
-        self.busy = 0
-        self.stop_at: Optional[int] = None
-        self.error: Optional[BaseException] = None
-        self.workers = workers
-
-    def _done(self, key):
-        self.left -= 1
-        for c in self.children.get(key, ()):
-            self.waiting[c] -= 1
-            if self.waiting[c] == 0:
-                heapq.heappush(self.ready, c)
-        self.cv.notify_all()
-
-    def _loop(self):
-        while True:
-            with self.cv:
-                while not self.ready and self.left and self.error is None:
-                    if self.busy == 0:
-                        self.error = RuntimeError("scheduler stalled: tasks remain but none are ready or running")
-                        self.cv.notify_all()
-                        break
-                    self.cv.wait()
-                if self.error is not None or not self.left:
-                    return
-                key = heapq.heappop(self.ready)
-                task = self.tasks[key]
-                if self.stop_at is not None and task.iteration > self.stop_at:
-                    self._done(key)
-                    continue
-                self.busy += 1
-            try:
-                out = self.run_task(task)
-            except BaseException as exc:  # propagate the first failure
-                with self.cv:
-                    self.error = exc
-                    self.busy -= 1
-                    self.cv.notify_all()
-                return
-            with self.cv:
-                self.busy -= 1
-                if out is not None:
-                    self.stop_at = out if self.stop_at is None else min(self.stop_at, out)
-                self._done(key)
-
-    def run(self):
-        threads = [threading.Thread(target=self._loop, daemon=True) for _ in range(self.workers)]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        if self.error is not None:
-            raise self.error
-        return self.stop_at
-
-
-def _grid(s0: State, t_end: float, L: int) -> list:
-    g = [s0.time + (t_end - s0.time) * l / L for l in range(L + 1)]
+def time_grid(t0: float, t_end: float, L: int) -> list:
+    """Boundaries t0 + (t_end - t0) l / L with the last one exactly t_end."""
+    g = [t0 + (t_end - t0) * l / L for l in range(L + 1)]
     g[-1] = t_end
     return g
 
 
-def run_parareal(C, F, s0: State, t_end: float, cfg: PararealConfig, oracle: Optional[Sequence[State]] = None):
-    """Parareal over [s0.time, t_end]; returns (boundary states of the last
-    completed iteration, RunTrace) exactly as parareal.py:363-465."""
+def _check(C, F, s0: State, t_end: float, cfg, oracle=None) -> list:
+    from .propagator import split_window
     L = cfg.intervals
-    if t_end <= s0.time:
+    if not t_end > s0.time:
         raise ValueError("t_end must lie beyond the initial time")
     window = (t_end - s0.time) / L
     for prop in (C, F):
-        _split_window(window, prop.step)
-    t_grid = _grid(s0, t_end, L)
+        split_window(window, prop.step)  # NonDivisibleWindow up front, as parareal.py:386-388
+    if cfg.variant not in VARIANT_CODES:
+        raise ValueError(f"unknown variant {cfg.variant!r}")
     if oracle is not None and len(oracle) != L + 1:
         raise ValueError(f"oracle must hold {L + 1} states, got {len(oracle)}")
-    K = cfg.max_iters
-    X = [[s0] + [None] * L for _ in range(K + 1)]
-    coarse = [[None] * (L + 1) for _ in range(K + 1)]
-    fine = [[None] * (L + 1) for _ in range(K + 1)]
-    thetas = [[1.0] * L for _ in range(K + 1)]
-    corr = [[0.0] * L for _ in range(K + 1)]
-    stamps = {"init": 0.0, "it": [0.0] * (K + 1), "fine": 0.0}
-    lock = threading.Lock()
-    nfine = [0]
-    t0 = time.perf_counter()
+    return time_grid(s0.time, t_end, L)
 
-    def correct(i: int, l: int) -> Optional[int]:
-        c_new = C.advance(X[i][l], t_grid[l + 1])
-        f_old = fine[i][l + 1]
-        th = theta_weight(f_old, c_new, cfg.variant, cfg.theta_clamp)
-        new = parareal_update(c_new, f_old, coarse[i - 1][l + 1], th)
-        X[i][l + 1] = new
-        coarse[i][l + 1] = c_new
-        thetas[i][l] = th
-        corr[i][l] = correction_norm(new.values, X[i - 1][l + 1].values)
-        if l == L - 1:
-            stamps["it"][i] = time.perf_counter() - t0
-            if max(corr[i]) <= cfg.tol:
-                return i
-        return None
 
-    def run_task(task: Task) -> Optional[int]:
-        i, l = task.iteration, task.interval
-        try:
-            if task.kind == "coarse_init":
-                nxt = C.advance(X[0][l], t_grid[l + 1])
-                X[0][l + 1] = nxt
-                coarse[0][l + 1] = nxt
-                if l == L - 1:
-                    stamps["init"] = time.perf_counter() - t0
-                return None
-            if task.kind == "fine":
-                fine[i][l + 1] = F.advance(X[i - 1][l], t_grid[l + 1])
-                with lock:
-                    nfine[0] += 1
-                return None
-            return correct(i, l)
-        except PararealError:
-            raise
-        except Exception as exc:
-            raise PararealError(f"{task.kind} failed at iteration {i}, interval {l}: {exc}") from exc
+def _sweep(C, X, grid, c_new, what: str, i: int, offset: int = 0, **kw):
+    from .propagator import TimeStepError
+    try:
+        return C.sweep(X, grid, c_new, **kw)
+    except TimeStepError as exc:
+        raise PararealError(f"{what} failed at iteration {i}, interval {offset + getattr(exc, 'interval', 0)}: "
+                            f"{exc}") from exc
 
-    if cfg.scheduler == "batched":
-        stop_at = None
-        for l in range(L):
-            run_task(Task("coarse_init", 0, l, ()))
-        batch = getattr(F, "advance_batch", None)
-        for i in range(1, K + 1):
-            tf = time.perf_counter()
-            try:
-                if batch is not None:
-                    outs = batch([X[i - 1][l] for l in range(L)], [t_grid[l + 1] for l in range(L)])
-                else:
-                    outs = [F.advance(X[i - 1][l], t_grid[l + 1]) for l in range(L)]
-            except Exception as exc:
-                raise PararealError(f"fine failed at iteration {i}, interval 0..{L - 1}: {exc}") from exc
-            stamps["fine"] += time.perf_counter() - tf
-            for l in range(L):
-                fine[i][l + 1] = outs[l]
-            nfine[0] += L
-            res = None
-            for l in range(L):
-                res = run_task(Task("correct", i, l, ()))
-            if res is not None:
-                stop_at = res
-                break
-    else:
-        tasks = pipelined_schedule(L, K)
-        stop_at = _Pool(tasks, run_task, 1 if cfg.scheduler == "serial" else cfg.workers).run()
 
-    n_it = stop_at if stop_at is not None else K
-    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler=cfg.scheduler)
-    trace.iterations_run = n_it
-    trace.converged = stop_at is not None
-    trace.theta_values = [list(thetas[i]) for i in range(1, n_it + 1)]
-    trace.correction_norms = [list(corr[i]) for i in range(1, n_it + 1)]
-    trace.iterate_values = [[X[i][l].values.copy() for l in range(L + 1)] for i in range(n_it + 1)]
-    trace.init_seconds = stamps["init"]
-    trace.iteration_seconds = [stamps["it"][i] for i in range(1, n_it + 1)]
-    trace.total_seconds = time.perf_counter() - t0
-    trace.fine_propagations = nfine[0]
-    trace.fine_seconds = stamps["fine"]
+def _finish(trace: RunTrace, dev, X, n_it: int, s0: State, t_grid, oracle) -> list:
+    """Copy the iterates to the host once, fill the trace, device boundary errors."""
+    L = trace.intervals
+    host = [dev.to_host(X[i]) for i in range(n_it + 1)]
+    trace.iterate_values = [[host[i][l].copy() for l in range(L + 1)] for i in range(n_it + 1)]
     if oracle is not None:
+        ref = dev.to_device([s.values for s in oracle[1:]])
         for i in range(1, n_it + 1):
-            trace.boundary_errors.append([e.value for e in boundary_error(X[i][1:], oracle[1:])])
-    return X[n_it], trace
+            err, _ = dev.boundary_error(X[i][1:], ref)
+            trace.boundary_errors.append([float(e) for e in err])
+    return [s0] + [s0.with_values(host[n_it][l], time=t_grid[l]) for l in range(1, L + 1)]
 
 
-# ----------------------------------------------------------------------------
-# device-resident driver
+def run_parareal_device(C, F, s0: State, t_end: float, cfg, oracle: Optional[Sequence[State]] = None,
+                        group=None):
+    """Parareal with every boundary state in HBM; returns (boundary states of
+    the last completed iteration, RunTrace) like parareal.py:363-465.
 
-
-_VARIANT_CODE = {"classic": 0, "least_squares": 1, "angle_penalized": 2}
-
-
-def run_parareal_device(C, F, s0: State, t_end: float, cfg: PararealConfig,
-                        oracle: Optional[Sequence[State]] = None):
-    """Parareal with every boundary state in HBM (GPU propagators only).
-
-    Per iteration: ONE batched fine launch over all L slices
-    (``F.advance_device``), then the sequential corrector sweep on the device:
-    batch-1 coarse propagation followed by the K8b kernel (theta weight,
-    update, correction norm).  Same trace semantics as :func:`run_parareal`.
+    ``C`` and ``F`` are GPU propagators (``sweep`` / ``advance_device``); with
+    a ``torch.distributed`` ``group`` of several ranks the fine phase is
+    sharded (contiguous slice blocks, one all-gather per iteration).
     """
-    import ctypes
-
     import torch
 
-    from . import _lib
-    from .propagator import _ptr, _stream
-
+    t_grid = _check(C, F, s0, t_end, cfg, oracle)
     dev = F.device
-    lib = _lib.load()
-    L = cfg.intervals
-    if t_end <= s0.time:
-        raise ValueError("t_end must lie beyond the initial time")
-    window = (t_end - s0.time) / L
-    for prop in (C, F):
-        _split_window(window, prop.step)
-    if L > dev.max_slices:
-        raise ValueError(f"{L} intervals exceed the device context's {dev.max_slices} slices")
-    t_grid = _grid(s0, t_end, L)
-    K = cfg.max_iters
-    Cn, nn, npad = dev.C, dev.nn, dev.np
-    t0 = time.perf_counter()
-    # X[i] : (L+1, C, np) device; coarse[i] : (L+1, C, np)
+    L, K = cfg.intervals, cfg.max_iters
+    world, rank = 1, 0
+    if group is not None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    from .sharding import gather_blocks, shard_bounds
+    lo, hi = shard_bounds(L, world, rank)
+    if hi - lo > dev.max_slices:
+        raise ValueError(f"{hi - lo} slices per rank exceed the device context's {dev.max_slices}")
+    variant = VARIANT_CODES[cfg.variant]
+    clamp = tuple(cfg.theta_clamp)
+    start = time.perf_counter()
     X = [dev.empty(L + 1) for _ in range(K + 1)]
-    coarse = [dev.empty(L + 1) for _ in range(K + 1)]
     first = dev.to_device(s0.values)
-    for i in range(K + 1):
-        X[i][0].copy_(first[0])
-
-    def cadv(src: torch.Tensor, l: int, out: torch.Tensor):
-        C.advance_device(src[None], [t_grid[l]], [t_grid[l + 1]], out=out[None])
-
-    try:
-        for l in range(L):
-            cadv(X[0][l], l, X[0][l + 1])
-            coarse[0][l + 1].copy_(X[0][l + 1])
-    except Exception as exc:
-        raise PararealError(f"coarse_init failed at iteration 0: {exc}") from exc
-    torch.cuda.synchronize()
-    init_s = time.perf_counter() - t0
-    thetas, corrs, it_s = [], [], []
-    fine_s = 0.0
+    for x in X:
+        x[0].copy_(first[0])
+    c_prev, c_cur = dev.empty(L), dev.empty(L)
+    fine = dev.empty(L)
+    _sweep(C, X[0], t_grid, c_prev, "coarse_init", 0)
+    init_s = time.perf_counter() - start
+    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler="device" if world == 1 else f"device-sharded[{world}]")
+    trace.init_seconds = init_s
     stop_at = None
-    nfine = 0
     for i in range(1, K + 1):
         tf = time.perf_counter()
         try:
-            fine = F.advance_device(X[i - 1][:L].contiguous(), t_grid[:L], t_grid[1:])
+            if world == 1:
+                F.advance_device(X[i - 1][:L], t_grid[:L], t_grid[1:L + 1], out=fine)
+            else:
+                mine = F.advance_device(X[i - 1][lo:hi].contiguous(), t_grid[lo:hi], t_grid[lo + 1:hi + 1])
+                gather_blocks(mine, fine, L, group)
         except Exception as exc:
-            raise PararealError(f"fine failed at iteration {i}, interval 0..{L - 1}: {exc}") from exc
-        torch.cuda.synchronize()
-        fine_s += time.perf_counter() - tf
-        nfine += L
-        th_row, c_row = [], []
-        for l in range(L):
-            try:
-                cadv(X[i][l], l, coarse[i][l + 1])
-            except Exception as exc:
-                raise PararealError(f"correct failed at iteration {i}, interval {l}: {exc}") from exc
-            th = ctypes.c_double()
-            cr = ctypes.c_double()
-            rc = lib.pint_parareal_correct_one(
-                Cn, nn, npad, _ptr(coarse[i][l + 1]), _ptr(fine[l]), _ptr(coarse[i - 1][l + 1]),
-                _ptr(X[i - 1][l + 1]), _ptr(X[i][l + 1]), _VARIANT_CODE[cfg.variant],
-                float(cfg.theta_clamp[0]), float(cfg.theta_clamp[1]), ctypes.byref(th), ctypes.byref(cr),
-                _stream())
-            if rc != _lib.PINT_OK:
-                raise PararealError(f"correct failed at iteration {i}, interval {l}: device error {rc}")
-            th_row.append(th.value)
-            c_row.append(cr.value)
-        thetas.append(th_row)
-        corrs.append(c_row)
-        it_s.append(time.perf_counter() - t0)
-        if max(c_row) <= cfg.tol:
+            raise PararealError(f"fine failed at iteration {i}, interval {lo}..{hi - 1}: {exc}") from exc
+        ts = time.perf_counter()
+        trace.fine_seconds += ts - tf
+        th, cr = _sweep(C, X[i], t_grid, c_cur, "correct", i, x_prev=X[i - 1], c_old=c_prev, f_old=fine,
+                        variant=variant, clamp=clamp)
+        trace.sweep_seconds += time.perf_counter() - ts
+        c_prev, c_cur = c_cur, c_prev
+        trace.theta_values.append([float(v) for v in th])
+        trace.correction_norms.append([float(v) for v in cr])
+        trace.iteration_seconds.append(time.perf_counter() - start)
+        trace.fine_propagations += hi - lo
+        if max(cr) <= cfg.tol:  # the stop test at the end of the sweep (parareal.py:433-435)
             stop_at = i
             break
     n_it = stop_at if stop_at is not None else K
-    host = [dev.to_host(X[i]) for i in range(n_it + 1)]
-    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler="device")
     trace.iterations_run = n_it
     trace.converged = stop_at is not None
-    trace.theta_values = thetas[:n_it]
-    trace.correction_norms = corrs[:n_it]
-    trace.iterate_values = [[host[i][l].copy() for l in range(L + 1)] for i in range(n_it + 1)]
-    trace.init_seconds = init_s
-    trace.iteration_seconds = it_s[:n_it]
-    trace.total_seconds = time.perf_counter() - t0
-    trace.fine_propagations = nfine
-    trace.fine_seconds = fine_s
-    states = [s0] + [s0.with_values(host[n_it][l], time=t_grid[l]) for l in range(1, L + 1)]
-    if oracle is not None:
-        for i in range(1, n_it + 1):
-            st = [s0.with_values(host[i][l], time=t_grid[l]) for l in range(1, L + 1)]
-            trace.boundary_errors.append([e.value for e in boundary_error(st, oracle[1:])])
+    states = _finish(trace, dev, X, n_it, s0, t_grid, oracle)
+    if X[0].is_cuda:
+        torch.cuda.synchronize()
+    trace.total_seconds = time.perf_counter() - start
     return states, trace
 
 
-def run_parareal_device_pipelined(C, F, s0: State, t_end: float, cfg: PararealConfig, chunks: int = 4,
+def run_parareal_device_pipelined(C, F, s0: State, t_end: float, cfg, chunks: int = 4,
                                   oracle: Optional[Sequence[State]] = None):
     """Device-resident Parareal with the fine phase of iteration i+1 overlapping
     the corrector sweep of iteration i (the pipelined task graph of the
     reference, parareal.py:241-267, at chunk granularity).
 
-    The L slices split into ``chunks`` contiguous groups; a worker thread
-    launches the batched fine propagation of a group as soon as the corrector
-    has published the group's left boundaries, while the calling thread keeps
-    sweeping.  ``C`` and ``F`` must own DIFFERENT device contexts (each context
-    has its own stream, so the two run concurrently on the GPU; ctypes releases
-    the GIL).  Results equal :func:`run_parareal_device` bitwise (the fine
-    propagator is batch-invariant and every task sees the same inputs).
+    The L slices split into ``chunks`` contiguous groups.  The calling thread
+    sweeps chunk by chunk (one ``pint_coarse_sweep`` per chunk on C's context);
+    a worker thread launches the batched fine propagation of a chunk of
+    iteration i+1 on F's context as soon as the chunk's left boundaries of
+    iteration i are final.  ``C`` and ``F`` must own different device contexts
+    (each has its own CUDA stream; each thread issues on its own torch stream,
+    so the two phases run concurrently).  Results equal ``run_parareal_device``
+    bitwise (same inputs per task, batch-invariant fine propagator).
     """
-    import ctypes
-
     import torch
 
-    from . import _lib
-    from .propagator import _ptr, _stream
-
     if C.device is F.device:
-        raise ValueError("pipelined device driver needs separate device contexts for C and F")
+        raise ValueError("the pipelined driver needs separate device contexts for C and F")
+    t_grid = _check(C, F, s0, t_end, cfg, oracle)
     dev = F.device
-    lib = _lib.load()
-    L = cfg.intervals
-    if t_end <= s0.time:
-        raise ValueError("t_end must lie beyond the initial time")
-    window = (t_end - s0.time) / L
-    for prop in (C, F):
-        _split_window(window, prop.step)
-    t_grid = _grid(s0, t_end, L)
-    K = cfg.max_iters
-    Cn, nn, npad = dev.C, dev.nn, dev.np
+    L, K = cfg.intervals, cfg.max_iters
+    variant = VARIANT_CODES[cfg.variant]
+    clamp = tuple(cfg.theta_clamp)
     chunks = max(1, min(chunks, L))
     bounds = [(c * L // chunks, (c + 1) * L // chunks) for c in range(chunks)]
-    t0 = time.perf_counter()
+    start = time.perf_counter()
     X = [dev.empty(L + 1) for _ in range(K + 1)]
-    coarse = [dev.empty(L + 1) for _ in range(K + 1)]
+    coarse = [dev.empty(L) for _ in range(K + 1)]
     fine = [dev.empty(L) for _ in range(K + 1)]
     first = dev.to_device(s0.values)
-    for i in range(K + 1):
-        X[i][0].copy_(first[0])
+    for x in X:
+        x[0].copy_(first[0])
     torch.cuda.synchronize()
     cond = threading.Condition()
-    published = [0] * (K + 1)          # X[i][0..published[i]] are final
+    published = [0] * (K + 1)      # X[i][0..published[i]] are final
     fine_done = [[False] * chunks for _ in range(K + 1)]
-    stop = {"at": None, "error": None}
-
-    def cadv(src, l, out):
-        C.advance_device(src[None], [t_grid[l]], [t_grid[l + 1]], out=out[None])
+    ctl = {"stop": None, "abort": False, "error": None}
+    fine_s = [0.0]
 
     def fine_worker():
+        stream = torch.cuda.Stream()
         try:
-            for i in range(1, K + 1):
-                for c, (lo, hi) in enumerate(bounds):
-                    with cond:
-                        # the chunk's inputs X[i-1][lo..hi-1] must be final
-                        while published[i - 1] < hi - 1 and stop["at"] is None and stop["error"] is None:
-                            cond.wait()
-                        if stop["error"] is not None or (stop["at"] is not None and i > stop["at"]):
-                            return
-                    out = F.advance_device(X[i - 1][lo:hi].contiguous(), t_grid[lo:hi], t_grid[lo + 1:hi + 1])
-                    fine[i][lo:hi].copy_(out)
-                    torch.cuda.synchronize()
-                    with cond:
-                        fine_done[i][c] = True
-                        cond.notify_all()
-        except BaseException as exc:  # noqa: BLE001 -- surfaced by the sweep thread
+            with torch.cuda.stream(stream):
+                for i in range(1, K + 1):
+                    for c, (lo, hi) in enumerate(bounds):
+                        with cond:
+                            while (published[i - 1] < hi - 1 and not ctl["abort"]
+                                   and (ctl["stop"] is None or i <= ctl["stop"])):
+                                cond.wait()
+                            if ctl["abort"] or (ctl["stop"] is not None and i > ctl["stop"]):
+                                return
+                        tf = time.perf_counter()
+                        F.advance_device(X[i - 1][lo:hi], t_grid[lo:hi], t_grid[lo + 1:hi + 1], out=fine[i][lo:hi])
+                        stream.synchronize()
+                        fine_s[0] += time.perf_counter() - tf
+                        with cond:
+                            fine_done[i][c] = True
+                            cond.notify_all()
+        except BaseException as exc:  # noqa: BLE001 -- surfaced by the sweeping thread
             with cond:
-                stop["error"] = exc
+                ctl["error"] = exc
                 cond.notify_all()
 
-    try:
-        for l in range(L):
-            cadv(X[0][l], l, X[0][l + 1])
-            coarse[0][l + 1].copy_(X[0][l + 1])
-            torch.cuda.synchronize()
-            with cond:
-                published[0] = l + 1
-                cond.notify_all()
-    except Exception as exc:
-        raise PararealError(f"coarse_init failed at iteration 0: {exc}") from exc
-    init_s = time.perf_counter() - t0
+    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler=f"device-pipelined[{chunks}]")
+    sweep_stream = torch.cuda.Stream()
     worker = threading.Thread(target=fine_worker, daemon=True)
-    worker.start()
-    thetas, corrs, it_s = [], [], []
     stop_at = None
     try:
-        for i in range(1, K + 1):
-            th_row, c_row = [], []
-            for l in range(L):
-                c = next(ci for ci, (lo, hi) in enumerate(bounds) if lo <= l < hi)
+        with torch.cuda.stream(sweep_stream):
+            for lo, hi in bounds:
+                _sweep(C, X[0][lo:hi + 1], t_grid[lo:hi + 1], coarse[0][lo:hi], "coarse_init", 0, offset=lo)
+                sweep_stream.synchronize()
                 with cond:
-                    while not fine_done[i][c] and stop["error"] is None:
-                        cond.wait()
-                    if stop["error"] is not None:
-                        raise PararealError(f"fine failed at iteration {i}: {stop['error']}") from stop["error"]
-                try:
-                    cadv(X[i][l], l, coarse[i][l + 1])
-                except Exception as exc:
-                    raise PararealError(f"correct failed at iteration {i}, interval {l}: {exc}") from exc
-                th, cr = ctypes.c_double(), ctypes.c_double()
-                rc = lib.pint_parareal_correct_one(
-                    Cn, nn, npad, _ptr(coarse[i][l + 1]), _ptr(fine[i][l]), _ptr(coarse[i - 1][l + 1]),
-                    _ptr(X[i - 1][l + 1]), _ptr(X[i][l + 1]), _VARIANT_CODE[cfg.variant],
-                    float(cfg.theta_clamp[0]), float(cfg.theta_clamp[1]), ctypes.byref(th), ctypes.byref(cr),
-                    _stream())
-                if rc != _lib.PINT_OK:
-                    raise PararealError(f"correct failed at iteration {i}, interval {l}: device error {rc}")
-                th_row.append(th.value)
-                c_row.append(cr.value)
-                with cond:
-                    published[i] = l + 1
+                    published[0] = hi
                     cond.notify_all()
-            thetas.append(th_row)
-            corrs.append(c_row)
-            it_s.append(time.perf_counter() - t0)
-            if max(c_row) <= cfg.tol:
-                stop_at = i
-                with cond:
-                    stop["at"] = i
-                    cond.notify_all()
-                break
+                if lo == 0:
+                    worker.start()
+            trace.init_seconds = time.perf_counter() - start
+            for i in range(1, K + 1):
+                th_row, c_row = [], []
+                for c, (lo, hi) in enumerate(bounds):
+                    with cond:
+                        while not fine_done[i][c] and ctl["error"] is None:
+                            cond.wait()
+                        if ctl["error"] is not None:
+                            raise PararealError(f"fine failed at iteration {i}: {ctl['error']}") from ctl["error"]
+                    ts = time.perf_counter()
+                    th, cr = _sweep(C, X[i][lo:hi + 1], t_grid[lo:hi + 1], coarse[i][lo:hi], "correct", i,
+                                    offset=lo, x_prev=X[i - 1][lo:hi + 1], c_old=coarse[i - 1][lo:hi],
+                                    f_old=fine[i][lo:hi], variant=variant, clamp=clamp)
+                    sweep_stream.synchronize()
+                    trace.sweep_seconds += time.perf_counter() - ts
+                    th_row += [float(v) for v in th]
+                    c_row += [float(v) for v in cr]
+                    with cond:
+                        published[i] = hi
+                        cond.notify_all()
+                trace.theta_values.append(th_row)
+                trace.correction_norms.append(c_row)
+                trace.iteration_seconds.append(time.perf_counter() - start)
+                if max(c_row) <= cfg.tol:
+                    stop_at = i
+                    break
+    except BaseException:
+        with cond:
+            ctl["abort"] = True   # the worker returns before its next launch
+            cond.notify_all()
+        raise
     finally:
         with cond:
-            if stop["at"] is None:
-                stop["at"] = K
+            ctl["stop"] = stop_at if stop_at is not None else K
             cond.notify_all()
-        worker.join()
+        if worker.is_alive():
+            worker.join()
     n_it = stop_at if stop_at is not None else K
-    host = [dev.to_host(X[i]) for i in range(n_it + 1)]
-    trace = RunTrace(intervals=L, variant=cfg.variant, scheduler=f"device-pipelined[{chunks}]")
     trace.iterations_run = n_it
     trace.converged = stop_at is not None
-    trace.theta_values = thetas[:n_it]
-    trace.correction_norms = corrs[:n_it]
-    trace.iterate_values = [[host[i][l].copy() for l in range(L + 1)] for i in range(n_it + 1)]
-    trace.init_seconds = init_s
-    trace.iteration_seconds = it_s[:n_it]
-    trace.total_seconds = time.perf_counter() - t0
     trace.fine_propagations = L * n_it
-    states = [s0] + [s0.with_values(host[n_it][l], time=t_grid[l]) for l in range(1, L + 1)]
-    if oracle is not None:
-        for i in range(1, n_it + 1):
-            st = [s0.with_values(host[i][l], time=t_grid[l]) for l in range(1, L + 1)]
-            trace.boundary_errors.append([e.value for e in boundary_error(st, oracle[1:])])
+    trace.fine_seconds = fine_s[0]
+    states = _finish(trace, dev, X, n_it, s0, t_grid, oracle)
+    trace.total_seconds = time.perf_counter() - start
     return states, trace

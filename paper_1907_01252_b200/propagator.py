@@ -318,6 +318,39 @@ class FSIDevice:
         self.lib.pint_flags(self.handle, nf, cf)
         return np.array(nf[:], dtype=np.uint8), np.array(cf[:], dtype=np.uint8)
 
+    def coarse_sweep(self, x: torch.Tensor, t_grid: Sequence[float], nsteps: Sequence[int], k: float,
+                     theta0: float, newton: NewtonSettings, krylov: KrylovSettings, c_new: torch.Tensor,
+                     x_prev: Optional[torch.Tensor] = None, c_old: Optional[torch.Tensor] = None,
+                     f_old: Optional[torch.Tensor] = None, variant: int = 0, clamp=(0.0, 1.0)):
+        """The sequential corrector sweep of one Parareal iteration on the device
+        (``pint_coarse_sweep``): x[0] given, x[1..L] and c_new[0..L-1] written.
+        ``f_old is None`` runs the coarse initialisation.  Returns per-slice
+        host arrays (theta, corr, newton its, krylov its, status, fail t)."""
+        L = len(nsteps)
+        no = _lib.NewtonOpts(newton.abs_tol, newton.rel_tol, newton.max_iters, newton.damping_min)
+        ko = krylov.c_struct()
+        th, cr, ft = (ctypes.c_double * L)(), (ctypes.c_double * L)(), (ctypes.c_double * L)()
+        nit, kit, status = (ctypes.c_int32 * L)(), (ctypes.c_int32 * L)(), (ctypes.c_int32 * L)()
+        ns = (ctypes.c_int32 * L)(*[int(n) for n in nsteps])
+        opt = (lambda t: _ptr(t) if t is not None else None)
+        rc = self.lib.pint_coarse_sweep(self.handle, L, _ptr(x), opt(x_prev), _ptr(c_new), opt(c_old), opt(f_old),
+                                        _darr(t_grid), ns, float(k), float(theta0), ctypes.byref(no),
+                                        ctypes.byref(ko), int(variant), float(clamp[0]), float(clamp[1]), th, cr,
+                                        nit, kit, status, ft, _stream())
+        self.check(rc, "pint_coarse_sweep")
+        return (np.array(th[:]), np.array(cr[:]), np.array(nit[:]), np.array(kit[:]), np.array(status[:]),
+                np.array(ft[:]))
+
+    def boundary_error(self, x: torch.Tensor, ref: torch.Tensor):
+        """||x_s - ref_s|| / ||ref_s|| per slice on the device (parareal.py:200-213);
+        returns (values, absolute flags)."""
+        S = x.shape[0]
+        err = (ctypes.c_double * S)()
+        ab = (ctypes.c_int32 * S)()
+        self.check(self.lib.pint_boundary_error(self.handle, S, _ptr(x), _ptr(ref), err, ab, _stream()),
+                   "pint_boundary_error")
+        return np.array(err[:]), np.array(ab[:], dtype=bool)
+
     def propagate(self, y_in: torch.Tensor, t0: Sequence[float], t_end: Sequence[float], nsteps: Sequence[int],
                   k: float, theta0: float, newton: NewtonSettings, krylov: KrylovSettings,
                   y_out: Optional[torch.Tensor] = None):
@@ -335,6 +368,19 @@ class FSIDevice:
                                      ft, _stream())
         self.check(rc, "pint_propagate")
         return y_out, np.array(nit[:]), np.array(kit[:]), np.array(status[:]), np.array(ft[:])
+
+
+def raise_step_failure(status, fail_t, k: float):
+    """Map the first failing slice's status to TimeStepError("implicit step
+    failed at t_n=..., k=...") wrapping NumericBreakdown / MaxItersExceeded
+    (integrators.py:92-95)."""
+    bad = [s for s in range(len(status)) if status[s] != _lib.PINT_OK]
+    if not bad:
+        return
+    s = bad[0]
+    cause = (MaxItersExceeded if status[s] == _lib.PINT_NEWTON_MAX_ITERS else NumericBreakdown)(
+        _lib.STATUS_NAMES.get(int(status[s]), str(status[s])))
+    raise TimeStepError(f"implicit step failed at t_n={float(fail_t[s])!r}, k={k!r}: {cause}") from cause
 
 
 # ----------------------------------------------------------------------------
@@ -363,6 +409,9 @@ class GPUThetaPropagator:
             device = FSIDevice(problem, max_slices, restart=self.krylov.restart)
         if device.problem != problem:
             raise ValueError("device context was built for another problem")
+        if device.restart != self.krylov.restart:
+            raise ValueError(f"device context has GMRES restart {device.restart}, the Krylov settings ask for "
+                             f"{self.krylov.restart}")
         self.device = device
         self.newton_iterations = 0
         self.krylov_iterations = 0
@@ -388,14 +437,33 @@ class GPUThetaPropagator:
             self.newton_iterations += int(nit.sum())
             self.krylov_iterations += int(kit.sum())
             self.steps_taken += int(sum(nsteps))
-        bad = [s for s in range(S) if status[s] != _lib.PINT_OK]
-        if bad:
-            s = bad[0]
-            cause = (MaxItersExceeded if status[s] == _lib.PINT_NEWTON_MAX_ITERS else NumericBreakdown)(
-                _lib.STATUS_NAMES.get(int(status[s]), str(status[s])))
-            k_fail = self.step
-            raise TimeStepError(f"implicit step failed at t_n={float(ft[s])!r}, k={k_fail!r}: {cause}") from cause
+        raise_step_failure(status, ft, self.step)
         return out
+
+    def sweep(self, x: torch.Tensor, t_grid: Sequence[float], c_new: torch.Tensor, x_prev=None, c_old=None,
+              f_old=None, variant: int = 0, clamp=(0.0, 1.0)):
+        """Sequential corrector sweep with this (coarse) propagator, on the device
+        (FSIDevice.coarse_sweep); returns (theta, corr) per slice and raises
+        TimeStepError for the first failing slice (its index in ``.interval``)."""
+        L = len(t_grid) - 1
+        nsteps = [split_window(t_grid[l + 1] - t_grid[l], self.step) if t_grid[l + 1] != t_grid[l] else 0
+                  for l in range(L)]
+        th, cr, nit, kit, status, ft = self.device.coarse_sweep(
+            x, t_grid, nsteps, self.step, self.settings.theta0, self.settings.newton, self.krylov, c_new,
+            x_prev=x_prev, c_old=c_old, f_old=f_old, variant=variant, clamp=clamp)
+        bad = [l for l in range(L) if status[l] != _lib.PINT_OK]
+        good = slice(0, bad[0]) if bad else slice(0, L)
+        with self._stats_lock:
+            self.newton_iterations += int(nit[good].sum())
+            self.krylov_iterations += int(kit[good].sum())
+            self.steps_taken += int(sum(nsteps[:bad[0]] if bad else nsteps))
+        if bad:
+            try:
+                raise_step_failure(status[bad[0]:bad[0] + 1], ft[bad[0]:bad[0] + 1], self.step)
+            except TimeStepError as exc:
+                exc.interval = bad[0]
+                raise
+        return th, cr
 
     # ---- host-State API (reference protocol) ---------------------------
     def advance_batch(self, states: Sequence[State], t_ends: Sequence[float]) -> List[State]:

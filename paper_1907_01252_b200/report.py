@@ -99,12 +99,34 @@ def load_rows(path: str) -> list:
     return out
 
 
+def model_speedup(r: float, iters: int, intervals: int) -> float:
+    """Theoretical Parareal speed-up 1 / (r + (K/N)(1 + r)) for step ratio
+    r = k/K, K iterations and N intervals."""
+    if not r > 0.0 or not 0 < iters <= intervals:
+        raise ValueError("need r > 0 and 0 < iters <= intervals")
+    return 1.0 / (r + (iters / intervals) * (1.0 + r))
+
+
+def sequential_device(F, s0, grid):
+    """Sequential fine solve over the boundary grid on the device (the
+    speed-up denominator of cli.py:305-316): [len(grid)] states, row 0 = s0."""
+    dev = F.device
+    out = dev.empty(len(grid))
+    out[0:1].copy_(dev.to_device(s0.values))
+    for l in range(len(grid) - 1):
+        F.advance_device(out[l:l + 1], [grid[l]], [grid[l + 1]], out=out[l + 1:l + 2])
+    return out
+
+
 def run_experiment_gpu(run_cfg, variants=("classic",), coarse_steps=None, reference_factor: int = 4,
                        max_iters: Optional[int] = None, tol: float = 1e-30, newton=None, krylov=None,
                        verbose: bool = False) -> list:
-    """Device restatement of the reference ``run_experiment`` for one FSI config."""
-    from .parareal import PararealConfig, SpeedupModel, boundary_error, run_parareal_device, sequential_solve, \
-        theoretical_speedup
+    """Device restatement of the reference ``run_experiment`` (cli.py:290-371)
+    for one FSI config: the sequential solve, the refined-step reference and
+    every Parareal iterate stay in HBM; boundary errors are device reductions."""
+    import torch
+
+    from .parareal import PararealConfig, run_parareal_device
     from .propagator import FSIDevice, KrylovSettings, NewtonSettings, ThetaSettings, initial_state, \
         make_propagator
     P = run_cfg.problem
@@ -117,15 +139,20 @@ def run_experiment_gpu(run_cfg, variants=("classic",), coarse_steps=None, refere
     grid = [run_cfg.t_end * l / L for l in range(L + 1)]
     grid[-1] = run_cfg.t_end
     fine = make_propagator(P, ThetaSettings(k, run_cfg.theta0, newton), krylov=krylov, device=dev)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    seq = sequential_solve(fine, s0, grid)
+    seq_dev = sequential_device(fine, s0, grid)
+    torch.cuda.synchronize()
     t_seq = time.perf_counter() - t0
     ref_prop = make_propagator(P, ThetaSettings(k / reference_factor, run_cfg.theta0, newton), krylov=krylov,
                                device=dev)
-    reference = sequential_solve(ref_prop, s0, grid)
-    disc = boundary_error(seq, reference)
-    rows = [ResultRow(P.name, 0.0, k, DISCRETIZATION_VARIANT, 0, l, disc[l].value, None) for l in range(1, L + 1)]
-    disc_final = disc[L].value
+    ref_dev = sequential_device(ref_prop, s0, grid)
+    disc, _ = dev.boundary_error(seq_dev[1:], ref_dev[1:])
+    rows = [ResultRow(P.name, 0.0, k, DISCRETIZATION_VARIANT, 0, l, float(disc[l - 1]), None)
+            for l in range(1, L + 1)]
+    disc_final = float(disc[L - 1])
+    seq_host = dev.to_host(seq_dev)
+    seq = [s0] + [s0.with_values(seq_host[l], time=grid[l]) for l in range(1, L + 1)]
     for K in (coarse_steps or [run_cfg.coarse_step]):
         for variant in variants:
             C = make_propagator(P, ThetaSettings(K, run_cfg.theta0, newton), krylov=krylov, device=dev)
@@ -136,16 +163,13 @@ def run_experiment_gpu(run_cfg, variants=("classic",), coarse_steps=None, refere
                 for l in range(1, L + 1):
                     rows.append(ResultRow(P.name, K, k, variant, i, l, tr.boundary_errors[i - 1][l - 1],
                                           tr.theta_values[i - 1][l - 1]))
-            qual = tr.iterations_run
-            for i in range(1, tr.iterations_run + 1):
-                if tr.boundary_errors[i - 1][L - 1] <= disc_final:
-                    qual = i
-                    break
+            # first iteration whose final-boundary error reaches the discretization floor
+            qual = next((i for i in range(1, tr.iterations_run + 1)
+                         if tr.boundary_errors[i - 1][L - 1] <= disc_final), tr.iterations_run)
             t_par = tr.iteration_seconds[qual - 1]
             rows.append(ResultRow(P.name, K, k, variant, qual, None, tr.boundary_errors[qual - 1][L - 1], None,
                                   t_seq_s=t_seq, t_par_s=t_par, speedup_meas=t_seq / t_par,
-                                  speedup_theory=theoretical_speedup(SpeedupModel(r=k / K, iters=qual,
-                                                                                  intervals=L))))
+                                  speedup_theory=model_speedup(k / K, qual, L)))
             if verbose:
                 print(f"[pint-b200] K={K:g} {variant}: {tr.iterations_run} its, t_par {t_par:.3f} s, "
                       f"t_seq {t_seq:.3f} s", flush=True)

@@ -4,6 +4,7 @@ CPU-oracle FSI propagators (oracle/fsi_oracle.py) as C and F.
 
   python tests/golden/make_parareal_goldens.py c1 classic
   python tests/golden/make_parareal_goldens.py small least_squares
+  python tests/golden/make_parareal_goldens.py small classic 2e-2   # tol-based stop
 
 Writes tests/golden/parareal_<case>_<variant>.npz with the final boundary
 states, the defect history (correction_norms), theta values and the
@@ -36,17 +37,18 @@ CASES = {
 }
 
 
-def main(case, variant):
+def main(case, variant, tol=1e-30):
     P, t_end, kf, kc, L, K = CASES[case]
     F = O.OracleFSIPropagator(P, kf, 1.0, NEWTON)
     C = O.OracleFSIPropagator(P, kc, 1.0, NEWTON)
     s0 = O.initial_state(P)
-    cfg = PararealConfig(intervals=L, max_iters=K, tol=1e-30, variant=variant)
+    cfg = PararealConfig(intervals=L, max_iters=K, tol=tol, variant=variant)
     t0 = time.time()
     states, trace = run_parareal(C, F, s0, t_end, cfg)
     dt = time.time() - t0
-    out = os.path.join(HERE, f"parareal_{case}_{variant}.npz")
-    np.savez_compressed(out, final=np.array([s.values for s in states]),
+    tag = "" if tol == 1e-30 else "_tol"
+    out = os.path.join(HERE, f"parareal_{case}_{variant}{tag}.npz")
+    np.savez_compressed(out, final=np.array([s.values for s in states]), tol=tol, converged=trace.converged,
                         correction_norms=np.array(trace.correction_norms),
                         theta_values=np.array(trace.theta_values), iterations_run=trace.iterations_run,
                         t_end=t_end, kf=kf, kc=kc, L=L, K=K, seconds=dt,
@@ -55,4 +57,5 @@ def main(case, variant):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "classic")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "classic",
+         float(sys.argv[3]) if len(sys.argv) > 3 else 1e-30)

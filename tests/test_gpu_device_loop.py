@@ -1,0 +1,191 @@
+"""GPU: the device-driven control flow (one CUDA graph with conditional
+WHILE / IF nodes per pint_propagate call, kernels_loop.cuh) against the
+host-driven loop (PINT_DEVICE_LOOP=0) -- same bits, same Newton / Krylov
+counts, same failure statuses and times -- and the device corrector sweep
+(pint_coarse_sweep) against its per-slice composition (batch-1 propagation +
+pint_parareal_correct_one), bitwise."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import fsi_oracle as O
+from paper_1907_01252_b200.problem import CONFIGS, channel_3d, small_problem
+
+pytestmark = pytest.mark.gpu
+NEWTON = dict(abs_tol=1e-10, rel_tol=1e-10)
+
+
+def _device(P, S, loop: bool):
+    from paper_1907_01252_b200.propagator import FSIDevice
+    old = os.environ.get("PINT_DEVICE_LOOP")
+    os.environ["PINT_DEVICE_LOOP"] = "1" if loop else "0"
+    try:
+        return FSIDevice(P, S)
+    finally:
+        if old is None:
+            del os.environ["PINT_DEVICE_LOOP"]
+        else:
+            os.environ["PINT_DEVICE_LOOP"] = old
+
+
+def _starts(P, step, S):
+    cpu = O.OracleFSIPropagator(P, step, 1.0, O.OracleNewtonSettings(**NEWTON))
+    s = [O.initial_state(P)]
+    for _ in range(S - 1):
+        s.append(cpu.advance(s[-1], s[-1].time + 2 * step))
+    return s
+
+
+def _run(dev, P, step, starts, windows, newton=None, krylov=None):
+    from paper_1907_01252_b200.propagator import KrylovSettings, NewtonSettings, split_window
+    newton = newton or NewtonSettings(**NEWTON)
+    krylov = krylov or KrylovSettings()
+    y = dev.to_device([s.values for s in starts])
+    t0 = [s.time for s in starts]
+    t1 = [s.time + w for s, w in zip(starts, windows)]
+    ns = [split_window(w, step) if w > 0 else 0 for w in windows]
+    out, nit, kit, status, ft = dev.propagate(y, t0, t1, ns, step, 1.0, newton, krylov)
+    return dev.to_host(out), nit, kit, status, ft
+
+
+@pytest.mark.parametrize("P,step", [
+    (small_problem(8, 2), 0.01),
+    (CONFIGS["c1"].problem, 0.002),
+    (channel_3d(10, 2, 2, name="small3d"), 0.01),
+])
+def test_device_loop_bitwise_equals_host_loop(cuda, P, step):
+    starts = _starts(P, step, 3)
+    windows = [5 * step, 3 * step, 0.0]  # ragged step counts and an empty window in one batch
+    a = _run(_device(P, 3, True), P, step, starts, windows)
+    b = _run(_device(P, 3, False), P, step, starts, windows)
+    assert a[0].tobytes() == b[0].tobytes()
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y), (x, y)
+    assert np.array_equal(a[0][2], starts[2].values)  # zero window: state unchanged
+
+
+def test_device_loop_batch_invariance_and_repeat(cuda):
+    P = small_problem(8, 2)
+    starts = _starts(P, 0.01, 3)
+    dev = _device(P, 3, True)
+    full = _run(dev, P, 0.01, starts, [0.04] * 3)
+    again = _run(dev, P, 0.01, starts, [0.04] * 3)
+    assert full[0].tobytes() == again[0].tobytes()
+    for s in range(3):
+        one = _run(dev, P, 0.01, starts[s:s + 1], [0.04])
+        assert one[0][0].tobytes() == full[0][s].tobytes()
+        assert one[1][0] == full[1][s] and one[2][0] == full[2][s]
+
+
+def test_device_loop_failure_statuses_match_host(cuda):
+    """A Newton budget of 1 iteration at a tight tolerance: MaxItersExceeded
+    on the first step of every slice, same status and t_n on both loops;
+    a NaN start: numeric breakdown."""
+    from paper_1907_01252_b200 import _lib
+    from paper_1907_01252_b200.propagator import NewtonSettings
+    P = small_problem(8, 2)
+    starts = _starts(P, 0.01, 2)
+    bad = starts[1].values.copy()
+    bad[P.num_nodes * 2 + 5] = np.nan
+    starts = [starts[0], starts[1].with_values(bad)]
+    tight = NewtonSettings(abs_tol=1e-14, rel_tol=0.0, max_iters=1)
+    a = _run(_device(P, 2, True), P, 0.01, starts, [0.03, 0.03], newton=tight)
+    b = _run(_device(P, 2, False), P, 0.01, starts, [0.03, 0.03], newton=tight)
+    assert list(a[3]) == list(b[3]) == [_lib.PINT_NEWTON_MAX_ITERS, _lib.PINT_NUMERIC_BREAKDOWN]
+    assert np.array_equal(a[4], b[4]) and a[4][0] == pytest.approx(0.01)
+    assert np.array_equal(a[1], b[1])
+
+
+def test_krylov_budget_is_per_slice(cuda):
+    """a slice at its Krylov budget stops alone; the other slices'
+    iterates do not depend on it (batch invariance under max_iters)."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = CONFIGS["c1"].problem
+    starts = _starts(P, 0.002, 2)
+    kr = KrylovSettings(max_iters=12, rtol_first=0.0)
+    for loop in (True, False):
+        dev = _device(P, 2, loop)
+        both = _run(dev, P, 0.002, starts, [0.004, 0.004], krylov=kr)
+        for s in range(2):
+            one = _run(dev, P, 0.002, starts[s:s + 1], [0.004], krylov=kr)
+            assert one[0][0].tobytes() == both[0][s].tobytes()
+
+
+def test_coarse_sweep_equals_per_slice_composition(cuda):
+    """pint_coarse_sweep (L loop-graph launches + K8b on the device, one host
+    sync) == batch-1 advance_device + pint_parareal_correct_one per slice."""
+    import ctypes
+    import torch
+    from paper_1907_01252_b200 import _lib
+    from paper_1907_01252_b200.propagator import NewtonSettings, ThetaSettings, _ptr, _stream, make_propagator
+    P = small_problem(8, 2)
+    L = 4
+    grid = [0.1 * l for l in range(L + 1)]
+    nw = NewtonSettings(**NEWTON)
+    C = make_propagator(P, ThetaSettings(0.05, 1.0, nw), max_slices=L)
+    dev = C.device
+    rng = np.random.default_rng(3)
+    base = _starts(P, 0.05, L + 1)
+    X = dev.to_device([s.values for s in base])
+    Xprev = dev.to_device([s.values + 1e-3 * rng.standard_normal(P.num_dofs) for s in base])
+    c_old = dev.to_device([s.values + 1e-3 * rng.standard_normal(P.num_dofs) for s in base[1:]])
+    f_old = dev.to_device([s.values + 1e-3 * rng.standard_normal(P.num_dofs) for s in base[1:]])
+    lib = _lib.load()
+    for variant in (0, 1, 2):
+        Xs, cs = X.clone(), dev.empty(L)
+        th, cr = C.sweep(Xs, grid, cs, x_prev=Xprev, c_old=c_old, f_old=f_old, variant=variant, clamp=(0.0, 1.2))
+        Xr, cr_ref, th_ref = X.clone(), [], []
+        for l in range(L):
+            cn = C.advance_device(Xr[l:l + 1], [grid[l]], [grid[l + 1]])
+            assert cn[0].cpu().numpy().tobytes() == cs[l].cpu().numpy().tobytes()
+            t, c = ctypes.c_double(), ctypes.c_double()
+            assert lib.pint_parareal_correct_one(dev.C, dev.nn, dev.np, _ptr(cn[0]), _ptr(f_old[l]), _ptr(c_old[l]),
+                                                 _ptr(Xprev[l + 1]), _ptr(Xr[l + 1]), variant, 0.0, 1.2,
+                                                 ctypes.byref(t), ctypes.byref(c), _stream()) == 0
+            th_ref.append(t.value)
+            cr_ref.append(c.value)
+        torch.cuda.synchronize()
+        assert Xs.cpu().numpy().tobytes() == Xr.cpu().numpy().tobytes()
+        assert list(th) == th_ref and list(cr) == cr_ref
+    # coarse initialisation: x[l+1] = c_new[l] = C(x[l])
+    Xi, ci = X.clone(), dev.empty(L)
+    th, cr = C.sweep(Xi, grid, ci)
+    assert list(th) == [1.0] * L and list(cr) == [0.0] * L
+    assert torch.equal(Xi[1:], ci)
+    seq = X.clone()
+    for l in range(L):
+        C.advance_device(seq[l:l + 1], [grid[l]], [grid[l + 1]], out=seq[l + 1:l + 2])
+    assert torch.equal(seq, Xi)
+
+
+def test_coarse_sweep_failure_names_the_slice(cuda):
+    from paper_1907_01252_b200.propagator import NewtonSettings, ThetaSettings, TimeStepError, make_propagator
+    P = small_problem(8, 2)
+    C = make_propagator(P, ThetaSettings(0.05, 1.0, NewtonSettings(**NEWTON)), max_slices=1)
+    dev = C.device
+    L = 3
+    X = dev.empty(L + 1)
+    X[0, 2, 5] = float("nan")
+    with pytest.raises(TimeStepError) as ei:
+        C.sweep(X, [0.0, 0.1, 0.2, 0.3], dev.empty(L))
+    assert ei.value.interval == 0
+
+
+def test_launch_count_is_reported(cuda):
+    """profile(1) counts the kernels the conditional bodies ran (device
+    counter) plus the top-level graph nodes."""
+    from paper_1907_01252_b200.propagator import KrylovSettings, NewtonSettings
+    P = small_problem(8, 2)
+    starts = _starts(P, 0.01, 2)
+    counts = {}
+    for loop in (True, False):
+        dev = _device(P, 2, loop)
+        _run(dev, P, 0.01, starts, [0.02, 0.02])  # warm-up (graph capture)
+        dev.profile(1)
+        _run(dev, P, 0.01, starts, [0.02, 0.02])
+        counts[loop] = dev.profile_read()["launches"]
+        dev.profile(0)
+    assert counts[True] > 100 and counts[False] > 100
+    assert 0.5 < counts[True] / counts[False] < 2.0, counts

@@ -1,11 +1,13 @@
 """GPU parity ladder, Parareal level: the batched GPU fine propagator and the
-device coarse sweep + K8 correction (run_parareal_device) against the CPU
-oracle driven by the REFERENCE driver (golden fixtures made by
-tests/golden/make_parareal_goldens.py): same iteration count, per-slice
-endpoint velocity / deformation / pressure to relative L2 <= 1e-6, defect
-history within |d_gpu - d_cpu| <= 1e-6 d_cpu + 10 delta_endpoint
-(SURVEY §8c rows 11a/11b).  Plus the driver contracts with the GPU
-propagator plugged in: exactness frontier, scheduler equivalence."""
+device coarse sweep + K8 correction (run_parareal_device: pint_coarse_sweep)
+against the CPU oracle driven by the REFERENCE driver (golden fixtures made by
+tests/golden/make_parareal_goldens.py): same iteration count (fixed-count and
+tolerance-stopped runs), per-slice endpoint velocity / deformation / pressure
+to relative L2 <= 1e-6, defect history within
+|d_gpu - d_cpu| <= 1e-6 d_cpu + 10 delta_endpoint,
+for the classic, least-squares and angle-penalized variants.  Plus the
+driver contracts with the GPU propagator plugged in: exactness frontier, the
+reference driver and the device driver agreeing, pipelined == device."""
 
 import os
 
@@ -14,6 +16,7 @@ import pytest
 
 from fields import field_errors
 from paper_1907_01252_b200.problem import CONFIGS, channel_3d, small_problem
+from refimport import pintbench
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -33,23 +36,29 @@ def _props(P, kf, kc, S):
     return F, C
 
 
-def _check_against_golden(case, variant, driver):
-    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal, run_parareal_device
+def _check_against_golden(case, variant, driver, tag=""):
+    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
-    path = os.path.join(GOLD, f"parareal_{case}_{variant}.npz")
+    path = os.path.join(GOLD, f"parareal_{case}_{variant}{tag}.npz")
     if not os.path.exists(path):
         pytest.skip(f"golden {path} not generated")
     g = np.load(path)
+    tol = float(g["tol"]) if "tol" in g else 1e-30
     P, t_end, kf, kc, L, K = CASES[case]
     F, C = _props(P, kf, kc, L)
-    cfg = PararealConfig(intervals=L, max_iters=K, tol=1e-30, variant=variant,
-                         scheduler="batched" if driver == "batched" else "serial")
     s0 = initial_state(P)
     if driver == "device":
+        cfg = PararealConfig(intervals=L, max_iters=K, tol=tol, variant=variant)
         states, tr = run_parareal_device(C, F, s0, t_end, cfg)
-    else:
-        states, tr = run_parareal(C, F, s0, t_end, cfg)
+    else:  # the unmodified reference driver with the GPU propagators plugged in
+        pb = pintbench()
+        if pb is None:
+            pytest.skip("reference package not available")
+        from pintbench.parareal import PararealConfig as RC, run_parareal as rrun
+        states, tr = rrun(C, F, s0, t_end, RC(intervals=L, max_iters=K, tol=tol, variant=variant))
     assert tr.iterations_run == int(g["iterations_run"])
+    if "converged" in g:
+        assert tr.converged == bool(g["converged"])
     delta = 0.0
     for l in range(1, L + 1):
         errs = field_errors(P, states[l].values, g["final"][l])
@@ -63,9 +72,23 @@ def _check_against_golden(case, variant, driver):
     return tr
 
 
-@pytest.mark.parametrize("driver", ["device", "batched"])
+@pytest.mark.parametrize("driver", ["device", "reference"])
 def test_small_classic_matches_reference_driver_on_oracle(cuda, driver):
     _check_against_golden("small", "classic", driver)
+
+
+@pytest.mark.parametrize("variant", ["least_squares", "angle_penalized"])
+def test_small_weighted_variants_match_reference_driver_on_oracle(cuda, variant):
+    tr = _check_against_golden("small", variant, "device")
+    assert all(0.0 <= th <= 1.0 for row in tr.theta_values for th in row)
+
+
+@pytest.mark.parametrize("driver", ["device", "reference"])
+def test_small_tolerance_stop_matches_reference_driver_on_oracle(cuda, driver):
+    """tol-based stop before max_iters: same iterations_run and
+    converged flag as the reference driver on the oracle."""
+    tr = _check_against_golden("small", "classic", driver, tag="_tol")
+    assert tr.converged and tr.iterations_run < 4
 
 
 def test_3d_classic_matches_reference_driver_on_oracle(cuda):
@@ -80,30 +103,43 @@ def test_c1_classic_matches_reference_driver_on_oracle(cuda):
 def test_exactness_frontier_with_gpu_fine(cuda):
     """Boundaries <= i of iteration i equal the sequential fine solution
     (reference test_parareal.py:217-224): needs a deterministic,
-    batch-invariant F."""
-    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device, sequential_solve
+    batch-invariant F; the boundary errors come from pint_boundary_error."""
+    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
     F, C = _props(P, kf, kc, L)
     s0 = initial_state(P)
     grid = [t_end * l / L for l in range(L + 1)]
-    seq = sequential_solve(F, s0, grid)
+    seq = [s0]
+    for t in grid[1:]:
+        seq.append(F.advance(seq[-1], t))
     _, tr = run_parareal_device(C, F, s0, t_end, PararealConfig(intervals=L, max_iters=3, tol=1e-30), oracle=seq)
     for i in range(1, tr.iterations_run + 1):
         for l in range(1, i + 1):
             assert tr.boundary_errors[i - 1][l - 1] <= 1e-12, (i, l, tr.boundary_errors[i - 1][l - 1])
+    # device boundary errors == the reference's definition on the host iterates
+    from oracle.parareal_oracle import boundary_error
+    for i in range(1, tr.iterations_run + 1):
+        for l in range(1, L + 1):
+            ref, _ = boundary_error(tr.iterate_values[i][l], seq[l].values)
+            assert abs(tr.boundary_errors[i - 1][l - 1] - ref) <= 1e-12 * max(ref, 1e-300) + 1e-15
 
 
-def test_device_and_host_drivers_agree(cuda):
-    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal, run_parareal_device
+@pytest.mark.skipif(pintbench() is None, reason="reference package not available")
+def test_device_and_reference_drivers_agree(cuda):
+    """The reference driver (host numpy correction, per-slice advance) and the
+    device driver (batched fine, pint_coarse_sweep) with the same GPU
+    propagators: same states to round-off, same theta / defects."""
+    from pintbench.parareal import PararealConfig as RC, run_parareal as rrun
+    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
     F, C = _props(P, kf, kc, L)
     s0 = initial_state(P)
-    for variant in ("classic", "angle_penalized"):
-        cfg = PararealConfig(intervals=L, max_iters=2, tol=1e-30, variant=variant)
-        a, ta = run_parareal_device(C, F, s0, t_end, cfg)
-        b, tb = run_parareal(C, F, s0, t_end, cfg)
+    for variant in ("classic", "least_squares", "angle_penalized"):
+        a, ta = run_parareal_device(C, F, s0, t_end, PararealConfig(intervals=L, max_iters=2, tol=1e-30,
+                                                                    variant=variant))
+        b, tb = rrun(C, F, s0, t_end, RC(intervals=L, max_iters=2, tol=1e-30, variant=variant))
         for l in range(L + 1):
             assert np.allclose(a[l].values, b[l].values, rtol=0, atol=1e-12 * max(1.0, np.abs(b[l].values).max()))
         assert np.allclose(ta.theta_values, tb.theta_values, rtol=1e-12, atol=0)
@@ -111,15 +147,15 @@ def test_device_and_host_drivers_agree(cuda):
 
 
 def test_k8_correction_kernel_matches_host(cuda):
-    """K8b (pint_parareal_correct_one) vs parareal_update + theta_weight +
-    correction norm on random states, all three variants, plus the
-    degenerate-block and clamp cases (reference test_parareal.py:57-99)."""
+    """K8b (pint_parareal_correct_one) vs the restated parareal_update +
+    theta_weight + correction norm (oracle/parareal_oracle.py) on random
+    states, all three variants, plus the degenerate-block and clamp cases
+    (reference test_parareal.py:57-99)."""
     import ctypes
     import torch
+    from oracle.parareal_oracle import correction_norm, parareal_update, theta_weight
     from paper_1907_01252_b200 import _lib
-    from paper_1907_01252_b200.parareal import correction_norm, parareal_update, theta_weight
     from paper_1907_01252_b200.propagator import _ptr, _stream
-    from paper_1907_01252_b200.state import State
     lib = _lib.load()
     C, nn, npad = 5, 300, 320
     rng = np.random.default_rng(0)
@@ -128,10 +164,10 @@ def test_k8_correction_kernel_matches_host(cuda):
         for clamp in ((0.0, 1.0), (0.0, 1.5)):
             vals = [rng.standard_normal(C * nn) for _ in range(4)]
             vals[0][2 * nn:3 * nn] = 0.0  # degenerate coarse block -> weight 1
-            cn, fo, co, xp = [State(v, 0.5, lay) for v in vals]
-            th_ref = theta_weight(fo, cn, variant, clamp)
+            cn, fo, co, xp = vals
+            th_ref = theta_weight(fo, cn, lay, variant, clamp)
             new_ref = parareal_update(cn, fo, co, th_ref)
-            corr_ref = correction_norm(new_ref.values, xp.values)
+            corr_ref = correction_norm(new_ref, xp)
             dev = [torch.zeros((C, npad), dtype=torch.float64, device="cuda") for _ in range(5)]
             for d, v in zip(dev, vals):
                 d[:, :nn] = torch.from_numpy(v.reshape(C, nn))
@@ -142,7 +178,7 @@ def test_k8_correction_kernel_matches_host(cuda):
             assert rc == 0
             out = dev[4][:, :nn].cpu().numpy().reshape(-1)
             assert abs(th.value - th_ref) <= 1e-13 * max(1.0, abs(th_ref))
-            assert np.allclose(out, new_ref.values, rtol=0, atol=1e-13)
+            assert np.allclose(out, new_ref, rtol=0, atol=1e-13)
             assert abs(cr.value - corr_ref) <= 1e-12 * corr_ref
     # K8a: batched pre-correction
     f = torch.randn(3, C, npad, dtype=torch.float64, device="cuda")

@@ -1,6 +1,7 @@
-"""CPU, world_size 2 (gloo): the sharded Parareal driver (one all-gather of
-fine endpoints per iteration) reproduces the serial driver bitwise, and the
-max-over-ranks timing reduction."""
+"""CPU, world_size 2 (gloo): the sharded device Parareal driver (one
+all_gather_into_tensor of the fine endpoints per iteration, device tensors)
+reproduces the single-rank driver bitwise, and the max-over-ranks timing
+reduction."""
 
 import os
 import socket
@@ -41,25 +42,31 @@ def _worker(rank, world, port, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    F = linprop.LinearPropagator(0.01, theta0=1.0)
-    C = linprop.LinearPropagator(0.1, theta0=1.0)
-    cfg = PararealConfig(intervals=6, max_iters=4, tol=1e-30, variant="least_squares")
-    _, tr = run_parareal_sharded(C, F, linprop.s0(), 1.2, cfg)
+    dev = linprop.CPUDevice()
+    F = linprop.DeviceLinearPropagator(0.01, theta0=1.0, device=dev)
+    C = linprop.DeviceLinearPropagator(0.1, theta0=1.0, device=dev)
+    cfg = PararealConfig(intervals=7, max_iters=4, tol=1e-30, variant="least_squares")
+    _, tr = run_parareal_sharded(C, F, linprop.s0(), 1.4, cfg)
     m = max_over_ranks(float(rank + 1))
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), it=np.array(tr.iterate_values),
-             corr=np.array(tr.correction_norms), theta=np.array(tr.theta_values), m=m, fine=tr.fine_propagations)
+             corr=np.array(tr.correction_norms), theta=np.array(tr.theta_values), m=m, fine=tr.fine_propagations,
+             fine_calls=F.calls)
     dist.destroy_process_group()
 
 
-def test_sharded_driver_equals_serial(tmp_path):
+def test_sharded_device_driver_equals_single_rank(tmp_path):
+    """world_size 2 over gloo: every rank propagates its block of 7 slices
+    (4 + 3), one all-gather per iteration, identical iterates on both ranks,
+    equal to the single-rank device driver bitwise."""
     import linprop
-    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal
+    from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     world = 2
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    F = linprop.LinearPropagator(0.01, theta0=1.0)
-    C = linprop.LinearPropagator(0.1, theta0=1.0)
-    _, ref = run_parareal(C, F, linprop.s0(), 1.2,
-                          PararealConfig(intervals=6, max_iters=4, tol=1e-30, variant="least_squares"))
+    dev = linprop.CPUDevice()
+    F = linprop.DeviceLinearPropagator(0.01, theta0=1.0, device=dev)
+    C = linprop.DeviceLinearPropagator(0.1, theta0=1.0, device=dev)
+    _, ref = run_parareal_device(C, F, linprop.s0(), 1.4,
+                                 PararealConfig(intervals=7, max_iters=4, tol=1e-30, variant="least_squares"))
     fines = 0
     for r in range(world):
         d = np.load(os.path.join(tmp_path, f"r{r}.npz"))
@@ -68,4 +75,5 @@ def test_sharded_driver_equals_serial(tmp_path):
         assert np.array_equal(d["theta"], np.array(ref.theta_values))
         assert float(d["m"]) == 2.0
         fines += int(d["fine"])
+        assert int(d["fine_calls"]) == (4 if r == 0 else 3) * 4  # only the rank's own block
     assert fines == ref.fine_propagations

@@ -50,7 +50,7 @@ def main():
         _, tr = run_parareal_device(C, F, initial_state(P), rc.t_end, cfg)
     wall = time.perf_counter() - t0
     print(json.dumps({"config": a.config, "driver": a.driver, "variant": a.variant, "stab_k": P.stab_k, "wall_s": wall, "init_s": tr.init_seconds,
-                      "fine_s": tr.fine_seconds, "iterations": tr.iterations_run,
+                      "fine_s": tr.fine_seconds, "sweep_s": tr.sweep_seconds, "iterations": tr.iterations_run,
                       "fine_steps_x_slices": rc.intervals * rc.fine_steps_per_window * tr.iterations_run,
                       "defects_last_boundary": [row[-1] for row in tr.correction_norms],
                       "max_defect_per_iteration": [max(row) for row in tr.correction_norms],
