@@ -1,37 +1,44 @@
 """Benchmark: batched fine propagator throughput (fine CN steps x slices / s).
 
 One bench *step* = the fine phase of one Parareal iteration of BASELINE
-config c2 (configs[1]): all 32 slices of the 64x16 channel/bar problem
-advanced over one window (64 shifted-CN steps of 2^-10 s, SURVEY §0.4
-substitution of the non-divisible 0.001) in ONE batched launch sequence,
-starting from the coarse-initialised boundary states (what iteration 1 of
-Parareal propagates).  Inputs are resident in HBM when the timed region
-starts; L2 (126 MB) is flushed before every timed step (a 256 MB write).
+config c3 (configs[2], the largest single-GPU configuration: 256x64 mesh,
+mu_s = 2e6): all 64 slices advanced over one window (64 shifted-CN steps of
+2^-11 s, SURVEY §0.4 substitution of the non-divisible 5e-4) in ONE
+pint_propagate call -- one CUDA-graph launch whose conditional nodes run the
+time-step / Newton / GMRES loops on the device -- starting from the
+coarse-initialised boundary states (what iteration 1 of Parareal propagates).
+Inputs are resident in HBM when the timed region starts; L2 (126 MB) is
+flushed before every timed step (a 256 MB write).  ``--config`` selects
+another BASELINE config (c1, c2, c4).
 
 ``value``  : slices x fine steps / device time (CUDA events, max over ranks)
 ``e2e``    : the same through the public host-State API (``advance_batch``:
              host States in, host States out; H2D of the inputs and D2H of
              the results inside every timed step)
-``roofline``: the level-0 cell-patch Vanka solve (k_vanka_cell), the
-             largest HBM-class kernel of the step, timed with CUDA events
-             around every launch in a separate profiled step; ``traffic`` is
-             its DRAM bytes per launch from the committed ncu --set full
-             capture (profiles/r01_ncu_traffic.json)
+``roofline``: the dominant HBM-class kernel (level-0 Vanka sweep), timed with
+             CUDA events around every launch in a separate profiled step;
+             ``traffic`` = its DRAM bytes per launch from the committed ncu
+             --set full capture (profiles/)
+``parity`` : the GPU propagator on the oracle-made start states of the
+             config fixture (tests/golden/config_<c>.npz) against the oracle's
+             endpoints: per-field relative L2 (north-star bar 1e-6)
 ``cpu_baseline``: the CPU oracle (numpy/scipy port of the same CN step,
-             oracle/fsi_oracle.py) on a bounded sample of the same workload.
+             oracle/fsi_oracle.py) on a bounded sample of the same workload,
+             from the same fixture start states, one core.
 
 ``--impl reference`` runs the reference arm: the CPU implementation of the
 path (the oracle port -- the reference package ships no FSI propagator,
-SURVEY §0.1) on all host cores, same metric/config, bounded sample per step.
+SURVEY §0.1) on all host cores, same metric / config, from the oracle's own
+coarse-initialised start states of the sample slices (the fixture; never GPU
+output), one process per sample slice, one CN step per slice per bench step.
 Multi-GPU (torchrun): slices shard across ranks with no data-path
-collective (weak scaling: every rank owns its own 32-slice batch).
+collective (weak scaling: every rank owns its own batch of the config).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -130,84 +137,156 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_oracle_sample(cfg, slices: int, steps: int, starts=None):
-    """Time the CPU oracle on ``slices`` x ``steps`` fine CN steps (1 core)."""
-    from oracle import fsi_oracle as O
-    P = cfg.problem
-    newton = O.OracleNewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
-    prop = O.OracleFSIPropagator(P, cfg.fine_step, cfg.theta0, newton)
+def fixture(config):
+    """The oracle-made parity / start-state fixture of a config (or None)."""
     import numpy as np
-    t0 = time.perf_counter()
-    for s in range(slices):
-        y = np.zeros(P.num_dofs) if starts is None else starts[s]
-        t = s * cfg.window
-        prop.advance_values(y, t, t + steps * cfg.fine_step)
+    path = os.path.join(ROOT, "tests", "golden", f"config_{config}.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    return {k: g[k] for k in g.files}
+
+
+def workload_config(args, cfg, ws):
+    """The static workload description, identical in both arms (the driver
+    compares the two lines' ``config``)."""
+    P = cfg.problem
+    return {"workload": f"{args.config}: fine phase of one Parareal iteration, "
+                        f"{cfg.intervals} slices x {cfg.fine_steps_per_window} shifted-CN steps per GPU",
+            "mesh": list(P.cells), "dofs_per_slice": P.num_dofs, "slices_per_gpu": cfg.intervals,
+            "fine_step": cfg.fine_step, "substitution": cfg.note or "none", "mu_s": P.mu_s,
+            "start_states": "coarse-initialised boundary states (Parareal iteration 1)",
+            "l2": "flushed before every step", "parallelism": f"slices sharded, {ws} GPU(s), no collective"}
+
+
+def _oracle_prop(cfg):
+    from oracle import fsi_oracle as O
+    return O.OracleFSIPropagator(cfg.problem, cfg.fine_step, cfg.theta0,
+                                 O.OracleNewtonSettings(abs_tol=1e-10, rel_tol=1e-10))
+
+
+def cpu_oracle_sample(cfg, fx, budget_s: float = 10.0):
+    """The CPU oracle (1 core) on fixture start states: fine CN steps of the
+    sample slices, round robin, until ``budget_s`` has passed (>= 1 step)."""
+    prop = _oracle_prop(cfg)
+    ys = {int(l): fx["starts"][j].copy() for j, l in enumerate(fx["slices"])}
+    ts = {l: l * cfg.window for l in ys}
+    order = sorted(ys)[::-1]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        l = order[done % len(order)]
+        ys[l] = prop.advance_values(ys[l], ts[l], ts[l] + cfg.fine_step)
+        ts[l] += cfg.fine_step
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
     dt = time.perf_counter() - t0
-    return slices * steps / dt, dt
+    return done / dt, dt, done
 
 
-def _ref_worker(args):
-    name, slices_idx, steps = args
+_REF = {}
+
+
+def _ref_init(name):
     from paper_1907_01252_b200.problem import CONFIGS
-    cfg = CONFIGS[name]
-    rate, dt = cpu_oracle_sample(cfg, len(slices_idx), steps)
-    return len(slices_idx) * steps, dt
+    _REF["cfg"] = CONFIGS[name]
+    _REF["prop"] = _oracle_prop(_REF["cfg"])
+    _REF["fx"] = fixture(name)
+
+
+def _ref_step(j):
+    """One fine CN step of sample slice j from its oracle-made start state."""
+    cfg, fx = _REF["cfg"], _REF["fx"]
+    l = int(fx["slices"][j])
+    t = l * cfg.window
+    _REF["prop"].advance_values(fx["starts"][j], t, t + cfg.fine_step)
+    return 1
 
 
 def run_reference(args):
-    """Reference arm: the CPU path (oracle port) on all host cores."""
+    """Reference arm: the CPU path (oracle port) on all host cores, from the
+    oracle's own coarse-initialised states of the config's sample slices."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
     import multiprocessing as mp
     from paper_1907_01252_b200.problem import CONFIGS
     cfg = CONFIGS[args.config]
+    fx = fixture(args.config)
+    if fx is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"fixture tests/golden/config_{args.config}.npz "
+                                                              "missing (oracle start states)"}), flush=True)
+        return
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    nproc = max(1, min(cores, cfg.intervals))
-    steps_per = 2
-    ctx = mp.get_context("spawn")
-    times = []
-    # one BLAS thread per worker process: the workers inherit the environment at spawn
+    nproc = max(1, min(cores, len(fx["slices"])))
+    # one BLAS thread per worker process (inherited at spawn); oracle built by the pool initializer
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
-    with ctx.Pool(nproc) as pool:
-        for it in range(args.warmup + args.steps):
+    # a CPU arm has nothing to warm up beyond its first step (no JIT, no caches
+    # that outlive a step): at most one untimed step, so the run stays bounded
+    warm = min(args.warmup, 1)
+    times = []
+    with mp.get_context("spawn").Pool(nproc, initializer=_ref_init, initargs=(args.config,)) as pool:
+        for it in range(warm + args.steps):
             t0 = time.perf_counter()
-            pool.map(_ref_worker, [(args.config, [p], steps_per) for p in range(nproc)])
+            units = sum(pool.map(_ref_step, list(range(nproc))))
             dt = time.perf_counter() - t0
-            if it >= args.warmup:
+            if it >= warm:
                 times.append(dt)
-    units = nproc * steps_per
     step_s = sum(times) / len(times)
     value = units / step_s
+    sample = (f"{nproc} slices ({', '.join(str(int(l)) for l in fx['slices'][:nproc])}) x 1 fine CN step of "
+              f"{args.config} per bench step, from the oracle's coarse-initialised states "
+              f"(tests/golden/config_{args.config}.npz), one process per slice, 1 BLAS thread each "
+              f"(oracle/fsi_oracle.py; the reference ships no FSI propagator, SURVEY §0.1)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} fine phase sample", "mesh": list(cfg.problem.cells),
-                   "slices": nproc, "fine_steps_per_slice": steps_per},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "port",
-                         "sample": f"{nproc} slices x {steps_per} fine CN steps of {args.config} per step from "
-                                   "rest at each window start, one process per slice (oracle/fsi_oracle.py; the "
-                                   "reference ships no FSI propagator, SURVEY §0.1)"},
+        "steps": args.steps, "warmup": warm, "warmup_requested": args.warmup, "ms_per_step": 1e3 * step_s,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, cfg, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def gpu_parity(F, dev, cfg, fx):
+    """GPU fine propagation of the fixture's parity slices from the oracle's
+    start states vs the oracle's endpoints: per-field relative L2."""
+    import numpy as np
+    if fx is None:
+        return None
+    P = cfg.problem
+    idx = [list(fx["slices"]).index(l) for l in fx["parity_slices"]]
+    starts = [fx["starts"][j] for j in idx]
+    t0 = [int(l) * cfg.window for l in fx["parity_slices"]]
+    steps = int(fx["fine_steps"])
+    out = dev.to_host(F.advance_device(dev.to_device(starts), t0, [t + steps * cfg.fine_step for t in t0]))
+    n, d = P.num_nodes, P.dim
+    fields = {"v": slice(0, d * n), "u": slice(d * n, 2 * d * n), "p": slice(2 * d * n, (2 * d + 1) * n)}
+    err = {}
+    for name, sl in fields.items():
+        e = 0.0
+        for s in range(len(starts)):
+            ref = fx["ends"][s][sl]
+            e = max(e, float(np.linalg.norm(out[s][sl] - ref) / np.linalg.norm(ref)))
+        err[name] = e
+    err.update({"slices": [int(l) for l in fx["parity_slices"]], "fine_steps": steps, "tolerance": 1e-6,
+                "pass": max(err[k] for k in fields) <= 1e-6,
+                "oracle": f"tests/golden/config_{cfg.problem.name}.npz (oracle coarse-initialised starts)"})
+    return err
+
+
 def coarse_states(C, dev, cfg, s0):
-    """Coarse-initialised boundary states X[0][0..L-1] on the device."""
+    """Coarse-initialised boundary states X[0][0..L-1] on the device (the
+    Parareal coarse initialisation, one pint_coarse_sweep call)."""
     import torch
     L = cfg.intervals
-    X = dev.empty(L)
-    cur = dev.to_device(s0.values)
-    X[0].copy_(cur[0])
-    for l in range(L - 1):
-        nxt = C.advance_device(cur, [l * cfg.window], [(l + 1) * cfg.window])
-        X[l + 1].copy_(nxt[0])
-        cur = nxt
+    X = dev.empty(L + 1)
+    X[0:1].copy_(dev.to_device(s0.values))
+    C.sweep(X, [l * cfg.window for l in range(L + 1)], dev.empty(L))
     torch.cuda.synchronize()
-    return X
+    return X[:L].clone()
 
 
 def run_ours(args):
@@ -321,28 +400,36 @@ def run_ours(args):
                     if l0_bytes < 126e6 else "") + "; see profiles/ and DESIGN.md §5"),
     }
 
+    # ---- parity on the oracle-made start states (outside the timed region)
+    fx = fixture(args.config)
+    parity = gpu_parity(F, dev, cfg, fx) if rank == 0 else None
+    # the GPU's own coarse initialisation vs the oracle's, at the fixture's sample slices
+    if rank == 0 and fx is not None:
+        got = dev.to_host(X0)
+        parity["coarse_init_rel_l2_max"] = max(
+            float(np.linalg.norm(got[int(l)] - fx["starts"][j]) / max(np.linalg.norm(fx["starts"][j]), 1e-300))
+            for j, l in enumerate(fx["slices"]) if int(l) < L and np.linalg.norm(fx["starts"][j]) > 0)
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        starts = dev.to_host(X0)[:2]
-        rate, dt = cpu_oracle_sample(cfg, 2, 4, starts=starts)
+    if rank == 0 and not args.no_cpu_baseline and fx is not None:
+        rate, dt, done = cpu_oracle_sample(cfg, fx)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"2 slices x 4 fine CN steps of {args.config} from the coarse-initialised states "
-                         f"({dt:.1f} s; numpy/scipy oracle, oracle/fsi_oracle.py)"}
+               "sample": f"{done} fine CN step(s) of {args.config} (sample slices "
+                         f"{', '.join(str(int(l)) for l in fx['slices'][::-1][:done])}) from the oracle's "
+                         f"coarse-initialised states ({dt:.1f} s; numpy/scipy oracle, oracle/fsi_oracle.py)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: fine phase of one Parareal iteration, "
-                                   f"{L} slices x {m_f} shifted-CN steps per GPU",
-                       "mesh": list(P.cells), "dofs_per_slice": P.num_dofs, "slices_per_gpu": L,
-                       "fine_step": cfg.fine_step, "substitution": cfg.note, "l2": "flushed before every step",
-                       "newton_per_step": nit, "krylov_per_newton": kit,
-                       "parallelism": f"slices sharded, {ws} GPU(s), no collective"},
+            "config": workload_config(args, cfg, ws),
+            "solver": {"newton_per_step": nit, "krylov_per_newton": kit,
+                       "control_flow": "device (one CUDA graph per call, conditional nodes)"
+                       if os.environ.get("PINT_DEVICE_LOOP", "1") != "0" else "host-driven"},
             "e2e": {"value": ws * L * m_f / e2e_s, "unit": UNIT, "h2d_bytes_per_step": bytes_io,
                     "d2h_bytes_per_step": bytes_io},
             "gpu_launches": launches,
             "roofline": roofline,
+            "parity": parity,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
@@ -357,7 +444,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default="c2", choices=("c1", "c2", "c3", "c4"))
+    ap.add_argument("--config", default="c3", choices=("c1", "c2", "c3", "c4"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pre", type=int, default=1, help="multigrid pre-smoothing sweeps")
     ap.add_argument("--post", type=int, default=1, help="multigrid post-smoothing sweeps")

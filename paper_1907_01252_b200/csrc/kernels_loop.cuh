@@ -157,11 +157,24 @@ __device__ __forceinline__ int cycle_begin(const LoopDev& d, int s, int m, int l
   return c;
 }
 
+// The cycles of one solve run in one of two WHILE loops: one-pass
+// Gram-Schmidt bodies when no running slice wants a second pass, two-pass
+// bodies (pass-2 kernels masked per slice) otherwise; the choice is fixed per
+// solve, so the other loop is never entered.
+__device__ __forceinline__ void set_cycle(const LoopDev& d, int any, int two, cudaGraphConditionalHandle h1,
+                                          int i1, cudaGraphConditionalHandle h2, int i2) {
+  any = __syncthreads_or(any);
+  two = __syncthreads_or(two);
+  set_cond(d, h1, i1, any && !two);
+  set_cond(d, h2, i2, any && two);
+}
+
 // tolerances and Gram-Schmidt passes per slice, then the first cycle
-__global__ void __launch_bounds__(kLoopThreads) k_gmres_init(LoopDev d, cudaGraphConditionalHandle h_cycle, int i_h_cycle) {
+__global__ void __launch_bounds__(kLoopThreads) k_gmres_init(LoopDev d, cudaGraphConditionalHandle h1, int i1,
+                                                             cudaGraphConditionalHandle h2, int i2) {
   pdl_wait();
   const LoopScalars* ls = d.ls;
-  int any = 0;
+  int any = 0, two = 0;
   for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
     // inexact-Newton forcing: first Newton iteration of the step at rtol_first
     const double rt = (d.its[s] == 0 && ls->lin_rtol_first > 0.0) ? fmax(ls->lin_rtol, ls->lin_rtol_first) : ls->lin_rtol;
@@ -169,54 +182,55 @@ __global__ void __launch_bounds__(kLoopThreads) k_gmres_init(LoopDev d, cudaGrap
     const double beta = d.running[s] ? d.rnorm[s] : 0.0;  // ||b|| = ||-r|| = ||r||, bitwise
     const double tol = fmax(rt * beta, at);
     d.gm_tol[s] = tol;
-    d.gm_two_pass[s] = ls->cgs_force ? (ls->cgs_force == 2) : (tol < 1e-7 * beta);
+    const int tp = ls->cgs_force ? (ls->cgs_force == 2) : (tol < 1e-7 * beta);
+    d.gm_two_pass[s] = tp;
     d.gres[s] = beta;
     d.gits[s] = 0;
     d.gm_its[s] = 0;
-    any |= cycle_begin(d, s, ls->m, ls->lin_max);
+    const int c = cycle_begin(d, s, ls->m, ls->lin_max);
+    any |= c;
+    two |= c && tp;
   }
-  any = __syncthreads_or(any);
-  set_cond(d, h_cycle, i_h_cycle, any);
+  set_cycle(d, any, two, h1, i1, h2, i2);
 }
 
 // cycle end: true residual norm and iteration count, then the next cycle
-__global__ void __launch_bounds__(kLoopThreads) k_cycle_end(LoopDev d, cudaGraphConditionalHandle h_cycle, int i_h_cycle) {
+__global__ void __launch_bounds__(kLoopThreads) k_cycle_end(LoopDev d, cudaGraphConditionalHandle h1, int i1,
+                                                            cudaGraphConditionalHandle h2, int i2) {
   pdl_wait();
   const LoopScalars* ls = d.ls;
-  int any = 0;
+  int any = 0, two = 0;
   for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
     if (d.cyc_active[s]) {
       d.gres[s] = d.norms[s];
       d.gits[s] = d.gm_its[s];
     }
-    any |= cycle_begin(d, s, ls->m, ls->lin_max);
+    const int c = cycle_begin(d, s, ls->m, ls->lin_max);
+    any |= c;
+    two |= c && d.gm_two_pass[s];
   }
-  any = __syncthreads_or(any);
-  set_cond(d, h_cycle, i_h_cycle, any);
+  set_cycle(d, any, two, h1, i1, h2, i2);
 }
 
-// before Arnoldi step j: any slice still iterating? any of them with a
-// second Gram-Schmidt pass?
-__global__ void __launch_bounds__(kLoopThreads) k_arnoldi_gate(LoopDev d, cudaGraphConditionalHandle h_step, int i_h_step,
-                                                               cudaGraphConditionalHandle h_two, int i_h_two) {
+// before a block of Arnoldi steps: any slice still iterating?
+__global__ void __launch_bounds__(kLoopThreads) k_arnoldi_gate(LoopDev d, cudaGraphConditionalHandle h_step,
+                                                               int i_h_step) {
   pdl_wait();
   const int S = d.ls->S;
-  int any = 0, two = 0;
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    const int a = d.gm_active[s];
-    any |= a;
-    two |= a && d.gm_two_pass[s];
-  }
+  int any = 0;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) any |= d.gm_active[s];
   any = __syncthreads_or(any);
-  two = __syncthreads_or(two);
   set_cond(d, h_step, i_h_step, any);
-  if (i_h_two >= 0) set_cond(d, h_two, i_h_two, two);
 }
 
+// after the solve: Krylov counts (multigrid drift rule), then the line search
+// (linalg.py:226-239) starts at lambda = 1 for every running slice
 __global__ void __launch_bounds__(kLoopThreads) k_gmres_end(LoopDev d) {
   pdl_wait();
   const LoopScalars* ls = d.ls;
   for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
+    d.lam[s] = 1.0;
+    d.ls_mask[s] = d.running[s];
     if (!d.running[s]) continue;
     d.kit[s] += d.gits[s];
     if (ls->it == 0) {
@@ -224,19 +238,6 @@ __global__ void __launch_bounds__(kLoopThreads) k_gmres_end(LoopDev d) {
       if (d.built_now[s]) d.base[s] = d.gits[s];
     }
   }
-}
-
-// ---- line search (linalg.py:226-239): lambda = 1, halve to damping_min
-__global__ void __launch_bounds__(kLoopThreads) k_ls_init(LoopDev d, cudaGraphConditionalHandle h_ls, int i_h_ls) {
-  pdl_wait();
-  int any = 0;
-  for (int s = threadIdx.x; s < d.ls->S; s += blockDim.x) {
-    d.lam[s] = 1.0;
-    d.ls_mask[s] = d.running[s];
-    any |= d.running[s];
-  }
-  any = __syncthreads_or(any);
-  set_cond(d, h_ls, i_h_ls, any);
 }
 
 __global__ void __launch_bounds__(kLoopThreads) k_ls_update(LoopDev d, cudaGraphConditionalHandle h_ls, int i_h_ls) {
@@ -259,31 +260,22 @@ __global__ void __launch_bounds__(kLoopThreads) k_ls_update(LoopDev d, cudaGraph
   set_cond(d, h_ls, i_h_ls, any);
 }
 
-// accept the trial (linalg.py:238-240): non-finite -> breakdown
-__global__ void __launch_bounds__(kLoopThreads) k_accept(LoopDev d) {
+// accept the trial (linalg.py:238-240; the copies of y and r were made by
+// k_accept_copy from the same mask): non-finite -> breakdown
+__global__ void __launch_bounds__(kLoopThreads) k_newton_update(LoopDev d, cudaGraphConditionalHandle h_newton, int i_h_newton) {
   pdl_wait();
-  for (int s = threadIdx.x; s < d.ls->S; s += blockDim.x) {
-    d.accept[s] = 0;
+  LoopScalars* ls = d.ls;
+  int any = 0;
+  for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
     if (!d.running[s]) continue;
     if (!isfinite(d.tnorm[s])) {
       d.status[s] = 1;
       d.running[s] = 0;
       continue;
     }
-    d.accept[s] = 1;
-  }
-}
-
-__global__ void __launch_bounds__(kLoopThreads) k_newton_update(LoopDev d, cudaGraphConditionalHandle h_newton, int i_h_newton) {
-  pdl_wait();
-  LoopScalars* ls = d.ls;
-  int any = 0;
-  for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
-    if (d.accept[s]) {
-      d.rnorm[s] = d.tnorm[s];
-      d.its[s] += 1;
-      d.running[s] = d.rnorm[s] > d.target[s];
-    }
+    d.rnorm[s] = d.tnorm[s];
+    d.its[s] += 1;
+    d.running[s] = d.rnorm[s] > d.target[s];
     any |= d.running[s];
   }
   any = __syncthreads_or(any);
@@ -291,6 +283,35 @@ __global__ void __launch_bounds__(kLoopThreads) k_newton_update(LoopDev d, cudaG
   __syncthreads();
   if (threadIdx.x == 0) ls->it = it;
   set_cond(d, h_newton, i_h_newton, any && it < ls->newton_max);
+}
+
+// GMRES start vectors for the running slices: b = -r, x = 0, u = b (cycle-start residual)
+__global__ void k_gmres_prep(double* __restrict__ b, double* __restrict__ x, double* __restrict__ u,
+                             const double* __restrict__ r, size_t per_slice, const int* __restrict__ running) {
+  pdl_wait();
+  const int s = blockIdx.y;
+  if (!running[s]) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = s * per_slice + i;
+    const double v = -r[e];
+    b[e] = v;
+    u[e] = v;
+    x[e] = 0.0;
+  }
+}
+
+// y = y_trial, r = r_trial on the slices whose trial is accepted (running, finite norm)
+__global__ void k_accept_copy(double* __restrict__ y, const double* __restrict__ yt, double* __restrict__ r,
+                              const double* __restrict__ rt, size_t per_slice, const int* __restrict__ running,
+                              const double* __restrict__ tnorm) {
+  pdl_wait();
+  const int s = blockIdx.y;
+  if (!running[s] || !isfinite(tnorm[s])) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = s * per_slice + i;
+    y[e] = yt[e];
+    r[e] = rt[e];
+  }
 }
 
 // after the Newton loop (linalg.py:244-248) and the step (integrators.py:157-162)

@@ -169,6 +169,8 @@ struct pint_ctx {
   // ---- device-driven control flow (Impl::propagate_dev): the whole
   // propagate call as one CUDA graph with conditional WHILE / IF nodes
   bool device_loop = true;      // PINT_DEVICE_LOOP=0: host-driven Newton / GMRES
+  int gate = 4;                 // PINT_GATE: Arnoldi steps per conditional IF block
+  int gate0 = 12;               // PINT_GATE0: leading Arnoldi steps of a cycle without a gate
   LoopDev ld{};
   LoopScalars* h_ls = nullptr;  // pinned staging of the call scalars
   size_t tab_cap = 0, lsv_cap = 0;
@@ -910,17 +912,16 @@ struct Impl {
     arnoldi_tail(ctx, S, j, npass == 2 ? ctx->gm_two_pass : nullptr, defer, st);
   }
 
-  // the same step inside the device-driven loop: the second Gram-Schmidt pass
-  // runs under IF(any active slice wants it), set by k_arnoldi_gate
-  static int arnoldi_step_dev(pint_ctx* ctx, int S, int j, cudaStream_t st, int depth,
-                              cudaGraphConditionalHandle h_two, int i_two) {
+  // the same step inside the device-driven loop: `two` selects the two-pass
+  // form (pass-2 kernels masked to the slices that want it, bitwise the
+  // one-pass computation for the others)
+  static int arnoldi_step_dev(pint_ctx* ctx, int S, int j, bool two, cudaStream_t st) {
     const bool defer = arnoldi_front(ctx, S, j, st);
     cgs_mdot(ctx, S, j, 0, nullptr, st);
-    PINT_TRY(capture_cond(ctx, st, depth, h_two, false, i_two, [&](cudaStream_t s2, int) {
-      cgs_update(ctx, S, j, 0, ctx->gm_two_pass, s2);
-      cgs_mdot(ctx, S, j, 1, ctx->gm_two_pass, s2);
-      return PINT_OK;
-    }));
+    if (two) {
+      cgs_update(ctx, S, j, 0, ctx->gm_two_pass, st);
+      cgs_mdot(ctx, S, j, 1, ctx->gm_two_pass, st);
+    }
     arnoldi_tail(ctx, S, j, ctx->gm_two_pass, defer, st);
     PINT_LAUNCHED();
     return PINT_OK;
@@ -1325,10 +1326,106 @@ struct Impl {
   // statement; every per-slice decision is made on the device from the
   // slice's own numbers, so there is no host round trip inside the call and the
   // result equals the host-driven path bitwise.
-  static int capture_propagate(pint_ctx* ctx, int S, const pint_krylov_opts* ko, cudaStream_t st0) {
+  // one restart cycle of flexible GMRES(m) on stream s (depth dp): v0 = u / beta,
+  // the Arnoldi steps (the first ctx->gate0 unconditionally, the rest under
+  // IF(any slice still iterating) in blocks of ctx->gate), the update
+  // x += Z y, the true residual u = b - J x and its norm; two: the second
+  // Gram-Schmidt pass runs (masked per slice)
+  static int capture_cycle(pint_ctx* ctx, int S, bool two, cudaStream_t s3, int dp3) {
     const size_t n = vs(ctx);
     const int m = ctx->restart;
     const size_t vstride = (size_t)ctx->maxS * n;
+    const LoopDev d = ctx->ld;
+    pint_launch(ctx, s3, k_scale_inv, vec_grid(n, S), 256, 0, ctx->V, (const double*)ctx->u,
+                (const double*)ctx->gm_beta, n, (const int*)ctx->cyc_active);
+    const int j_free = std::min(m, ctx->gate0);
+    for (int j = 0; j < j_free; ++j) PINT_TRY(arnoldi_step_dev(ctx, S, j, two, s3));
+    for (int j0 = j_free; j0 < m; j0 += ctx->gate) {
+      const int j1 = std::min(m, j0 + ctx->gate);
+      cudaGraphConditionalHandle h_j;
+      const int i_j = (int)ctx->body_nodes.size();
+      PINT_TRY(new_cond(ctx, &h_j));
+      pint_launch(ctx, s3, k_arnoldi_gate, 1, kLoopThreads, 0, d, h_j, i_j);
+      PINT_TRY(capture_cond(ctx, s3, dp3, h_j, false, i_j, [&](cudaStream_t s4, int) -> int {
+        for (int j = j0; j < j1; ++j) PINT_TRY(arnoldi_step_dev(ctx, S, j, two, s4));
+        return PINT_OK;
+      }));
+    }
+    pint_launch(ctx, s3, k_gmres_solve, (S + 127) / 128, 128, 0, m, (const double*)ctx->H, (const double*)ctx->gv,
+                (const int*)ctx->gm_steps, ctx->ybuf, (const int*)ctx->cyc_active, S);
+    pint_launch(ctx, s3, k_mcombine, vec_grid(n, S), 256, 0, ctx->u, (const double*)ctx->Z, vstride,
+                (const double*)ctx->ybuf, m + 1, (const int*)ctx->gm_steps, n, (const int*)ctx->cyc_active);
+    pint_launch(ctx, s3, k_axpy_one, vec_grid(n, S), 256, 0, ctx->dx, (const double*)ctx->u, n,
+                (const int*)ctx->cyc_active);
+    if (wide(ctx->g.nn, S))
+      pint_launch(ctx, s3, k_spmv<D, true, 3>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
+                  (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
+                  (const int*)ctx->cyc_active);
+    else
+      pint_launch(ctx, s3, k_spmv<D, true, 9>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
+                  (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
+                  (const int*)ctx->cyc_active);
+    return norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, s3);
+  }
+
+  // one line-search trial: y_trial = y + lambda dx, its residual norm, the
+  // halving rule (linalg.py:226-237); sets the line-search handle
+  static int capture_trial(pint_ctx* ctx, int S, cudaGraphConditionalHandle h_ls, int i_ls, cudaStream_t st) {
+    const size_t n = vs(ctx);
+    const LoopDev d = ctx->ld;
+    pint_launch(ctx, st, k_trial, vec_grid(n, S), 256, 0, ctx->ytrial, (const double*)ctx->ynew,
+                (const double*)ctx->dx, (const double*)d.lam, n, (const int*)d.ls_mask);
+    PINT_TRY(residual(ctx, S, ctx->ytrial, ctx->ystate, ctx->rtrial, d.ls_mask, nullptr, st));
+    pint_launch(ctx, st, k_ls_update, 1, kLoopThreads, 0, d, h_ls, i_ls);
+    return PINT_OK;
+  }
+
+  // one Newton iteration (linalg.py:220-240); sets the Newton handle
+  static int capture_newton_iter(pint_ctx* ctx, int S, const pint_krylov_opts* ko, cudaGraphConditionalHandle h_newton,
+                                 int i_newton, cudaStream_t s2, int dp2) {
+    const size_t n = vs(ctx);
+    const LoopDev d = ctx->ld;
+    PINT_TRY(assemble(ctx, S, ctx->ynew, ctx->ystate, d.running, s2));
+    cudaGraphConditionalHandle h_prec;
+    const int i_prec = (int)ctx->body_nodes.size();
+    PINT_TRY(new_cond(ctx, &h_prec));
+    pint_launch(ctx, s2, k_precond_decide, 1, kLoopThreads, 0, d, h_prec, i_prec);
+    PINT_TRY(capture_cond(ctx, s2, dp2, h_prec, false, i_prec, [&](cudaStream_t s3, int) -> int {
+      return precond_setup(ctx, S, ko, d.need, s3);
+    }));
+    pint_launch(ctx, s2, k_gmres_prep, vec_grid(n, S), 256, 0, ctx->b, ctx->dx, ctx->u, (const double*)ctx->r, n,
+                (const int*)d.running);
+    // restart cycles: two-pass loop first (a solve can only drop from two passes to one)
+    cudaGraphConditionalHandle h1, h2;
+    const int i1 = (int)ctx->body_nodes.size();
+    PINT_TRY(new_cond(ctx, &h1));
+    const int i2 = (int)ctx->body_nodes.size();
+    PINT_TRY(new_cond(ctx, &h2));
+    pint_launch(ctx, s2, k_gmres_init, 1, kLoopThreads, 0, d, h1, i1, h2, i2);
+    for (int two = 1; two >= 0; --two)
+      PINT_TRY(capture_cond(ctx, s2, dp2, two ? h2 : h1, true, two ? i2 : i1, [&](cudaStream_t s3, int dp3) -> int {
+        PINT_TRY(capture_cycle(ctx, S, two == 1, s3, dp3));
+        pint_launch(ctx, s3, k_cycle_end, 1, kLoopThreads, 0, d, h1, i1, h2, i2);
+        return PINT_OK;
+      }));
+    pint_launch(ctx, s2, k_gmres_end, 1, kLoopThreads, 0, d);
+    // line search: the first trial always, further halvings under WHILE
+    cudaGraphConditionalHandle h_ls;
+    const int i_ls = (int)ctx->body_nodes.size();
+    PINT_TRY(new_cond(ctx, &h_ls));
+    PINT_TRY(capture_trial(ctx, S, h_ls, i_ls, s2));
+    PINT_TRY(capture_cond(ctx, s2, dp2, h_ls, true, i_ls, [&](cudaStream_t s3, int) -> int {
+      return capture_trial(ctx, S, h_ls, i_ls, s3);
+    }));
+    pint_launch(ctx, s2, k_accept_copy, vec_grid(n, S), 256, 0, ctx->ynew, (const double*)ctx->ytrial, ctx->r,
+                (const double*)ctx->rtrial, n, (const int*)d.running, (const double*)d.tnorm);
+    pint_launch(ctx, s2, k_newton_update, 1, kLoopThreads, 0, d, h_newton, i_newton);
+    PINT_LAUNCHED();
+    return PINT_OK;
+  }
+
+  static int capture_propagate(pint_ctx* ctx, int S, const pint_krylov_opts* ko, cudaStream_t st0) {
+    const size_t n = vs(ctx);
     const LoopDev d = ctx->ld;
     cudaGraphConditionalHandle h_step;
     const int i_step = (int)ctx->body_nodes.size();
@@ -1344,79 +1441,10 @@ struct Impl {
       const int i_newton = (int)ctx->body_nodes.size();
       PINT_TRY(new_cond(ctx, &h_newton));
       pint_launch(ctx, s1, k_newton_init, 1, kLoopThreads, 0, d, h_newton, i_newton);
+      // the first Newton iteration always (a converged start runs it masked), the rest under WHILE
+      PINT_TRY(capture_newton_iter(ctx, S, ko, h_newton, i_newton, s1, dp1));
       PINT_TRY(capture_cond(ctx, s1, dp1, h_newton, true, i_newton, [&](cudaStream_t s2, int dp2) -> int {
-        // ---- one Newton iteration (linalg.py:220-240)
-        PINT_TRY(assemble(ctx, S, ctx->ynew, ctx->ystate, d.running, s2));
-        cudaGraphConditionalHandle h_prec;
-        const int i_prec = (int)ctx->body_nodes.size();
-        PINT_TRY(new_cond(ctx, &h_prec));
-        pint_launch(ctx, s2, k_precond_decide, 1, kLoopThreads, 0, d, h_prec, i_prec);
-        PINT_TRY(capture_cond(ctx, s2, dp2, h_prec, false, i_prec, [&](cudaStream_t s3, int) -> int {
-          return precond_setup(ctx, S, ko, d.need, s3);
-        }));
-        pint_launch(ctx, s2, k_negate, vec_grid(n, S), 256, 0, ctx->b, (const double*)ctx->r, n, (const int*)d.running);
-        pint_launch(ctx, s2, k_zero_active, vec_grid(n, S), 256, 0, ctx->dx, n, (const int*)d.running);
-        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->u, (const double*)ctx->b, n,
-                    (const int*)d.running);
-        cudaGraphConditionalHandle h_cycle;
-        const int i_cycle = (int)ctx->body_nodes.size();
-        PINT_TRY(new_cond(ctx, &h_cycle));
-        pint_launch(ctx, s2, k_gmres_init, 1, kLoopThreads, 0, d, h_cycle, i_cycle);
-        PINT_TRY(capture_cond(ctx, s2, dp2, h_cycle, true, i_cycle, [&](cudaStream_t s3, int dp3) -> int {
-          // ---- one restart cycle of flexible GMRES(m): v0 = r / beta
-          pint_launch(ctx, s3, k_scale_inv, vec_grid(n, S), 256, 0, ctx->V, (const double*)ctx->u,
-                      (const double*)ctx->gm_beta, n, (const int*)ctx->cyc_active);
-          for (int j = 0; j < m; ++j) {
-            cudaGraphConditionalHandle h_j, h_two;
-            const int i_j = (int)ctx->body_nodes.size();
-            PINT_TRY(new_cond(ctx, &h_j));
-            const int i_two = (int)ctx->body_nodes.size();
-            PINT_TRY(new_cond(ctx, &h_two));
-            pint_launch(ctx, s3, k_arnoldi_gate, 1, kLoopThreads, 0, d, h_j, i_j, h_two, i_two);
-            PINT_TRY(capture_cond(ctx, s3, dp3, h_j, false, i_j, [&](cudaStream_t s4, int dp4) -> int {
-              return arnoldi_step_dev(ctx, S, j, s4, dp4, h_two, i_two);
-            }));
-          }
-          // x += Z y (flexible GMRES), true residual r = b - J x into u (next cycle start)
-          pint_launch(ctx, s3, k_gmres_solve, (S + 127) / 128, 128, 0, m, (const double*)ctx->H,
-                      (const double*)ctx->gv, (const int*)ctx->gm_steps, ctx->ybuf, (const int*)ctx->cyc_active, S);
-          pint_launch(ctx, s3, k_mcombine, vec_grid(n, S), 256, 0, ctx->u, (const double*)ctx->Z, vstride,
-                      (const double*)ctx->ybuf, m + 1, (const int*)ctx->gm_steps, n, (const int*)ctx->cyc_active);
-          pint_launch(ctx, s3, k_axpy_one, vec_grid(n, S), 256, 0, ctx->dx, (const double*)ctx->u, n,
-                      (const int*)ctx->cyc_active);
-          if (wide(ctx->g.nn, S))
-            pint_launch(ctx, s3, k_spmv<D, true, 3>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
-                        (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
-                        (const int*)ctx->cyc_active);
-          else
-            pint_launch(ctx, s3, k_spmv<D, true, 9>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g,
-                        (const double*)ctx->lv[0].A, (const double*)ctx->dx, (const double*)ctx->b, ctx->u,
-                        (const int*)ctx->cyc_active);
-          PINT_TRY(norms(ctx, S, ctx->u, ctx->u, ctx->cyc_active, true, nullptr, nullptr, s3));
-          pint_launch(ctx, s3, k_cycle_end, 1, kLoopThreads, 0, d, h_cycle, i_cycle);
-          return PINT_OK;
-        }));
-        pint_launch(ctx, s2, k_gmres_end, 1, kLoopThreads, 0, d);
-        // ---- line search: lambda = 1, halve down to damping_min, accept anyway
-        cudaGraphConditionalHandle h_ls;
-        const int i_ls = (int)ctx->body_nodes.size();
-        PINT_TRY(new_cond(ctx, &h_ls));
-        pint_launch(ctx, s2, k_ls_init, 1, kLoopThreads, 0, d, h_ls, i_ls);
-        PINT_TRY(capture_cond(ctx, s2, dp2, h_ls, true, i_ls, [&](cudaStream_t s3, int) -> int {
-          pint_launch(ctx, s3, k_trial, vec_grid(n, S), 256, 0, ctx->ytrial, (const double*)ctx->ynew,
-                      (const double*)ctx->dx, (const double*)d.lam, n, (const int*)d.ls_mask);
-          PINT_TRY(residual(ctx, S, ctx->ytrial, ctx->ystate, ctx->rtrial, d.ls_mask, nullptr, s3));
-          pint_launch(ctx, s3, k_ls_update, 1, kLoopThreads, 0, d, h_ls, i_ls);
-          return PINT_OK;
-        }));
-        pint_launch(ctx, s2, k_accept, 1, kLoopThreads, 0, d);
-        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->ynew, (const double*)ctx->ytrial, n,
-                    (const int*)d.accept);
-        pint_launch(ctx, s2, k_copy_active, vec_grid(n, S), 256, 0, ctx->r, (const double*)ctx->rtrial, n,
-                    (const int*)d.accept);
-        pint_launch(ctx, s2, k_newton_update, 1, kLoopThreads, 0, d, h_newton, i_newton);
-        PINT_LAUNCHED();
-        return PINT_OK;
+        return capture_newton_iter(ctx, S, ko, h_newton, i_newton, s2, dp2);
       }));
       pint_launch(ctx, s1, k_step_end, 1, kLoopThreads, 0, d, h_step, i_step);
       pint_launch(ctx, s1, k_copy_active, vec_grid(n, S), 256, 0, ctx->ystate, (const double*)ctx->ynew, n,
@@ -1459,6 +1487,13 @@ int check_S(pint_ctx* ctx, int S) {
 }
 
 // ---------------------------------------------------------------- device-driven propagate (host side)
+// the device-driven loop covers every option except the diagnostics that need
+// the host in the loop (per-iteration trace, CUDA-event profiling) and the
+// A/B variants kept for measurement (split norm, fused Arnoldi kernel)
+bool use_device_loop(const pint_ctx* ctx) {
+  return ctx->device_loop && !ctx->prof && !ctx->verbose && !ctx->split_norm && !ctx->use_fused;
+}
+
 template <typename T>
 int grow(pint_ctx* ctx, T** d, T** h, size_t count) {
   if (*d) cudaFree(*d);
@@ -1675,19 +1710,33 @@ int coarse_sweep(pint_ctx* ctx, int L, double* x, const double* x_prev, double* 
     ctx->h_nsteps[l] = nsteps[l];
     ctx->h_lsv[l] = call_scalars(ctx, 1, nsteps[l], no, ko, off[l], l);
   }
+  // host-driven fallback (PINT_DEVICE_LOOP=0 / profiling): batch-1 host loop per slice, same bits
+  const bool dev_loop = use_device_loop(ctx);
   std::pair<cudaGraphExec_t, long long>* graph = nullptr;
-  PINT_TRY(get_loop_graph(ctx, 1, ko, st, &graph));
+  if (dev_loop) PINT_TRY(get_loop_graph(ctx, 1, ko, st, &graph));
   PINT_CHECK(cudaMemcpyAsync(ctx->d_sts, ctx->h_sts, sizeof(StepScalars) * ents, cudaMemcpyHostToDevice, st));
   PINT_CHECK(cudaMemcpyAsync(ctx->d_t1tab, ctx->h_t1tab, sizeof(double) * ents, cudaMemcpyHostToDevice, st));
   PINT_CHECK(cudaMemcpyAsync(ctx->d_nsteps, ctx->h_nsteps, sizeof(int) * L, cudaMemcpyHostToDevice, st));
   PINT_CHECK(cudaMemcpyAsync(ctx->d_lsv, ctx->h_lsv, sizeof(LoopScalars) * L, cudaMemcpyHostToDevice, st));
+  std::vector<int> h_status(L, 0), h_nit(L, 0), h_kit(L, 0);
+  std::vector<double> h_ft(L, 0.0);
   for (int l = 0; l < L; ++l) {
-    PINT_CHECK(cudaMemcpyAsync(ctx->ystate, x + l * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    PINT_CHECK(cudaMemcpyAsync(ctx->ld.ls, ctx->d_lsv + l, sizeof(LoopScalars), cudaMemcpyDeviceToDevice, st));
-    PINT_CHECK(cudaGraphLaunch(graph->first, st));
-    ctx->launches += graph->second;
-    pint_launch(ctx, st, k_sweep_record, 1, 32, 0, ctx->ld, l, ctx->sw_status, ctx->sw_nit, ctx->sw_kit, ctx->sw_ft);
     double* cn = c_new + l * n;
+    if (dev_loop) {
+      PINT_CHECK(cudaMemcpyAsync(ctx->ystate, x + l * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      PINT_CHECK(cudaMemcpyAsync(ctx->ld.ls, ctx->d_lsv + l, sizeof(LoopScalars), cudaMemcpyDeviceToDevice, st));
+      PINT_CHECK(cudaGraphLaunch(graph->first, st));
+      ctx->launches += graph->second;
+      pint_launch(ctx, st, k_sweep_record, 1, 32, 0, ctx->ld, l, ctx->sw_status, ctx->sw_nit, ctx->sw_kit,
+                  ctx->sw_ft);
+    } else {
+      const double t0 = t_grid[l], t1 = t_grid[l + 1];
+      const int ns = nsteps[l];
+      PINT_TRY(ctx->D == 2 ? Impl<2>::propagate(ctx, 1, x + l * n, cn, &t0, &t1, &ns, k, theta0, no, ko,
+                                                &h_nit[l], &h_kit[l], &h_status[l], &h_ft[l], st)
+                           : Impl<3>::propagate(ctx, 1, x + l * n, cn, &t0, &t1, &ns, k, theta0, no, ko,
+                                                &h_nit[l], &h_kit[l], &h_status[l], &h_ft[l], st));
+    }
     PINT_CHECK(cudaMemcpyAsync(cn, ctx->ystate, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     if (f_old)
       correct_dev(ctx, l, cn, f_old + l * n, c_old + l * n, x_prev + (l + 1) * n, x + (l + 1) * n, variant, lo, hi,
@@ -1711,19 +1760,12 @@ int coarse_sweep(pint_ctx* ctx, int L, double* x, const double* x_prev, double* 
   for (int l = 0; l < L; ++l) {
     if (theta_out) theta_out[l] = f_old ? h[l] : 1.0;
     if (corr_out) corr_out[l] = f_old ? h[cap + l] : 0.0;
-    if (fail_t) fail_t[l] = h[2 * cap + l];
-    if (status_out) status_out[l] = hn[l];
-    if (newton_iters) newton_iters[l] = hn[cap + l];
-    if (krylov_iters) krylov_iters[l] = hn[2 * cap + l];
+    if (fail_t) fail_t[l] = dev_loop ? h[2 * cap + l] : h_ft[l];
+    if (status_out) status_out[l] = dev_loop ? hn[l] : h_status[l];
+    if (newton_iters) newton_iters[l] = dev_loop ? hn[cap + l] : h_nit[l];
+    if (krylov_iters) krylov_iters[l] = dev_loop ? hn[2 * cap + l] : h_kit[l];
   }
   return PINT_OK;
-}
-
-// the device-driven loop covers every option except the diagnostics that need
-// the host in the loop (per-iteration trace, CUDA-event profiling) and the
-// A/B variants kept for measurement (split norm, fused Arnoldi kernel)
-bool use_device_loop(const pint_ctx* ctx) {
-  return ctx->device_loop && !ctx->prof && !ctx->verbose && !ctx->split_norm && !ctx->use_fused;
 }
 
 }  // namespace
@@ -1947,6 +1989,8 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
       }
   }
   ctx->device_loop = !(std::getenv("PINT_DEVICE_LOOP") && std::getenv("PINT_DEVICE_LOOP")[0] == '0');
+  if (const char* e = std::getenv("PINT_GATE")) ctx->gate = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PINT_GATE0")) ctx->gate0 = std::max(0, std::atoi(e));
   if (cudaMallocHost(&ctx->h_dbl, sizeof(double) * S) != cudaSuccess ||
       cudaMallocHost(&ctx->h_int, sizeof(int) * S) != cudaSuccess ||
       cudaMallocHost(&ctx->h_cap, sizeof(int)) != cudaSuccess ||
@@ -2280,11 +2324,6 @@ int pint_coarse_sweep(pint_ctx* ctx, int32_t L, double* x, const double* x_prev,
       return PINT_INVALID_ARG;
     }
   std::lock_guard<std::mutex> lock(ctx->mu);
-  if (!use_device_loop(ctx)) {
-    ctx->err = "pint_coarse_sweep needs the device-driven loop (PINT_DEVICE_LOOP=0, profiling or a host-only A/B "
-               "switch is active)";
-    return PINT_INVALID_ARG;
-  }
   StreamGuard guard(ctx, stream);
   return coarse_sweep(ctx, L, x, x_prev, c_new, c_old, f_old, t_grid, nsteps, k, theta0, newton, krylov, variant,
                       clamp_lo, clamp_hi, theta_out, corr_out, newton_iters, krylov_iters, status, fail_t,
