@@ -86,6 +86,13 @@ typedef struct pint_krylov_opts {
 /* ---- lifetime -------------------------------------------------------- */
 /* restart <= 31 (the CGS kernel keeps one accumulator per basis vector in registers) */
 int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out);
+/* flags: PINT_CTX_MATRIX_FREE -- no block-stencil Jacobian and no multigrid
+ * hierarchy are allocated (the c5 roofline sweep at 1e6 cells x 32 / 64
+ * slices); residual, J w and the matrix-free linear solve work, every call
+ * that needs the Jacobian or the preconditioner returns PINT_INVALID_ARG. */
+enum { PINT_CTX_MATRIX_FREE = 1 };
+int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, int32_t flags,
+                   pint_ctx** out);
 int pint_destroy(pint_ctx* ctx);
 const char* pint_last_error(const pint_ctx* ctx);
 /* nn nodes, np padded stride, C dofs/node, number of multigrid levels */
@@ -137,6 +144,13 @@ int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, voi
  * equal the context's restart length (PINT_INVALID_ARG otherwise). */
 int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, const pint_krylov_opts* krylov,
                       int32_t* its, double* resid, void* stream);
+
+/* matrix-free GMRES solve J(y) x = b (operator by the K2' J w kernel at the
+ * linearisation point y / y_old with per-slice step data k, theta, t1; no
+ * preconditioner); works on matrix-free and assembled contexts */
+int pint_linear_solve_mf(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                         const double* theta, const double* t1, const double* b, double* x,
+                         const pint_krylov_opts* krylov, int32_t* its, double* resid, void* stream);
 
 /* ---- profiling (bench.py) --------------------------------------------
  * enable: resets the counters; 1 = count launches only (CUDA-graph replay

@@ -382,13 +382,15 @@ def _dirichlet(mesh: Mesh, t1: float):
     return fixed.reshape(-1), g.reshape(-1)
 
 
-def residual(problem: FSIProblem, y, y_old, k: float, theta: float, t1: float):
+def residual(problem: FSIProblem, y, y_old, k: float, theta: float, t1: float, admissible_only: bool = True):
     """Global CN residual R(y; y_old) at t1 = t0 + k; +inf if the trial mesh
-    is inadmissible (J <= 0 at a quadrature point)."""
+    is inadmissible (J <= 0 at a quadrature point), the line-search back-off
+    of integrators.py:83-90.  ``admissible_only=False`` returns the raw
+    assembled residual anyway (kernel parity on tangled random inputs)."""
     mesh = build_mesh(problem)
     y = np.asarray(y, dtype=np.float64)
     Re, jmin = element_residual(mesh, _gather(mesh, y), _gather(mesh, y_old), k, theta)
-    if np.any(jmin <= 0.0):
+    if admissible_only and np.any(jmin <= 0.0):
         return np.full(y.size, np.inf)
     Re = Re * _row_mask(mesh)
     P = problem
@@ -399,6 +401,13 @@ def residual(problem: FSIProblem, y, y_old, k: float, theta: float, t1: float):
     fixed, g = _dirichlet(mesh, t1)
     r[fixed] = y[fixed] - g[fixed]
     return r
+
+
+def degenerate(problem: FSIProblem, y, y_old, k: float, theta: float) -> bool:
+    """True when the trial mesh of y is inadmissible (J <= 0 at a quadrature point)."""
+    mesh = build_mesh(problem)
+    _, jmin = element_residual(mesh, _gather(mesh, np.asarray(y, dtype=np.float64)), _gather(mesh, y_old), k, theta)
+    return bool(np.any(jmin <= 0.0))
 
 
 _CSTEP = 1e-30

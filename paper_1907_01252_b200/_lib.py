@@ -32,12 +32,14 @@ STATUS_NAMES = {
 
 # every symbol include/pint_b200.h declares (tests check the export table)
 EXPORTS = (
-    "pint_create", "pint_destroy", "pint_last_error", "pint_sizes", "pint_level0_fp32", "pint_flags",
+    "pint_create", "pint_create_ex", "pint_destroy", "pint_last_error", "pint_sizes", "pint_level0_fp32", "pint_flags",
     "pint_propagate", "pint_residual", "pint_jvp", "pint_assemble", "pint_jacobian_blocks",
     "pint_spmv", "pint_precond_setup", "pint_precond_apply", "pint_linear_solve",
     "pint_parareal_precorrect", "pint_parareal_correct_one", "pint_profile", "pint_profile_read",
-    "pint_profile_kernel", "pint_coarse_sweep", "pint_boundary_error",
+    "pint_profile_kernel", "pint_coarse_sweep", "pint_boundary_error", "pint_linear_solve_mf",
 )
+
+PINT_CTX_MATRIX_FREE = 1
 
 
 class ProblemDesc(ctypes.Structure):
@@ -93,6 +95,9 @@ _IP = ctypes.POINTER(ctypes.c_int32)
 
 _SIGNATURES = {
     "pint_create": (_I, [ctypes.POINTER(ProblemDesc), _I, _I, ctypes.POINTER(_P)]),
+    "pint_create_ex": (_I, [ctypes.POINTER(ProblemDesc), _I, _I, _I, ctypes.POINTER(_P)]),
+    "pint_linear_solve_mf": (_I, [_P, _I, _P, _P, _DP, _DP, _DP, _P, _P, ctypes.POINTER(KrylovOpts), _IP, _DP,
+                                  _P]),
     "pint_destroy": (_I, [_P]),
     "pint_last_error": (ctypes.c_char_p, [_P]),
     "pint_sizes": (_I, [_P, _IP, _IP, _IP, _IP]),

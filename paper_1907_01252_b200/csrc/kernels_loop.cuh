@@ -300,6 +300,16 @@ __global__ void k_gmres_prep(double* __restrict__ b, double* __restrict__ x, dou
   }
 }
 
+// u = b - u (matrix-free true residual: u held J x)
+__global__ void k_bsub(double* __restrict__ u, const double* __restrict__ b, size_t per_slice,
+                       const int* __restrict__ active) {
+  pdl_wait();
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slice; i += (size_t)gridDim.x * blockDim.x)
+    u[s * per_slice + i] = b[s * per_slice + i] - u[s * per_slice + i];
+}
+
 // y = y_trial, r = r_trial on the slices whose trial is accepted (running, finite norm)
 __global__ void k_accept_copy(double* __restrict__ y, const double* __restrict__ yt, double* __restrict__ r,
                               const double* __restrict__ rt, size_t per_slice, const int* __restrict__ running,

@@ -94,7 +94,7 @@ struct pint_ctx {
   double *ystate = nullptr, *ynew = nullptr, *r = nullptr, *dx = nullptr, *ytrial = nullptr, *rtrial = nullptr,
          *b = nullptr;
   // GMRES
-  double *V = nullptr, *H = nullptr, *gv = nullptr, *cs = nullptr, *sn = nullptr, *ybuf = nullptr, *z = nullptr,
+  double *V = nullptr, *H = nullptr, *gv = nullptr, *cs = nullptr, *sn = nullptr, *ybuf = nullptr,
          *w = nullptr, *u = nullptr, *gm_res = nullptr, *gm_tol = nullptr, *gm_beta = nullptr;
   int *gm_active = nullptr, *gm_steps = nullptr, *gm_its = nullptr, *cyc_active = nullptr;
   int* gm_two_pass = nullptr;  // per slice: second Gram-Schmidt pass in this solve
@@ -164,6 +164,11 @@ struct pint_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   pint_krylov_opts kopt{};
+  // matrix-free context (pint_create_ex, PINT_CTX_MATRIX_FREE): no Jacobian,
+  // no multigrid hierarchy; GMRES on J(y) w by the K2' kernel, unpreconditioned
+  bool matrix_free = false;
+  const double* mf_y = nullptr;   // linearisation point of the running matrix-free solve
+  const double* mf_yo = nullptr;
   int* gm_cap = nullptr;        // Krylov budget of the running solve (givens_one)
   int* h_cap = nullptr;         // pinned
   // ---- device-driven control flow (Impl::propagate_dev): the whole
@@ -829,6 +834,10 @@ struct Impl {
     const size_t vstride = (size_t)ctx->maxS * vs(ctx);
     double* vj = ctx->V + j * vstride;
     double* zj = ctx->Z + j * vstride;
+    if (ctx->matrix_free) {  // z_j = v_j (Z aliases V), w = J(y) v_j by the K2' kernel
+      jvp(ctx, S, ctx->mf_y, ctx->mf_yo, vj, ctx->w, st);
+      return false;
+    }
     // v_j = w / h_{j,j-1} deferred into the first smoothing sweep of this
     // step's V-cycle (level 0 outside the tail, fused 2-d Vanka sweep)
     const bool defer = ctx->defer_scale && ctx->kopt.smoother == 1 && !ctx->vanka_split && ctx->tail_first != 0 &&
@@ -1004,7 +1013,7 @@ struct Impl {
 
   static int run_arnoldi(pint_ctx* ctx, int S, int j, cudaStream_t st) {
     if (ctx->fused && (!ctx->use_graphs || ctx->prof)) return launch_fused(ctx, S, j, st);
-    if (!ctx->use_graphs || ctx->prof) {
+    if (!ctx->use_graphs || ctx->prof || ctx->matrix_free) {
       arnoldi_step(ctx, S, j, st);
       PINT_LAUNCHED();
       return PINT_OK;
@@ -1124,7 +1133,10 @@ struct Impl {
                                                  ctx->cyc_active);
       pint_launch(ctx, st, k_axpy_one, vec_grid(n, S), 256, 0, x, ctx->u, n, ctx->cyc_active);
       // true residual r = b - J x into ctx->u (reused as cycle start)
-      if (wide(ctx->g.nn, S))
+      if (ctx->matrix_free) {
+        PINT_TRY(jvp(ctx, S, ctx->mf_y, ctx->mf_yo, x, ctx->u, st));
+        pint_launch(ctx, st, k_bsub, vec_grid(n, S), 256, 0, ctx->u, b, n, (const int*)ctx->cyc_active);
+      } else if (wide(ctx->g.nn, S))
         pint_launch(ctx, st, k_spmv<D, true, 3>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
       else
         pint_launch(ctx, st, k_spmv<D, true, 9>, row_grid(ctx->g.nn, S), row_block<D>(), 0, ctx->g, ctx->lv[0].A, x, b, ctx->u, ctx->cyc_active);
@@ -1487,6 +1499,12 @@ int check_S(pint_ctx* ctx, int S) {
 }
 
 // ---------------------------------------------------------------- device-driven propagate (host side)
+int mf_reject(pint_ctx* ctx, const char* what) {
+  ctx->err = std::string(what) + " needs the Jacobian / multigrid hierarchy, which a matrix-free context "
+                                 "(PINT_CTX_MATRIX_FREE) does not hold";
+  return PINT_INVALID_ARG;
+}
+
 // the device-driven loop covers every option except the diagnostics that need
 // the host in the loop (per-iteration trace, CUDA-event profiling) and the
 // A/B variants kept for measurement (split norm, fused Arnoldi kernel)
@@ -1775,7 +1793,13 @@ int coarse_sweep(pint_ctx* ctx, int L, double* x, const double* x_prev, double* 
 extern "C" {
 
 int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, pint_ctx** out) {
+  return pint_create_ex(desc, max_slices, restart, 0, out);
+}
+
+int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t restart, int32_t flags,
+                   pint_ctx** out) {
   if (!desc || !out || max_slices < 1 || restart < 1 || restart + 1 > kMdotMax) return PINT_INVALID_ARG;
+  if (flags & ~PINT_CTX_MATRIX_FREE) return PINT_INVALID_ARG;
   if (desc->dim != 2 && desc->dim != 3) return PINT_INVALID_ARG;
   for (int m = 0; m < desc->dim; ++m)
     if (desc->cells[m] < 1) return PINT_INVALID_ARG;
@@ -1786,6 +1810,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ctx->C = 2 * desc->dim + 1;
   ctx->maxS = max_slices;
   ctx->restart = restart;
+  ctx->matrix_free = (flags & PINT_CTX_MATRIX_FREE) != 0;
   ctx->verbose = std::getenv("PINT_VERBOSE") && std::getenv("PINT_VERBOSE")[0] == '1';
   ctx->use_graphs = !(std::getenv("PINT_GRAPHS") && std::getenv("PINT_GRAPHS")[0] == '0');
   ctx->use_tail = !(std::getenv("PINT_TAIL") && std::getenv("PINT_TAIL")[0] == '0');
@@ -1863,12 +1888,13 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
     Level L;
     L.g = make_grid(ctx->D, cl);
     ctx->lv.push_back(L);
+    if (ctx->matrix_free) break;  // no hierarchy: level 0's grid only, nothing allocated
     bool even = true;
     for (int m = 0; m < ctx->D; ++m) even = even && (cl[m] % 2 == 0) && cl[m] >= 2;
     if (!even) break;
     for (int m = 0; m < ctx->D; ++m) cl[m] /= 2;
   }
-  for (size_t l = 0; l < ctx->lv.size(); ++l) {
+  for (size_t l = 0; l < (ctx->matrix_free ? 0 : ctx->lv.size()); ++l) {
     Level& L = ctx->lv[l];
     const size_t np = L.g.np;
     ALLOC(L.A, (size_t)S * L.g.noff * C * C * np);
@@ -1891,8 +1917,10 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // the coarsest and that still fits kDenseMax dofs
   ctx->dense_cap = 0;
   for (const Level& L : ctx->lv)
+    if (ctx->matrix_free) break;
+    else
     if (C * L.g.nn <= kDenseMax) ctx->dense_cap = std::max(ctx->dense_cap, C * L.g.nn);
-  if (ctx->dense_cap == 0 && C * Lc.g.nn <= kDenseMax) ctx->dense_cap = C * Lc.g.nn;
+  if (!ctx->matrix_free && ctx->dense_cap == 0 && C * Lc.g.nn <= kDenseMax) ctx->dense_cap = C * Lc.g.nn;
   if (ctx->dense_cap > 0) {
     ALLOC(ctx->d_dense, (size_t)S * ctx->dense_cap * 2 * ctx->dense_cap);
     ALLOC(ctx->d_dense32, (size_t)S * ctx->dense_cap * ((ctx->dense_cap + 3) / 4 * 4));
@@ -1907,8 +1935,8 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   ALLOC(ctx->b, S * vsz);
   const int m = restart;
   ALLOC(ctx->V, (size_t)(m + 1) * S * vsz);
-  ALLOC(ctx->z, S * vsz);
-  ALLOC(ctx->Z, (size_t)m * S * vsz);
+  if (ctx->matrix_free) ctx->Z = ctx->V;  // no preconditioner: z_j = v_j
+  else ALLOC(ctx->Z, (size_t)m * S * vsz);
   ALLOC(ctx->w, S * vsz);
   ALLOC(ctx->u, S * vsz);
   ALLOC(ctx->H, (size_t)S * (m + 1) * m);
@@ -1942,7 +1970,7 @@ int pint_create(const pint_problem_desc* desc, int32_t max_slices, int32_t resta
   // optional fp32 copy of the level-0 operator for the V-cycle residuals (half
   // the bytes of the two level-0 SpMVs of every cycle); skipped when it does
   // not fit next to the rest of the workspace (or with PINT_A32=0)
-  if (!(std::getenv("PINT_A32") && std::getenv("PINT_A32")[0] == '0')) {
+  if (!ctx->matrix_free && !(std::getenv("PINT_A32") && std::getenv("PINT_A32")[0] == '0')) {
     Level& L0 = ctx->lv[0];
     const size_t cnt = (size_t)S * L0.g.noff * C * C * L0.g.np;
     size_t free_b = 0, total_b = 0;
@@ -2152,6 +2180,7 @@ int pint_propagate(pint_ctx* ctx, int32_t S, const double* y_in, double* y_out, 
                std::to_string(ctx->restart);
     return PINT_INVALID_ARG;
   }
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_propagate");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   cudaStream_t st = ctx->stream;
@@ -2191,6 +2220,7 @@ int pint_assemble(pint_ctx* ctx, int32_t S, const double* y, const double* y_old
                   const double* theta, const double* t1, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_assemble");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   cudaStream_t st = ctx->stream;
@@ -2201,6 +2231,7 @@ int pint_assemble(pint_ctx* ctx, int32_t S, const double* y, const double* y_old
 int pint_jacobian_blocks(pint_ctx* ctx, int32_t S, double* out, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_jacobian_blocks");
   std::lock_guard<std::mutex> lock(ctx->mu);
   const size_t ms = (size_t)ctx->g.noff * ctx->C * ctx->C * ctx->g.np;
   StreamGuard guard(ctx, stream);
@@ -2211,6 +2242,7 @@ int pint_jacobian_blocks(pint_ctx* ctx, int32_t S, double* out, void* stream) {
 int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_spmv");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   DISPATCH(spmv(ctx, 0, S, x, y, nullptr, ctx->stream));
@@ -2221,6 +2253,7 @@ int pint_spmv(pint_ctx* ctx, int32_t S, const double* x, double* y, void* stream
 int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_precond_setup");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   return DISPATCH(precond_setup(ctx, S, krylov, nullptr, ctx->stream));
@@ -2229,6 +2262,7 @@ int pint_precond_setup(pint_ctx* ctx, int32_t S, const pint_krylov_opts* krylov,
 int pint_precond_apply(pint_ctx* ctx, int32_t S, const double* b, double* x, void* stream) {
   int rc = check_S(ctx, S);
   if (rc) return rc;
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_precond_apply");
   std::lock_guard<std::mutex> lock(ctx->mu);
   if (ctx->prec_levels == 0) {
     ctx->err = "pint_precond_apply before pint_precond_setup";
@@ -2249,9 +2283,42 @@ int pint_linear_solve(pint_ctx* ctx, int32_t S, const double* b, double* x, cons
                std::to_string(ctx->restart);
     return PINT_INVALID_ARG;
   }
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_linear_solve");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   return DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, nullptr, nullptr, its, resid, ctx->stream));
+}
+
+int pint_linear_solve_mf(pint_ctx* ctx, int32_t S, const double* y, const double* y_old, const double* k,
+                         const double* theta, const double* t1, const double* b, double* x,
+                         const pint_krylov_opts* krylov, int32_t* its, double* resid, void* stream) {
+  int rc = check_S(ctx, S);
+  if (rc) return rc;
+  if (!y || !y_old || !k || !theta || !t1 || !b || !x || !krylov) {
+    ctx->err = "invalid argument to pint_linear_solve_mf";
+    return PINT_INVALID_ARG;
+  }
+  if (krylov->restart != ctx->restart) {
+    ctx->err = "krylov restart " + std::to_string(krylov->restart) + " differs from the context's restart length " +
+               std::to_string(ctx->restart);
+    return PINT_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  StreamGuard guard(ctx, stream);
+  cudaStream_t st = ctx->stream;
+  if ((rc = upload_steps(ctx, S, k, theta, t1, st))) return rc;
+  // an assembled context solves matrix-free too, with its preconditioner off
+  const bool was_mf = ctx->matrix_free;
+  ctx->matrix_free = true;
+  ctx->mf_y = y;
+  ctx->mf_yo = y_old;
+  double* Zsave = ctx->Z;
+  ctx->Z = ctx->V;
+  rc = DISPATCH(gmres(ctx, S, b, x, nullptr, krylov, nullptr, nullptr, its, resid, st));
+  ctx->Z = Zsave;
+  ctx->matrix_free = was_mf;
+  ctx->mf_y = ctx->mf_yo = nullptr;
+  return rc;
 }
 
 int pint_parareal_precorrect(int32_t S, int32_t C, int32_t nn, int32_t np, const double* f_old,
@@ -2323,6 +2390,7 @@ int pint_coarse_sweep(pint_ctx* ctx, int32_t L, double* x, const double* x_prev,
       ctx->err = "pint_coarse_sweep: time grid must be non-decreasing with non-negative step counts";
       return PINT_INVALID_ARG;
     }
+  if (ctx->matrix_free) return mf_reject(ctx, "pint_coarse_sweep");
   std::lock_guard<std::mutex> lock(ctx->mu);
   StreamGuard guard(ctx, stream);
   return coarse_sweep(ctx, L, x, x_prev, c_new, c_old, f_old, t_grid, nsteps, k, theta0, newton, krylov, variant,

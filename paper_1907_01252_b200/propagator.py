@@ -188,15 +188,17 @@ class FSIDevice:
     up to ``max_slices`` batched slices.  Calls are serialized by the
     library's context mutex; ctypes releases the GIL during them."""
 
-    def __init__(self, problem: FSIProblem, max_slices: int, restart: int = 30):
+    def __init__(self, problem: FSIProblem, max_slices: int, restart: int = 30, matrix_free: bool = False):
         _require_cuda()
         self.lib = _lib.load()
         self.problem = problem
         self.max_slices = int(max_slices)
         self.restart = int(restart)
+        self.matrix_free = bool(matrix_free)  # no Jacobian / hierarchy: residual, J w, linear_solve_mf only
         handle = ctypes.c_void_p()
         desc = problem_desc(problem)
-        rc = self.lib.pint_create(ctypes.byref(desc), self.max_slices, self.restart, ctypes.byref(handle))
+        rc = self.lib.pint_create_ex(ctypes.byref(desc), self.max_slices, self.restart,
+                                     _lib.PINT_CTX_MATRIX_FREE if self.matrix_free else 0, ctypes.byref(handle))
         if rc != _lib.PINT_OK:
             msg = self.lib.pint_last_error(handle).decode() if handle else "allocation failed"
             if handle:
@@ -298,6 +300,18 @@ class FSIDevice:
         res = (ctypes.c_double * S)()
         self.check(self.lib.pint_linear_solve(self.handle, S, _ptr(b), _ptr(out), ctypes.byref(ko), its, res,
                                               _stream()), "pint_linear_solve")
+        return out, np.array(its[:]), np.array(res[:])
+
+    def linear_solve_mf(self, y, y_old, k, theta, t1, b, krylov: KrylovSettings, out=None):
+        """Unpreconditioned GMRES on J(y) x = b with the matrix-free K2' operator."""
+        S = b.shape[0]
+        out = out if out is not None else self.empty(S)
+        ko = krylov.c_struct()
+        its = (ctypes.c_int32 * S)()
+        res = (ctypes.c_double * S)()
+        self.check(self.lib.pint_linear_solve_mf(self.handle, S, _ptr(y), _ptr(y_old), _darr(k), _darr(theta),
+                                                 _darr(t1), _ptr(b), _ptr(out), ctypes.byref(ko), its, res,
+                                                 _stream()), "pint_linear_solve_mf")
         return out, np.array(its[:]), np.array(res[:])
 
     def profile(self, mode: int):

@@ -2,6 +2,7 @@
 
   python tests/golden/make_config_fixtures.py c3          # one config
   python tests/golden/make_config_fixtures.py c5_1e5      # kernel fixture only
+  python tests/golden/make_config_fixtures.py --kernel c3 # redo the kernel part of an existing fixture
 
 For a time-loop config (c2, c3, c4) the fixture holds
   * ``starts[j]``  -- the oracle's coarse-initialised boundary state X0[l_j]
@@ -13,7 +14,10 @@ For a time-loop config (c2, c3, c4) the fixture holds
     (integrators.py:144-166 bookkeeping, the fine task of parareal.py:417-421);
   * ``r`` / ``jw`` -- residual R(y; y_old) and exact J(y) w at seeded c5-type
     inputs on the config's mesh (seeds stored; the inputs are regenerated
-    with ``problem.c5_random_states``), the K1 / K2' kernel fixtures.
+    with ``problem.c5_random_states``), the K1 / K2' kernel fixtures.  The
+    BASELINE c5 deformation N(0, 1e-3^2) tangles the finer meshes (J <= 0 at
+    some points); ``degenerate`` records that, and ``r`` is then the raw
+    assembled residual (the propagator would treat it as +inf).
 
 The GPU tests (tests/test_gpu_configs.py) and bench.py's parity field and
 reference arm read these files; nothing here runs on the GPU box.
@@ -33,7 +37,7 @@ from paper_1907_01252_b200.problem import CONFIGS, c5_problem, c5_random_states 
 
 NEWTON = O.OracleNewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
 SAMPLES = 8          # sample slices with stored start states (reference arm)
-PARITY = 2           # of which the first PARITY also store fine endpoints
+PARITY = 2           # of which the last PARITY also store fine endpoints
 FINE_STEPS = 4
 SEEDS = (101, 102, 103)   # y, y_old, w of the kernel fixture
 KT1 = (2.0 ** -10, 0.3)   # step and time of the kernel fixture (theta = 1/2 + k)
@@ -43,9 +47,9 @@ def kernel_fixture(P):
     Y, Yo, W = (c5_random_states(P, 1, sd)[0] for sd in SEEDS)
     k, t1 = KT1
     th = 0.5 + k
-    r = O.residual(P, Y, Yo, k, th, t1)
+    r = O.residual(P, Y, Yo, k, th, t1, admissible_only=False)
     J = O.jacobian(P, Y, Yo, k, th, t1)
-    return r, J @ W
+    return r, J @ W, O.degenerate(P, Y, Yo, k, th)
 
 
 def sample_slices(L):
@@ -57,9 +61,9 @@ def main(name):
     t_start = time.time()
     if name.startswith("c5_"):
         P = c5_problem(name[3:])
-        r, jw = kernel_fixture(P)
+        r, jw, dg = kernel_fixture(P)
         out = os.path.join(HERE, f"config_{name}.npz")
-        np.savez_compressed(out, r=r, jw=jw, seeds=np.array(SEEDS), kt1=np.array(KT1))
+        np.savez_compressed(out, r=r, jw=jw, degenerate=dg, seeds=np.array(SEEDS), kt1=np.array(KT1))
         print(out, f"{time.time() - t_start:.1f} s")
         return
     cfg = CONFIGS[name]
@@ -84,9 +88,9 @@ def main(name):
         n0 = F.newton_iterations
         ends.append(F.advance_values(starts[l], t0, t0 + FINE_STEPS * cfg.fine_step))
         fine_newton.append(F.newton_iterations - n0)
-    r, jw = kernel_fixture(P)
+    r, jw, dg = kernel_fixture(P)
     out = os.path.join(HERE, f"config_{name}.npz")
-    np.savez_compressed(out, slices=np.array(slices), starts=np.array([starts[l] for l in slices]),
+    np.savez_compressed(out, degenerate=dg, slices=np.array(slices), starts=np.array([starts[l] for l in slices]),
                         parity_slices=np.array(slices[-PARITY:]), ends=np.array(ends),
                         fine_steps=FINE_STEPS, fine_newton=np.array(fine_newton),
                         coarse_newton=C.newton_iterations, r=r, jw=jw, seeds=np.array(SEEDS),
@@ -94,6 +98,20 @@ def main(name):
     print(out, f"{time.time() - t_start:.1f} s")
 
 
+def redo_kernel(name):
+    """Recompute r / jw / degenerate of an existing fixture (the rest is kept)."""
+    out = os.path.join(HERE, f"config_{name}.npz")
+    g = dict(np.load(out))
+    P = c5_problem(name[3:]) if name.startswith("c5_") else CONFIGS[name].problem
+    g["r"], g["jw"], g["degenerate"] = kernel_fixture(P)
+    np.savez_compressed(out, **g)
+    print(out, "kernel part redone; degenerate =", bool(g["degenerate"]))
+
+
 if __name__ == "__main__":
-    for n in sys.argv[1:]:
-        main(n)
+    if sys.argv[1] == "--kernel":
+        for n in sys.argv[2:]:
+            redo_kernel(n)
+    else:
+        for n in sys.argv[1:]:
+            main(n)

@@ -78,3 +78,38 @@ def test_c5_1e5_properties(cuda):
     dev.precond_setup(1, ks)
     v1 = dev.precond_apply(w1[one].contiguous())
     assert torch.equal(r1[0], r3[1]) and torch.equal(s1[0], s3[1]) and torch.equal(v1[0], v3[1])
+
+
+def test_matrix_free_context_and_solve(cuda):
+    """PINT_CTX_MATRIX_FREE: no Jacobian / hierarchy allocated; residual and
+    J w match an assembled context bitwise; the unpreconditioned matrix-free
+    GMRES solves J x = b (checked against the oracle's sparse J); calls that
+    need the hierarchy are refused."""
+    from paper_1907_01252_b200.propagator import DeviceError, FSIDevice, KrylovSettings
+    P = c5_problem("1e4")
+    S = 2
+    full, lean = FSIDevice(P, S, restart=30), FSIDevice(P, S, restart=30, matrix_free=True)
+    Y, Yo, W = (0.1 * c5_random_states(P, S, sd) for sd in (21, 22, 23))
+    k, th, t1 = _args(S)
+    for name in ("residual", "jvp"):
+        a = [full.to_device(v) for v in (Y, Yo, W)]
+        b = [lean.to_device(v) for v in (Y, Yo, W)]
+        if name == "residual":
+            ra, _ = full.residual(a[0], a[1], k, th, t1)
+            rb, _ = lean.residual(b[0], b[1], k, th, t1)
+        else:
+            ra = full.jvp(a[0], a[1], a[2], k, th, t1)
+            rb = lean.jvp(b[0], b[1], b[2], k, th, t1)
+        assert full.to_host(ra).tobytes() == lean.to_host(rb).tobytes()
+    y, yo, rhs = lean.to_device(Y), lean.to_device(Yo), lean.to_device(W)
+    x, its, res = lean.linear_solve_mf(y, yo, k, th, t1, rhs, KrylovSettings(rtol=1e-8, max_iters=60))
+    xh = lean.to_host(x)
+    for s in range(S):
+        # the reported residual is the true ||b - J x|| of the matrix-free operator: equal to the
+        # oracle's sparse-J residual of the returned x, and reduced by the Krylov iterations
+        J = O.jacobian(P, Y[s], Yo[s], k[s], th[s], t1[s])
+        true = np.linalg.norm(W[s] - J @ xh[s])
+        assert abs(true - res[s]) <= 1e-8 * np.linalg.norm(W[s]), (s, its[s], res[s], true)
+        assert res[s] < 0.5 * np.linalg.norm(W[s]) and its[s] == 60
+    with pytest.raises(DeviceError, match="matrix-free"):
+        lean.assemble(y, yo, k, th, t1)

@@ -1,0 +1,109 @@
+"""GPU parity at every BASELINE time-loop config (c2 64x16, c3 256x64 with the
+stiff solid mu_s = 2e6, c4 40x8x8) and the c5 1e5-cell kernel mesh, against
+oracle fixtures (tests/golden/config_<c>.npz, made by
+tests/golden/make_config_fixtures.py from oracle/fsi_oracle.py):
+
+* K1 residual and K2 (assembled J and matrix-free J w) at seeded c5-type
+  inputs on the config's mesh: relative L2 <= 1e-12;
+* the fine propagator over 4 shifted-CN steps from the oracle's own
+  coarse-initialised start states of the last sample slices: per-slice
+  endpoint velocity / deformation / pressure to relative L2 <= 1e-6 (the
+  north-star bar);
+* the GPU coarse initialisation (pint_coarse_sweep) against the oracle's at
+  the sample slices (same physics, same coarse steps): relative L2 <= 1e-6.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from fields import field_errors
+from paper_1907_01252_b200.problem import CONFIGS, c5_problem, c5_random_states
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _fixture(name):
+    path = os.path.join(GOLD, f"config_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {path} not generated")
+    return np.load(path)
+
+
+def _problem(name):
+    return c5_problem(name[3:]) if name.startswith("c5_") else CONFIGS[name].problem
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5_1e5"])
+def test_residual_and_jacobian_match_oracle_fixture(cuda, name):
+    from paper_1907_01252_b200.propagator import FSIDevice
+    g = _fixture(name)
+    P = _problem(name)
+    Y, Yo, W = (c5_random_states(P, 1, int(sd)) for sd in g["seeds"])
+    k, t1 = (float(v) for v in g["kt1"])
+    dev = FSIDevice(P, 1)
+    y, yo, w = dev.to_device(Y), dev.to_device(Yo), dev.to_device(W)
+    r, norms = dev.residual(y, yo, [k], [0.5 + k], [t1])
+    r = dev.to_host(r)[0]
+    assert np.linalg.norm(r - g["r"]) <= 1e-12 * np.linalg.norm(g["r"])
+    if bool(g["degenerate"]):
+        # tangled random mesh (J <= 0 somewhere): the residual norm is +inf,
+        # the line-search back-off signal (integrators.py:83-90)
+        assert norms[0] == np.inf
+    else:
+        assert abs(norms[0] - np.linalg.norm(g["r"])) <= 1e-12 * np.linalg.norm(g["r"])
+    jw = dev.to_host(dev.jvp(y, yo, w, [k], [0.5 + k], [t1]))[0]
+    assert np.linalg.norm(jw - g["jw"]) <= 1e-12 * np.linalg.norm(g["jw"])
+    dev.assemble(y, yo, [k], [0.5 + k], [t1])
+    aw = dev.to_host(dev.spmv(w))[0]
+    assert np.linalg.norm(aw - g["jw"]) <= 1e-12 * np.linalg.norm(g["jw"])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_fine_endpoints_match_oracle_fixture(cuda, name):
+    """4 fine CN steps from the oracle's start states, both parity slices in
+    one batch: per-field relative L2 <= 1e-6."""
+    from paper_1907_01252_b200.propagator import NewtonSettings, ThetaSettings, make_propagator
+    g = _fixture(name)
+    cfg = CONFIGS[name]
+    P = cfg.problem
+    slices = [int(l) for l in g["parity_slices"]]
+    idx = [list(g["slices"]).index(l) for l in slices]
+    F = make_propagator(P, ThetaSettings(cfg.fine_step, cfg.theta0, NewtonSettings(1e-10, 1e-10)),
+                        max_slices=len(slices))
+    dev = F.device
+    steps = int(g["fine_steps"])
+    t0 = [l * cfg.window for l in slices]
+    out = dev.to_host(F.advance_device(dev.to_device([g["starts"][j] for j in idx]), t0,
+                                       [t + steps * cfg.fine_step for t in t0]))
+    for s in range(len(slices)):
+        errs = field_errors(P, out[s], g["ends"][s])
+        assert max(errs.values()) <= 1e-6, (name, slices[s], errs)
+    assert F.steps_taken == steps * len(slices)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_coarse_initialisation_matches_oracle_fixture(cuda, name):
+    """The device coarse initialisation (pint_coarse_sweep, f_old = NULL)
+    reproduces the oracle's sequential coarse sweep at the sample slices."""
+    from paper_1907_01252_b200.propagator import NewtonSettings, ThetaSettings, initial_state, make_propagator
+    g = _fixture(name)
+    cfg = CONFIGS[name]
+    P = cfg.problem
+    L = int(max(g["slices"]))
+    C = make_propagator(P, ThetaSettings(cfg.coarse_step, cfg.theta0, NewtonSettings(1e-10, 1e-10)),
+                        max_slices=1)
+    dev = C.device
+    X = dev.empty(L + 1)
+    X[0:1].copy_(dev.to_device(initial_state(P).values))
+    C.sweep(X, [l * cfg.window for l in range(L + 1)], dev.empty(L))
+    got = dev.to_host(X)
+    for j, l in enumerate(int(v) for v in g["slices"]):
+        ref = g["starts"][j]
+        if np.linalg.norm(ref) == 0.0:
+            assert np.linalg.norm(got[l]) == 0.0
+            continue
+        errs = field_errors(P, got[l], ref)
+        assert max(errs.values()) <= 1e-6, (name, l, errs)

@@ -48,12 +48,46 @@ def timed(fn, flush, reps=5):
     return ts[len(ts) // 2]
 
 
+def lean_line(P, size, S, a, pk, pk_kind, flush):
+    """Matrix-free context (PINT_CTX_MATRIX_FREE: no Jacobian, no hierarchy)
+    for the (size, S) whose assembled context exceeds the memory budget: K1,
+    K2' and one unpreconditioned matrix-free GMRES(1) iteration."""
+    nn, C = P.num_nodes, P.dofs_per_node
+    V = C * 8 * nn
+    dev = FSIDevice(P, S, restart=1, matrix_free=True)
+    Y = c5_random_states(P, S, a.seed)
+    Yo = c5_random_states(P, S, a.seed + 1)
+    W = c5_random_states(P, S, a.seed + 2)
+    y, yo, w = dev.to_device(Y), dev.to_device(Yo), dev.to_device(W)
+    del Y, Yo, W
+    k, th, t1 = [2.0 ** -10] * S, [0.5 + 2.0 ** -10] * S, [0.3] * S
+    r, jw, out = dev.empty(S), dev.empty(S), dev.empty(S)
+    krylov = KrylovSettings(rtol=1e-30, max_iters=1, restart=1)
+    res = {"residual": (timed(lambda: dev.residual(y, yo, k, th, t1, out=r), flush), 3 * V),
+           "jvp": (timed(lambda: dev.jvp(y, yo, w, k, th, t1, out=jw), flush), 4 * V),
+           # v0 = b / beta (2V), w = J v0 (4V), <v0, w> (2V), update + norm (3V), x = Z y (2V) + x update (3V),
+           # true residual J x (4V) + b - J x (3V), its norm (V): 24V, plus the initial ||b|| (V)
+           "gmres_iteration_mf": (timed(lambda: dev.linear_solve_mf(y, yo, k, th, t1, w, krylov, out=out), flush),
+                                  25 * V)}
+    line = {"config": "c5", "size": size, "mesh": list(C5_MESHES[size]), "slices": S, "dofs_per_slice": P.num_dofs,
+            "seed": a.seed, "peak_gbs": pk, "peak_kind": pk_kind, "context": "matrix-free (PINT_CTX_MATRIX_FREE)",
+            "kernels": {}}
+    for name, (ms, bytes_per_slice) in res.items():
+        gbs = S * bytes_per_slice / 1e9 / (ms / 1e3)
+        line["kernels"][name] = {"ms": ms, "algorithmic_bytes": S * bytes_per_slice, "GB_s": gbs,
+                                 "frac_of_peak": gbs / pk}
+    print(json.dumps(line), flush=True)
+    del dev
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", nargs="+", default=["1e4", "1e5", "1e6"])
     ap.add_argument("--slices", nargs="+", type=int, default=[1, 2, 4, 8, 16, 32, 64])
     ap.add_argument("--seed", type=int, default=2024)
-    ap.add_argument("--mem-gb", type=float, default=150.0, help="skip (size, S) whose context exceeds this")
+    ap.add_argument("--mem-gb", type=float, default=150.0,
+                    help="(size, S) whose assembled context exceeds this run in a matrix-free context")
     a = ap.parse_args()
     pk, pk_kind = peak()
     fp64_tflops = 36.59  # measured DFMA peak on this pool's B200 (tools/fp64_peak.cu, profiles/)
@@ -68,8 +102,7 @@ def main():
         per_slice_gb = (Ablk * 1.34 + 1.34 * ncell * (400 * 4 + 160) + 40 * V) / 1e9
         for S in a.slices:
             if S * per_slice_gb > a.mem_gb:
-                print(json.dumps({"size": size, "slices": S, "skipped": f"~{S * per_slice_gb:.0f} GB context"}),
-                      flush=True)
+                lean_line(P, size, S, a, pk, pk_kind, flush)
                 continue
             dev = FSIDevice(P, S, restart=1)
             Y = c5_random_states(P, S, a.seed)
