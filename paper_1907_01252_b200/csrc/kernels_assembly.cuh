@@ -295,19 +295,22 @@ struct JacLin {
   static constexpr int NS = 1 + D;               // seeds / test kinds per component
   static constexpr int EPB = D == 2 ? 32 : 8;    // elements per block
   static constexpr int T = EPB * A;              // threads per block
-  static constexpr int OCC = D == 2 ? 4 : 3;     // resident blocks per SM
+  static constexpr int OCC = D == 2 ? 3 : 3;     // resident blocks per SM
   static constexpr int GSZ = C * NS * NS;        // volume entries per (element, point)
   static constexpr int FSZ = D * NS;             // face entries per (element, face point)
   static constexpr int TVSZ = A * A * NS;        // volume shape table
   static constexpr int TFSZ = (A / 2) * A * NS;  // face shape table
-  static constexpr size_t smem = sizeof(double) * ((size_t)(GSZ + FSZ) * T + TVSZ + TFSZ);
+  static constexpr size_t smem = sizeof(double) * ((size_t)(GSZ + FSZ) * T + TVSZ + TFSZ) + sizeof(int) * A * EPB;
+  static_assert(2 * C * A * EPB <= (GSZ + FSZ) * T, "node staging must fit the G region");
+  static_assert((2 * C * A * EPB) % T == 0, "staging loads per thread");
 };
 
 template <int D, int G>
 __device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& st, const ElemIndex<D>& e, int q,
                                              const double* __restrict__ y, const double* __restrict__ yo, int np,
                                              int cp, double* __restrict__ sg, int T, const double* __restrict__ tv,
-                                             const double* __restrict__ tf) {
+                                             const double* __restrict__ tf, const QFields<D, double>& fn,
+                                             const QFields<D, double>& fo) {
   constexpr int A = 1 << D, NS = 1 + D;
   // shape values / gradients of point q from the block's tables ([b][NS])
   auto shape = [&](const double* t, double (&N)[A], double (&dN)[A][D]) {
@@ -323,11 +326,7 @@ __device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& 
   auto gy = [&](int a, int c) { return __ldg(y + c * np + e.node[a]); };
   auto go = [&](int a, int c) { return __ldg(yo + c * np + e.node[a]); };
   {
-    double N[A], dN[A][D];
-    shape(tv + q * A * NS, N, dN);
-    QFields<D, double> fn, fo;
-    interp<D>(N, dN, gy, fn);
-    interp<D>(N, dN, go, fo);
+    // volume point: fields interpolated by the caller from the staged node values
 #pragma unroll 1
     for (int dir = 0; dir < NS; ++dir) {
       typename ST::F fd;
@@ -352,18 +351,18 @@ __device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& 
   }
   constexpr int GSZ = (2 * D + 1) * NS * NS;
   if constexpr (G != 2) {
-   if ((e.cflag & kCellOutflow) && q < (A >> 1)) {
+   if ((e.cflag & kCellOutflow) && q < (A >> 1)) {  // rare (outflow column): gathered from global memory
     double N[A], dN[A][D];
     shape(tf + q * A * NS, N, dN);
-    QFields<D, double> fn, fo;
-    interp<D>(N, dN, gy, fn);
-    interp<D>(N, dN, go, fo);
+    QFields<D, double> gn, gold;
+    interp<D>(N, dN, gy, gn);
+    interp<D>(N, dN, go, gold);
 #pragma unroll 1
     for (int dir = 0; dir < NS; ++dir) {
       typename ST::F fd;
-      seed_dir<D, G>(fn, cp, dir, fd);
+      seed_dir<D, G>(gn, cp, dir, fd);
       Dual B[D];
-      qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, fo, B);
+      qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, gold, B);
 #pragma unroll
       for (int i = 0; i < D; ++i) sg[(GSZ + i * NS + dir) * T] = B[i].d;
     }
@@ -402,19 +401,57 @@ __global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(M
     }
   }
   ElemIndex<D> e;
-  const bool valid = colour_element<D>(m, colour, blockIdx.x * L::EPB + lane / A, e);
+  constexpr int EPB = L::EPB;
+  const int el = lane / A;
+  const bool valid = colour_element<D>(m, colour, blockIdx.x * EPB + el, e);
   const size_t vs = (size_t)C * m.g.np;
   const bool outflow = valid && (e.cflag & kCellOutflow);
-  __syncthreads();  // shape tables
+  const double* ys = y + s * vs;
+  const double* yos = yo + s * vs;
+  // stage the node values of the block's elements ([lvl][c][a][e], in the G
+  // region, which phase 1 overwrites only after the fields are interpolated):
+  // every load of the block in flight at once instead of per-point gathers
+  int* snode = reinterpret_cast<int*>(tf + L::TFSZ);
+  if (q == 0) {
+#pragma unroll
+    for (int a = 0; a < A; ++a) snode[a * EPB + el] = valid ? e.node[a] : -1;
+  }
+  __syncthreads();  // shape tables, node table
+  {
+    constexpr int PER = 2 * C * A * EPB / T;
+    double v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;
+      const int ee = idx % EPB, a = (idx / EPB) % A, c = (idx / (EPB * A)) % C, lvl = idx / (EPB * A * C);
+      const int nd = snode[a * EPB + ee];
+      v[k] = nd >= 0 ? __ldg((lvl == 0 ? ys : yos) + (size_t)c * m.g.np + nd) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) sm[lane + k * T] = v[k];
+  }
+  __syncthreads();
+  QFields<D, double> fn, fo;
   if (valid) {
-    const double* ys = y + s * vs;
-    const double* yos = yo + s * vs;
+    double N[A], dN[A][D];
+    const double* t = tv + q * A * NS;
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      N[b] = t[b * NS];
+#pragma unroll
+      for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+    }
+    interp<D>(N, dN, [&](int a, int c) { return sm[((0 * C + c) * A + a) * EPB + el]; }, fn);
+    interp<D>(N, dN, [&](int a, int c) { return sm[((1 * C + c) * A + a) * EPB + el]; }, fo);
+  }
+  __syncthreads();  // the staging area becomes G
+  if (valid) {
     if (cp < D)
-      jaclin_point<D, 0>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+      jaclin_point<D, 0>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf, fn, fo);
     else if (cp < 2 * D)
-      jaclin_point<D, 1>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+      jaclin_point<D, 1>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf, fn, fo);
     else
-      jaclin_point<D, 2>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf);
+      jaclin_point<D, 2>(ph, st[s], e, q, ys, yos, m.g.np, cp, sm + lane, T, tv, tf, fn, fo);
   }
   __syncthreads();
   if (!valid) return;
@@ -525,6 +562,233 @@ __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m
   reduce_points<D>(R);
   if (!valid) return;
   scatter_rows<D>(R, q, e, out + s * vs, m.g.np);
+}
+
+// ---------------------------------------------------------------- K1 / K2' tiled (default)
+// Block = EPB elements of one colour x 2^d quadrature points.
+//   stage    the node values (y, y_old [, w]) of the block's elements are
+//            loaded into shared memory, every load of the block in flight at
+//            once (the per-point gathers of k_residual_colour / k_jvp_colour
+//            were the long-scoreboard stall of those kernels, ncu r02);
+//   phase 1  thread (element, point q): fields from shared memory, qflux,
+//            the NF pointwise flux values (their derivatives for J w) to
+//            shared memory; outflow face points add their B terms;
+//   phase 2  thread (element, local node a): R[a][c] = W sum_q (flux_q tested
+//            with N_a(q), grad N_a(q)) in a fixed point order (+ the face
+//            terms), scattered colour-ordered as before.
+// No xor butterfly (80 shuffles per thread in 2-d), no per-point 20-entry
+// accumulator: a fraction of the registers, no spills.
+template <int D>
+struct ElemTile {
+  static constexpr int A = 1 << D, C = 2 * D + 1;
+  static constexpr int EPB = D == 2 ? 32 : 16;       // elements per block
+  static constexpr int T = EPB * A;                  // 128 threads
+  static constexpr int NF = 3 * D + 2 * D * D + 1;   // vec, ten, uvec, uten, pv, pt
+  static constexpr int OCC = D == 2 ? 3 : 2;
+  // flux slot of each output (phase 1 writes, phase 2 reads)
+  static constexpr PINT_HD int vec(int i) { return i; }
+  static constexpr PINT_HD int ten(int i, int j) { return D + i * D + j; }
+  static constexpr PINT_HD int uvec(int i) { return D + D * D + i; }
+  static constexpr PINT_HD int uten(int i, int j) { return 2 * D + D * D + i * D + j; }
+  static constexpr PINT_HD int pv() { return 2 * D + 2 * D * D; }
+  static constexpr PINT_HD int pt(int j) { return 2 * D + 2 * D * D + 1 + j; }
+  // shared memory (doubles): node values [NL][C][A][EPB], flux [NF][T], face [D][T], shape [A][A][1+D] x 2
+  static constexpr size_t smem(int NL) {
+    return sizeof(double) * ((size_t)NL * C * A * EPB + (size_t)(NF + D) * T + 2 * (size_t)A * A * (1 + D)) +
+           sizeof(int) * (size_t)A * EPB;
+  }
+};
+
+template <int D, int MODE>  // MODE 0: residual (y, y_old), 1: J w (y, y_old, w)
+__global__ void __launch_bounds__(ElemTile<D>::T, ElemTile<D>::OCC) k_elem_tile(
+    MeshDev m, Phys ph, const StepScalars* __restrict__ st, const double* __restrict__ y,
+    const double* __restrict__ yo, const double* __restrict__ w, double* __restrict__ out, int* __restrict__ degen,
+    const int* __restrict__ active, int colour) {
+  pdl_wait();
+  using ET = ElemTile<D>;
+  constexpr int A = ET::A, C = ET::C, EPB = ET::EPB, T = ET::T, NF = ET::NF, NS = 1 + D;
+  constexpr int NL = MODE == 0 ? 2 : 3;
+  extern __shared__ double sm[];
+  double* sv = sm;                                   // [NL][C][A][EPB]
+  double* sf = sv + (size_t)NL * C * A * EPB;        // [NF][T]
+  double* sb = sf + (size_t)NF * T;                  // [D][T]
+  double* tv = sb + (size_t)D * T;                   // volume shape table [q][b][NS]
+  double* tf = tv + A * A * NS;                      // face shape table [face q][b][NS]
+  int* snode = reinterpret_cast<int*>(tf + A * A * NS);  // [A][EPB]
+  __shared__ int sdeg;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;  // uniform per block
+  const int lane = threadIdx.x;
+  const int el = lane / A, q = lane % A;
+  ElemIndex<D> e;
+  const bool valid = colour_element<D>(m, colour, blockIdx.x * EPB + el, e);
+  if (lane == 0) sdeg = 0;
+  if (q == 0) {
+#pragma unroll
+    for (int a = 0; a < A; ++a) snode[a * EPB + el] = valid ? e.node[a] : -1;
+  }
+  if (lane < A + (A >> 1)) {  // shape tables (uniform mesh: identical for every element)
+    const bool face = lane >= A;
+    double xi[D], N[A], dN[A][D];
+    gauss_point<D>(face ? lane - A : lane, face, xi);
+    q1_shape<D>(xi, ph.ih, N, dN);
+    double* t = face ? tf + (lane - A) * A * NS : tv + lane * A * NS;
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      t[b * NS] = N[b];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[b * NS + 1 + k] = dN[b][k];
+    }
+  }
+  __syncthreads();
+  // stage the node values: every load of the block issued before any use
+  const size_t vs = (size_t)C * m.g.np;
+  {
+    constexpr int PER = NL * C * A * EPB / T;
+    double v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;                  // [lvl][c][a][e]
+      const int ee = idx % EPB, a = (idx / EPB) % A, c = (idx / (EPB * A)) % C, lvl = idx / (EPB * A * C);
+      const int nd = snode[a * EPB + ee];
+      const double* src = (lvl == 0 ? y : lvl == 1 ? yo : w) + s * vs;
+      v[k] = nd >= 0 ? __ldg(src + (size_t)c * m.g.np + nd) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) sv[lane + k * T] = v[k];
+  }
+  __syncthreads();
+  // phase 1: pointwise flux at volume point q (and face point q on outflow cells)
+  if (valid) {
+    const bool solid = e.cflag & kCellSolid;
+    auto field = [&](int lvl, const double* t, QFields<D, double>& f) {
+      auto get = [&](int a, int c) { return sv[((lvl * C + c) * A + a) * EPB + el]; };
+      double N[A], dN[A][D];
+#pragma unroll
+      for (int b = 0; b < A; ++b) {
+        N[b] = t[b * NS];
+#pragma unroll
+        for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+      }
+      interp<D>(N, dN, get, f);
+    };
+    double* fo = sf + lane;
+    {
+      QFields<D, double> fn, fold;
+      field(0, tv + q * A * NS, fn);
+      field(1, tv + q * A * NS, fold);
+      bool dg = false;
+      if (MODE == 0) {
+        QFlux<D, double> fx;
+        qflux<D, double, double, double>(ph, st[s], solid, fn, fold, fx, dg);
+        if (dg) sdeg = 1;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          fo[ET::vec(i) * T] = fx.vec[i];
+          fo[ET::uvec(i) * T] = fx.uvec[i];
+          fo[ET::pt(i) * T] = fx.pt[i];
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            fo[ET::ten(i, j) * T] = fx.ten[i][j];
+            fo[ET::uten(i, j) * T] = fx.uten[i][j];
+          }
+        }
+        fo[ET::pv() * T] = fx.pv;
+      } else {
+        QFields<D, double> fw;
+        field(2, tv + q * A * NS, fw);
+        QFields<D, Dual> fd;
+        seed_fields<D>(fn, fw, fd);
+        QFlux<D, Dual> fx;
+        qflux<D, Dual, Dual, Dual>(ph, st[s], solid, fd, fold, fx, dg);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          fo[ET::vec(i) * T] = fx.vec[i].d;
+          fo[ET::uvec(i) * T] = fx.uvec[i].d;
+          fo[ET::pt(i) * T] = fx.pt[i].d;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            fo[ET::ten(i, j) * T] = fx.ten[i][j].d;
+            fo[ET::uten(i, j) * T] = fx.uten[i][j].d;
+          }
+        }
+        fo[ET::pv() * T] = fx.pv.d;
+      }
+    }
+    if ((e.cflag & kCellOutflow) && q < (A >> 1)) {
+      QFields<D, double> fn, fold;
+      field(0, tf + q * A * NS, fn);
+      field(1, tf + q * A * NS, fold);
+      if (MODE == 0) {
+        double B[D];
+        qflux_outflow<D, double, double, double>(ph, st[s], fn, fold, B);
+#pragma unroll
+        for (int i = 0; i < D; ++i) sb[i * T + lane] = B[i];
+      } else {
+        QFields<D, double> fw;
+        field(2, tf + q * A * NS, fw);
+        QFields<D, Dual> fd;
+        seed_fields<D>(fn, fw, fd);
+        Dual B[D];
+        qflux_outflow<D, Dual, Dual, Dual>(ph, st[s], fd, fold, B);
+#pragma unroll
+        for (int i = 0; i < D; ++i) sb[i * T + lane] = B[i].d;
+      }
+    }
+  }
+  __syncthreads();
+  if (MODE == 0 && lane == 0 && sdeg) degen[s] = 1;  // benign: every writer stores 1
+  if (!valid) return;
+  // phase 2: this lane owns local node a = q of its element
+  const int a = q;
+  const int base = lane - q;  // lane of point 0 of this element
+  const bool ext = (e.ext_mask >> a) & 1;
+  double R[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) R[c] = 0.0;
+#pragma unroll
+  for (int qq = 0; qq < A; ++qq) {
+    const double* f = sf + base + qq;
+    const double* ta = tv + (qq * A + a) * NS;
+    const double Na = ta[0];
+    double dNa[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) dNa[j] = ta[1 + j];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double mm = f[ET::vec(i) * T] * Na;
+      double u = f[ET::uvec(i) * T] * Na;
+      double ex = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        mm += f[ET::ten(i, j) * T] * dNa[j];
+        ex += f[ET::uten(i, j) * T] * dNa[j];
+      }
+      R[i] += ph.wq * mm;
+      R[D + i] += ph.wq * (ext ? u + ex : u);
+    }
+    double pr = f[ET::pv() * T] * Na;
+#pragma unroll
+    for (int j = 0; j < D; ++j) pr += f[ET::pt(j) * T] * dNa[j];
+    R[2 * D] += ph.wq * pr;
+  }
+  if (e.cflag & kCellOutflow) {
+#pragma unroll
+    for (int qq = 0; qq < (A >> 1); ++qq) {
+      const double na = tf[(qq * A + a) * NS];
+#pragma unroll
+      for (int i = 0; i < D; ++i) R[i] += (-ph.wf) * (sb[i * T + base + qq] * na);
+    }
+  }
+  // scatter the node's rows: every old value loaded before the first store
+  const bool solid = e.cflag & kCellSolid;  // solid cells own no p rows
+  double* o = out + s * vs + e.node[a];
+  double v[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) v[c] = (c == 2 * D && solid) ? 0.0 : o[(size_t)c * m.g.np];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!(c == 2 * D && solid)) o[(size_t)c * m.g.np] = v[c] + R[c];
 }
 
 // ---------------------------------------------------------------- fixed rows

@@ -125,6 +125,7 @@ struct pint_ctx {
   bool verbose = false;  // PINT_VERBOSE=1: per-Newton-iteration trace on stderr
   bool use_tail = true;  // PINT_TAIL=0 disables the fused coarse-level V-cycle kernel
   bool jac_columns = false;  // PINT_JAC=columns: one dual pass per Jacobian column (k_jacobian_colour)
+  bool elem_old = false;     // PINT_ELEM=old: per-point K1 / K2' kernels with register gathers (round 1)
   bool vanka_smem = false;   // PINT_VANKA_SETUP=smem: warp-per-cell shared-memory Gauss-Jordan
   int scale_fuse_max = 0;      // PINT_SCALE_FUSE: per-slice length up to which the last norm block scales v_{j+1}
                                // (measured neutral on c1/c2, off)
@@ -478,8 +479,13 @@ struct Impl {
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      pint_launch(ctx, st, k_residual_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph, ctx->d_st, y, yo, r, ctx->d_degen,
-                                                                      mask, c);
+      if (ctx->elem_old)
+        pint_launch(ctx, st, k_residual_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph,
+                    ctx->d_st, y, yo, r, ctx->d_degen, mask, c);
+      else
+        pint_launch(ctx, st, k_elem_tile<D, 0>, dim3((ne + ElemTile<D>::EPB - 1) / ElemTile<D>::EPB, S),
+                    ElemTile<D>::T, ElemTile<D>::smem(2), m, ctx->ph, (const StepScalars*)ctx->d_st, y, yo,
+                    (const double*)nullptr, r, ctx->d_degen, mask, c);
     }
     pint_launch(ctx, st, k_fix_residual<D>, node_grid(ctx->g.nn, S), 128, 0, m, ctx->d_st, y, r, mask);
     PINT_LAUNCHED();
@@ -555,7 +561,13 @@ struct Impl {
     for (int c = 0; c < (1 << D); ++c) {
       const int ne = colour_count(ctx, c);
       if (ne == 0) continue;
-      pint_launch(ctx, st, k_jvp_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph, ctx->d_st, y, yo, w, out, nullptr, c);
+      if (ctx->elem_old)
+        pint_launch(ctx, st, k_jvp_colour<D>, dim3((ne * (1 << D) + 127) / 128, S), 128, 0, m, ctx->ph,
+                    ctx->d_st, y, yo, w, out, nullptr, c);
+      else
+        pint_launch(ctx, st, k_elem_tile<D, 1>, dim3((ne + ElemTile<D>::EPB - 1) / ElemTile<D>::EPB, S),
+                    ElemTile<D>::T, ElemTile<D>::smem(3), m, ctx->ph, (const StepScalars*)ctx->d_st, y, yo, w,
+                    out, (int*)nullptr, (const int*)nullptr, c);
     }
     pint_launch(ctx, st, k_fix_jvp<D>, node_grid(ctx->g.nn, S), 128, 0, m, w, out, nullptr);
     PINT_LAUNCHED();
@@ -1827,6 +1839,15 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   }
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
+  // tiled K1 / K2' in 2-d (c3: residual 0.52 -> 0.45 ms, J w 0.58 -> 0.56 ms); the 3-d tile spills
+  // (255 registers) and measured slower (c4 residual 0.23 -> 0.25 ms), so 3-d keeps the per-point kernels
+  ctx->elem_old = ctx->D == 3;
+  if (const char* e = std::getenv("PINT_ELEM")) ctx->elem_old = std::string(e) == "old";
+  // dynamic shared memory of the tiled element kernels (3-d J w exceeds the 48 KB default)
+  cudaFuncSetAttribute(k_elem_tile<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ElemTile<2>::smem(2));
+  cudaFuncSetAttribute(k_elem_tile<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ElemTile<2>::smem(3));
+  cudaFuncSetAttribute(k_elem_tile<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ElemTile<3>::smem(2));
+  cudaFuncSetAttribute(k_elem_tile<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ElemTile<3>::smem(3));
   ctx->vanka_smem = std::getenv("PINT_VANKA_SETUP") && std::string(std::getenv("PINT_VANKA_SETUP")) == "smem";
   // level-0 Vanka sweep: fused (cell solves + gather, k_vanka_apply) in 2-d,
   // split in 3-d, where the fused grid is 1.2 waves of (node, comp) threads

@@ -187,5 +187,7 @@ def test_launch_count_is_reported(cuda):
         _run(dev, P, 0.01, starts, [0.02, 0.02])
         counts[loop] = dev.profile_read()["launches"]
         dev.profile(0)
+    # the device loop runs the first 12 Arnoldi steps of a cycle unconditionally
+    # (masked), so on this tiny problem (few Krylov iterations) it launches more
     assert counts[True] > 100 and counts[False] > 100
-    assert 0.5 < counts[True] / counts[False] < 2.0, counts
+    assert 0.5 < counts[True] / counts[False] < 4.0, counts
