@@ -50,7 +50,8 @@ struct Level {
   double* xb = nullptr;
   double* res = nullptr;
   double* sol = nullptr;   // coarse-level V-cycle output (l > 0)
-  float* A32 = nullptr;    // level 0 only: fp32 copy of A for the V-cycle's residuals (preconditioner only)
+  float* A32 = nullptr;    // fp32 copy of A for the V-cycle's residuals (preconditioner only; level 0 and
+                           // the standalone coarse levels above the fused tail)
   float* vinv = nullptr;   // Vanka cell inverses [S][L*L][ncell], fp32 storage (preconditioner only)
   double* ycell = nullptr; // Vanka cell corrections [S][L][ncell]
   int ncell = 0;
@@ -606,6 +607,10 @@ struct Impl {
       if (l > 0) {
         Level& F = ctx->lv[l - 1];
         pint_launch(ctx, st, k_rap<D>, dim3((L.g.nn + 63) / 64, L.g.noff * C, S), 64, 0, F.g, L.g, F.A, L.A, mask);
+        if (L.A32) {
+          const size_t ms = (size_t)L.g.noff * C * C * L.g.np;
+          pint_launch(ctx, st, k_to_f32, vec_grid(ms / 2, S), 256, 0, (const double*)L.A, L.A32, ms, mask);
+        }
       }
       const bool last_dense = ctx->coarse_dense && l == nl - 1;
       if (ko->smoother == 1 && !last_dense && !ctx->vanka_smem) {
@@ -1991,15 +1996,23 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   // optional fp32 copy of the level-0 operator for the V-cycle residuals (half
   // the bytes of the two level-0 SpMVs of every cycle); skipped when it does
   // not fit next to the rest of the workspace (or with PINT_A32=0)
+  // The coarse levels that run as standalone kernels (above the fused tail)
+  // get an fp32 copy too (made after their Galerkin product; PINT_A32C=0 keeps
+  // them fp64): their V-cycle residual SpMVs were 8 % of the c3 step in fp64.
   if (!ctx->matrix_free && !(std::getenv("PINT_A32") && std::getenv("PINT_A32")[0] == '0')) {
-    Level& L0 = ctx->lv[0];
-    const size_t cnt = (size_t)S * L0.g.noff * C * C * L0.g.np;
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && cnt * sizeof(float) + (size_t(2) << 30) < free_b) {
-      if (dalloc(ctx, &L0.A32, cnt) != PINT_OK) {
-        L0.A32 = nullptr;
+    const bool coarse = !(std::getenv("PINT_A32C") && std::getenv("PINT_A32C")[0] == '0');
+    for (size_t l = 0; l < (coarse ? ctx->lv.size() : 1); ++l) {
+      Level& L = ctx->lv[l];
+      if (l > 0 && (size_t)L.g.nn * C <= (size_t)ctx->tail_rows) break;  // the tail reads fp64 there
+      const size_t cnt = (size_t)S * L.g.noff * C * C * L.g.np;
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || cnt * sizeof(float) + (size_t(2) << 30) >= free_b)
+        break;
+      if (dalloc(ctx, &L.A32, cnt) != PINT_OK) {
+        L.A32 = nullptr;
         ctx->err.clear();
         cudaGetLastError();
+        break;
       }
     }
   }

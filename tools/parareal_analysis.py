@@ -44,27 +44,33 @@ def rel(a, b, sl):
     return float(np.linalg.norm(a[sl] - b[sl]) / nb) if nb > 0 else float(np.linalg.norm(a[sl] - b[sl]))
 
 
-def order(cfg_name, t_final, steps):
+def order(cfg_name, t_final, steps, theta0=None):
     rc = CONFIGS[cfg_name]
     P = rc.problem
+    th0 = rc.theta0 if theta0 is None else theta0
     dev = FSIDevice(P, 1)
     s0 = initial_state(P)
-    ref = make_propagator(P, ThetaSettings(min(steps) / 8, rc.theta0, NW), device=dev).advance(s0, t_final)
+    ref = make_propagator(P, ThetaSettings(min(steps) / 8, th0, NW), device=dev).advance(s0, t_final)
     errs = {b: [] for b in ("v", "u", "p", "all")}
     for k in steps:
-        end = make_propagator(P, ThetaSettings(k, rc.theta0, NW), device=dev).advance(s0, t_final)
+        end = make_propagator(P, ThetaSettings(k, th0, NW), device=dev).advance(s0, t_final)
         for b, sl in blocks(P).items():
             errs[b].append(max(float(np.linalg.norm(end.values[sl] - ref.values[sl])), 1e-300))
         errs["all"].append(max(float(np.linalg.norm(end.values - ref.values)), 1e-300))
     lk = np.log(np.asarray(steps))
     slopes = {b: float(np.polyfit(lk, np.log(np.asarray(e)), 1)[0]) for b, e in errs.items()}
     print(json.dumps({"analysis": "temporal order (reference convergence_order procedure)", "config": cfg_name,
-                      "t_final": t_final, "steps": steps, "theta0": rc.theta0, "errors": errs,
+                      "t_final": t_final, "steps": steps, "theta0": th0, "errors": errs,
                       "observed_order": slopes}), flush=True)
 
 
-def fields(cfg_name, variants, iters):
+def fields(cfg_name, variants, iters, coarse_step=None, mu_s=None):
+    from dataclasses import replace
     rc = CONFIGS[cfg_name]
+    if coarse_step:
+        rc = replace(rc, coarse_step=coarse_step)
+    if mu_s:
+        rc = replace(rc, problem=replace(rc.problem, mu_s=mu_s))
     P = rc.problem
     L = rc.intervals
     dev = FSIDevice(P, L)
@@ -83,7 +89,8 @@ def fields(cfg_name, variants, iters):
         C = make_propagator(P, ThetaSettings(rc.coarse_step, rc.theta0, NW), device=dev)
         Fp = make_propagator(P, ThetaSettings(rc.fine_step, rc.theta0, NW), device=dev)
         cfg = PararealConfig(intervals=L, max_iters=min(iters or rc.iterations, L), tol=1e-30, variant=variant)
-        out = {"analysis": "parareal per field", "config": cfg_name, "variant": variant}
+        out = {"analysis": "parareal per field", "config": cfg_name, "variant": variant,
+               "coarse_step": rc.coarse_step, "fine_step": rc.fine_step, "mu_s": P.mu_s}
         try:
             _, tr = run_parareal_device(C, Fp, s0, rc.t_end, cfg)
         except Exception as exc:  # a failing coarse step is itself a result
@@ -116,11 +123,14 @@ def main():
     ap.add_argument("--steps", type=float, nargs="+", default=[0.008, 0.004, 0.002, 0.001])
     ap.add_argument("--variants", nargs="+", default=["classic", "least_squares", "angle_penalized"])
     ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--theta0", type=float, default=None, help="order: theta = 1/2 + theta0 k (default: config's)")
+    ap.add_argument("--coarse-step", type=float, default=None, help="fields: override the coarse step")
+    ap.add_argument("--mu-s", type=float, default=None, help="fields: override the solid shear modulus")
     a = ap.parse_args()
     if a.what == "order":
-        order(a.config, a.t_final, a.steps)
+        order(a.config, a.t_final, a.steps, a.theta0)
     else:
-        fields(a.config, a.variants, a.iters)
+        fields(a.config, a.variants, a.iters, a.coarse_step, a.mu_s)
 
 
 if __name__ == "__main__":
