@@ -64,7 +64,7 @@ def order(cfg_name, t_final, steps, theta0=None):
                       "observed_order": slopes}), flush=True)
 
 
-def fields(cfg_name, variants, iters, coarse_step=None, mu_s=None):
+def fields(cfg_name, variants, iters, coarse_step=None, mu_s=None, coarse_theta0=None):
     from dataclasses import replace
     rc = CONFIGS[cfg_name]
     if coarse_step:
@@ -86,11 +86,13 @@ def fields(cfg_name, variants, iters, coarse_step=None, mu_s=None):
                       "per_block_max_over_boundaries": {b: max(v) for b, v in disc.items()},
                       "per_block_last_boundary": {b: v[-1] for b, v in disc.items()}}), flush=True)
     for variant in variants:
-        C = make_propagator(P, ThetaSettings(rc.coarse_step, rc.theta0, NW), device=dev)
+        cth0 = rc.theta0 if coarse_theta0 is None else coarse_theta0
+        C = make_propagator(P, ThetaSettings(rc.coarse_step, cth0, NW), device=dev)
         Fp = make_propagator(P, ThetaSettings(rc.fine_step, rc.theta0, NW), device=dev)
         cfg = PararealConfig(intervals=L, max_iters=min(iters or rc.iterations, L), tol=1e-30, variant=variant)
         out = {"analysis": "parareal per field", "config": cfg_name, "variant": variant,
-               "coarse_step": rc.coarse_step, "fine_step": rc.fine_step, "mu_s": P.mu_s}
+               "coarse_step": rc.coarse_step, "coarse_theta": ThetaSettings(rc.coarse_step, cth0, NW).theta,
+               "fine_step": rc.fine_step, "mu_s": P.mu_s}
         try:
             _, tr = run_parareal_device(C, Fp, s0, rc.t_end, cfg)
         except Exception as exc:  # a failing coarse step is itself a result
@@ -125,12 +127,14 @@ def main():
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--theta0", type=float, default=None, help="order: theta = 1/2 + theta0 k (default: config's)")
     ap.add_argument("--coarse-step", type=float, default=None, help="fields: override the coarse step")
+    ap.add_argument("--coarse-theta0", type=float, default=None,
+                    help="fields: coarse theta = 1/2 + theta0 K (clamped to 1: 0.5/K gives implicit Euler)")
     ap.add_argument("--mu-s", type=float, default=None, help="fields: override the solid shear modulus")
     a = ap.parse_args()
     if a.what == "order":
         order(a.config, a.t_final, a.steps, a.theta0)
     else:
-        fields(a.config, a.variants, a.iters, a.coarse_step, a.mu_s)
+        fields(a.config, a.variants, a.iters, a.coarse_step, a.mu_s, a.coarse_theta0)
 
 
 if __name__ == "__main__":
