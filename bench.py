@@ -122,7 +122,7 @@ def _traffic(config, kernel):
     """DRAM bytes per launch of the roofline kernel from the committed ncu
     --set full capture (tools/ncu_traffic.py), or None when there is none."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             e = json.load(f)[config]
     except Exception:
         return None

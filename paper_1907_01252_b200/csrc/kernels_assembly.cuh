@@ -28,6 +28,13 @@ struct MeshDev {
   const double* profile;       // [nn] inflow x-velocity at s(t) = 1
 };
 
+// row (node flags f, component c) is a Dirichlet / identity row
+__device__ __forceinline__ bool row_fixed(uint8_t f, int c, int D) {
+  if (c < D) return f & kDirV;
+  if (c < 2 * D) return f & kDirU;
+  return !(f & kFluidTouch);
+}
+
 template <int D>
 struct ElemIndex {
   int node[1 << D];
@@ -539,6 +546,321 @@ __global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(M
       if (!(c == 2 * D && solid)) o[idx(b, c)] = K[c][b];
 }
 
+// ---------------------------------------------------------------- K2 Jacobian, node-owner strips (2-d default)
+// The colour-ordered kernels above add every element block into the stencil
+// with a read-modify-write after a zeroing pass, and a separate pass makes
+// the fp32 copy: c3 moved 10.3 GB of DRAM per assembly for 1.9 GB of
+// operator (ncu r02: 1.37 GB read + 1.20 GB written per colour launch), and
+// long-scoreboard stalls on those reads were the largest stall reason.
+// Here a block OWNS the stencil rows of a strip of W node columns x a chunk
+// of node rows, for one column component cp, and sweeps the strip's cell rows
+// bottom to top:
+//   stage    node values of the next node row go to a 3-row ring in shared
+//            memory (loads issued before phase 1, stored after it);
+//   phase 1  thread = (cell of the row, Gauss point): the pointwise flux
+//            derivative table G (as k_jacobian_lin, 1 + d dual passes) for the
+//            W + 1 cells of the row (the left halo cell is recomputed: no cell
+//            is shared between blocks for writing);
+//   phase 2  thread = (node column, row component ca): contracts G of the two
+//            cells left / right of the node into the 9 stencil entries of row
+//            (node, ca), column component cp.  Node row cj gets its
+//            bottom-corner terms from cell row cj on top of its top-corner
+//            terms from cell row cj - 1 (kept in shared memory since the
+//            previous row), is then complete and is written ONCE -- fp64 and
+//            the fp32 copy, with the identity rows of fixed dofs -- so there is
+//            no zeroing pass, no read-modify-write, no k_fix_jacobian and no
+//            k_to_f32 behind it.
+// Every entry is a sum in a fixed order (cell row j-1 left, right, row j
+// left, right; points in order, then outflow face points): deterministic and
+// independent of the batch.
+struct JacStrip {
+  static constexpr int A = 4, C = 5, NS = 3, D = 2;
+  static constexpr int T = 128;          // threads: 32 cells x 4 points in phase 1
+  static constexpr int WMAX = T / A - 1;  // owned node columns per strip (<= 31)
+  static constexpr int GSZ = C * NS * NS;
+  static constexpr int FSZ = D * NS;
+  static constexpr int RW = WMAX + 3;    // staged node columns (cells + 1, padded)
+  static constexpr int NPART = 6;        // top-corner partials: offsets with dj in {-1, 0}
+  static constexpr int ITEMS = 160;      // phase-2 item slots (>= WMAX * C)
+  static constexpr size_t smem = sizeof(double) * ((size_t)(GSZ + FSZ) * T + A * A * NS + (A / 2) * A * NS +
+                                                   (size_t)3 * 2 * C * RW + (size_t)NPART * ITEMS);
+};
+
+template <int G>
+__device__ __forceinline__ void strip_point(const Phys& ph, const StepScalars& st, bool solid, bool face_pt, int cp,
+                                            const QFields<2, double>& fn, const QFields<2, double>& fo,
+                                            const QFields<2, double>& gn, const QFields<2, double>& go,
+                                            double* __restrict__ sg) {
+  using J = JacStrip;
+  constexpr int D = 2, NS = J::NS, T = J::T;
+  using ST = SeedTypes<D, G>;
+#pragma unroll 1
+  for (int dir = 0; dir < NS; ++dir) {
+    typename ST::F fd;
+    seed_dir<D, G>(fn, cp, dir, fd);
+    QFlux<D, Dual> fx;
+    bool dg = false;
+    qflux<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, solid, fd, fo, fx, dg);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      sg[((i * NS + 0) * NS + dir) * T] = fx.vec[i].d;
+      sg[(((D + i) * NS + 0) * NS + dir) * T] = fx.uvec[i].d;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        sg[((i * NS + 1 + j) * NS + dir) * T] = fx.ten[i][j].d;
+        sg[(((D + i) * NS + 1 + j) * NS + dir) * T] = fx.uten[i][j].d;
+      }
+    }
+    sg[((2 * D * NS + 0) * NS + dir) * T] = fx.pv.d;
+#pragma unroll
+    for (int j = 0; j < D; ++j) sg[((2 * D * NS + 1 + j) * NS + dir) * T] = fx.pt[j].d;
+  }
+  if constexpr (G != 2) {
+    if (face_pt) {
+#pragma unroll 1
+      for (int dir = 0; dir < NS; ++dir) {
+        typename ST::F fd;
+        seed_dir<D, G>(gn, cp, dir, fd);
+        Dual B[D];
+        qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, go, B);
+#pragma unroll
+        for (int i = 0; i < D; ++i) sg[(J::GSZ + i * NS + dir) * T] = B[i].d;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+                                                                  const double* __restrict__ y, const double* __restrict__ yo,
+                                                                  double* __restrict__ J, float* __restrict__ J32,
+                                                                  const int* __restrict__ active, int W, int nstrips, int H) {
+  pdl_wait();
+  using L = JacStrip;
+  constexpr int A = L::A, C = L::C, NS = L::NS, T = L::T, D = 2, RW = L::RW;
+  extern __shared__ double sm[];
+  double* sg = sm;                                   // G [GSZ + FSZ][T]
+  double* tv = sg + (size_t)(L::GSZ + L::FSZ) * T;   // [q][b][NS]
+  double* tf = tv + A * A * NS;                      // [face q][b][NS]
+  double* ring = tf + (A / 2) * A * NS;              // [slot 3][lvl 2][c][RW]
+  double* part = ring + 3 * 2 * C * RW;              // [NPART][ITEMS]
+  const int s = blockIdx.z;
+  if (active && !active[s]) return;  // uniform per block
+  const int cp = blockIdx.y;
+  const int lane = threadIdx.x;
+  const int nx = m.cells[0], ny = m.cells[1];        // cells
+  const int strip = blockIdx.x % nstrips, chunk = blockIdx.x / nstrips;
+  const int i0 = strip * W;
+  const int nown = min(W, nx + 1 - i0);              // owned node columns i0 .. i0 + nown - 1
+  const int j0 = chunk * H, j1 = min(j0 + H, ny + 1);  // owned node rows
+  if (nown <= 0 || j0 >= j1) return;
+  const int c_lo = max(i0 - 1, 0), c_hi = min(i0 + nown - 1, nx - 1);  // cell columns
+  const int ncell = c_hi - c_lo + 1;
+  const int ncol = ncell + 1;                        // staged node columns c_lo .. c_hi + 1
+  const int cj_lo = max(j0 - 1, 0), cj_hi = min(j1 - 1, ny - 1);
+  const int np = m.g.np;
+  const size_t vs = (size_t)C * np;
+  const double* ys = y + s * vs;
+  const double* yos = yo + s * vs;
+  if (lane < A + (A >> 1)) {  // shape tables (uniform mesh)
+    const bool face = lane >= A;
+    double xi[D], N[A], dN[A][D];
+    gauss_point<D>(face ? lane - A : lane, face, xi);
+    q1_shape<D>(xi, ph.ih, N, dN);
+    double* t = face ? tf + (lane - A) * A * NS : tv + lane * A * NS;
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      t[b * NS] = N[b];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[b * NS + 1 + k] = dN[b][k];
+    }
+  }
+  // node row r -> ring slot r % 3; entries [lvl][c][col]
+  constexpr int PER = (2 * C * RW + T - 1) / T;
+  auto load_row = [&](int r, double (&v)[PER]) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;
+      const int col = idx % RW, c = (idx / RW) % C, lvl = idx / (RW * C);
+      v[k] = (lvl < 2 && col < ncol) ? __ldg((lvl == 0 ? ys : yos) + (size_t)c * np + node_index(m.g, c_lo + col, r, 0))
+                                     : 0.0;
+    }
+  };
+  auto store_row = [&](int r, const double (&v)[PER]) {
+    double* dst = ring + (r % 3) * 2 * C * RW;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;
+      if (idx < 2 * C * RW) dst[idx] = v[k];
+    }
+  };
+  {
+    double v[PER];
+    load_row(cj_lo, v);
+    store_row(cj_lo, v);
+    load_row(cj_lo + 1, v);
+    store_row(cj_lo + 1, v);
+  }
+  // phase 1 lane = q * 32 + lc (cell c_lo + lc, point q): G entries of one point
+  // are contiguous over the cells, so phase 2 (lanes = consecutive node
+  // columns) reads them without bank conflicts
+  const int lc = lane % 32, q = lane / 32;
+  const int nitems = nown * C;
+  __syncthreads();
+  for (int cj = cj_lo; cj <= cj_hi; ++cj) {
+    double pre[PER];
+    const bool more = cj + 2 <= min(cj_hi + 1, ny);
+    if (more) load_row(cj + 2, pre);
+    // ---- phase 1: G of (cell c_lo + lc, row cj) at point q
+    if (lc < ncell) {
+      const int ci = c_lo + lc;
+      const uint8_t cf = m.cell_flags[cj * nx + ci];
+      const bool solid = cf & kCellSolid;
+      const double* r0 = ring + (cj % 3) * 2 * C * RW;        // node row cj
+      const double* r1 = ring + ((cj + 1) % 3) * 2 * C * RW;  // node row cj + 1
+      auto getter = [&](int lvl) {
+        return [=](int a, int c) {
+          const double* rr = (a >> 1) ? r1 : r0;
+          return rr[(lvl * C + c) * RW + lc + (a & 1)];
+        };
+      };
+      QFields<D, double> fn, fo, gn, go;
+      {
+        double N[A], dN[A][D];
+        const double* t = tv + q * A * NS;
+#pragma unroll
+        for (int b = 0; b < A; ++b) {
+          N[b] = t[b * NS];
+#pragma unroll
+          for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+        }
+        interp<D>(N, dN, getter(0), fn);
+        interp<D>(N, dN, getter(1), fo);
+      }
+      const bool face_pt = (cf & kCellOutflow) && q < (A >> 1) && cp < 2 * D;
+      if (face_pt) {
+        double N[A], dN[A][D];
+        const double* t = tf + q * A * NS;
+#pragma unroll
+        for (int b = 0; b < A; ++b) {
+          N[b] = t[b * NS];
+#pragma unroll
+          for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+        }
+        interp<D>(N, dN, getter(0), gn);
+        interp<D>(N, dN, getter(1), go);
+      }
+      if (cp < D)
+        strip_point<0>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+      else if (cp < 2 * D)
+        strip_point<1>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+      else
+        strip_point<2>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+    }
+    if (more) store_row(cj + 2, pre);  // slot (cj + 2) % 3 = (cj - 1) % 3: not read in this row
+    __syncthreads();
+    // ---- phase 2: rows (node (i, cj), ca) and (node (i, cj + 1), ca)
+    for (int it = lane; it < nitems; it += T) {
+      const int ca = it / nown, li = it % nown;
+      const int i = i0 + li;
+      double K[9];
+      const bool own_bottom = cj >= j0;                     // node row cj owned (else: halo row)
+      const bool own_top = cj + 1 < j1;                     // node row cj + 1 owned
+      const bool top_final = own_top && cj + 1 == ny;       // no cell row above: complete now
+#pragma unroll
+      for (int o = 0; o < 9; ++o) K[o] = 0.0;
+      if (own_bottom && cj > cj_lo) {
+#pragma unroll
+        for (int o = 0; o < L::NPART; ++o) K[o] = part[o * L::ITEMS + it];
+      }
+      // contribution of cell (ci, cj) to row (a, ca): K[off(a, b)] += ...
+      auto cell_terms = [&](int ci, int a, double (&Kx)[9]) {
+        if (ci < 0 || ci >= nx) return;
+        const int lcell = ci - c_lo;
+        const uint8_t cf = m.cell_flags[cj * nx + ci];
+        const bool solid = cf & kCellSolid;
+        if (ca == 2 * D && solid) return;                   // solid cells own no p rows
+        const int nj = cj + (a >> 1);
+        const uint8_t nf = m.node_flags[node_index(m.g, i, nj, 0)];
+        const bool ext = solid || !(nf & kSolidTouch);
+        const bool full = !(ca >= D && ca < 2 * D) || ext;  // u rows without the extension row: value part only
+#pragma unroll 1
+        for (int qq = 0; qq < A; ++qq) {
+          const double* g = sg + qq * 32 + lcell;
+          const double* ta = tv + (qq * A + a) * NS;
+          double h[NS];
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            double v = g[((ca * NS + 0) * NS + k) * T] * ta[0];
+            if (full) {
+#pragma unroll
+              for (int o = 1; o < NS; ++o) v += g[((ca * NS + o) * NS + k) * T] * ta[o];
+            }
+            h[k] = ph.wq * v;
+          }
+#pragma unroll
+          for (int b = 0; b < A; ++b) {
+            const double* tb = tv + (qq * A + b) * NS;
+            double v = h[0] * tb[0];
+#pragma unroll
+            for (int k = 1; k < NS; ++k) v += h[k] * tb[k];
+            Kx[offset_index((b & 1) - (a & 1), (b >> 1) - (a >> 1), 0, D)] += v;
+          }
+        }
+        if ((cf & kCellOutflow) && cp < 2 * D && ca < D) {
+#pragma unroll 1
+          for (int qq = 0; qq < (A >> 1); ++qq) {
+            const double* g = sg + (size_t)L::GSZ * T + qq * 32 + lcell;
+            const double na = tf[(qq * A + a) * NS];
+            double h[NS];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) h[k] = (-ph.wf) * (g[(ca * NS + k) * T] * na);
+#pragma unroll
+            for (int b = 0; b < A; ++b) {
+              const double* tb = tf + (qq * A + b) * NS;
+              double v = h[0] * tb[0];
+#pragma unroll
+              for (int k = 1; k < NS; ++k) v += h[k] * tb[k];
+              Kx[offset_index((b & 1) - (a & 1), (b >> 1) - (a >> 1), 0, D)] += v;
+            }
+          }
+        }
+      };
+      auto write_row = [&](int j, const double (&Kx)[9]) {
+        const int n = node_index(m.g, i, j, 0);
+        const uint8_t nf = m.node_flags[n];
+        const bool fixed = row_fixed(nf, ca, D);
+        const int ctr = center_offset(D);
+        const size_t base = (size_t)s * m.g.noff * C * C * np + ((size_t)ca * C + cp) * np + n;
+#pragma unroll
+        for (int o = 0; o < 9; ++o) {
+          const double v = fixed ? ((o == ctr && cp == ca) ? 1.0 : 0.0) : Kx[o];
+          J[base + (size_t)o * C * C * np] = v;
+          if (J32) J32[base + (size_t)o * C * C * np] = (float)v;
+        }
+      };
+      if (own_bottom) {
+        cell_terms(i - 1, 1, K);  // node is the bottom-right corner of the left cell
+        cell_terms(i, 0, K);      // bottom-left corner of the right cell
+        write_row(cj, K);
+      }
+      if (own_top) {
+        double P[9];
+#pragma unroll
+        for (int o = 0; o < 9; ++o) P[o] = 0.0;
+        cell_terms(i - 1, 3, P);  // top-right corner of the left cell
+        cell_terms(i, 2, P);      // top-left corner of the right cell
+        if (top_final) {
+          write_row(cj + 1, P);
+        } else {
+#pragma unroll
+          for (int o = 0; o < L::NPART; ++o) part[o * L::ITEMS + it] = P[o];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- Jacobian-vector product (matrix-free)
 template <int D>
 __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
@@ -792,11 +1114,6 @@ __global__ void __launch_bounds__(ElemTile<D>::T, ElemTile<D>::OCC) k_elem_tile(
 }
 
 // ---------------------------------------------------------------- fixed rows
-__device__ __forceinline__ bool row_fixed(uint8_t f, int c, int D) {
-  if (c < D) return f & kDirV;
-  if (c < 2 * D) return f & kDirU;
-  return !(f & kFluidTouch);
-}
 
 // residual rows r = y - g on Dirichlet / identity rows
 template <int D>

@@ -334,6 +334,57 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
   y[o] = RESID ? b[o] - acc : acc;
 }
 
+// Thread = node, all C rows (the V-cycle residuals with the fp32 operator
+// copy).  The (node, row) kernel above re-reads the node's C*NOFF neighbour
+// x values once per row thread: with 4-byte coefficients those x loads were
+// 2/3 of its L1 wavefronts (c3 level 0 at 0.69 of HBM, ncu r02).  Here every
+// x value is loaded once per node and kept in registers across the C rows.
+// Same association order per row as stencil_row (offsets o, o+3, o+6 into
+// partial o % 3, components cb in order, then (p0 + p1) + p2): bitwise the
+// (node, row) kernel.
+template <int D, bool RESID, typename MT>
+__global__ void __launch_bounds__(128) k_spmv_node(Grid g, const MT* __restrict__ A, const double* __restrict__ x,
+                                                   const double* __restrict__ b, double* __restrict__ y,
+                                                   const int* __restrict__ active) {
+  pdl_wait();
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.nn) return;
+  const int np = g.np;
+  const size_t vs = (size_t)C * np;
+  const MT* As = A + (size_t)s * NOFF * C * C * np + n;
+  const double* xs = x + s * vs;
+  int nbs[NOFF];
+  stencil_neighbours<D>(g, n, nbs);
+  double part[C][3];
+#pragma unroll
+  for (int ca = 0; ca < C; ++ca) part[ca][0] = part[ca][1] = part[ca][2] = 0.0;
+#pragma unroll
+  for (int o = 0; o < NOFF; ++o) {
+    double xv[C];
+    MT a[C][C];
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) xv[cb] = ld_nc(xs + cb * np + nbs[o]);
+#pragma unroll
+    for (int ca = 0; ca < C; ++ca)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) a[ca][cb] = ld_nc(As + ((size_t)(o * C + ca) * C + cb) * np);
+#pragma unroll
+    for (int ca = 0; ca < C; ++ca)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) part[ca][o % 3] = fma((double)a[ca][cb], xv[cb], part[ca][o % 3]);
+  }
+#pragma unroll
+  for (int ca = 0; ca < C; ++ca) {
+    const double acc = (part[ca][0] + part[ca][1]) + part[ca][2];
+    const size_t off = s * vs + (size_t)ca * np + n;
+    y[off] = RESID ? b[off] - acc : acc;
+  }
+}
+
 // ---------------------------------------------------------------- K4 node-block Jacobi
 // Dinv[s][ca][cb][n] = inverse of the centre block (Gauss-Jordan, partial pivoting)
 template <int D>

@@ -142,6 +142,8 @@ struct pint_ctx {
   std::vector<int> first_its;   // per slice: Krylov its of the latest first-Newton-iteration solve
   int poll_every = 4;           // PINT_POLL: Arnoldi steps between host polls of the convergence mask
   bool pdl = true;              // PINT_PDL=0: launch without programmatic stream serialization
+  bool jac_strip = true;        // PINT_JAC=colour: 2-d Jacobian by colour-ordered element scatter (k_jacobian_lin)
+  bool spmv32_node = true;      // PINT_SPMV32=row: fp32 V-cycle residuals with one thread per (node, row)
   int tail_rows = 2048;         // PINT_TAIL_ROWS: first level of the fused V-cycle tail has <= this many rows
   int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
@@ -513,6 +515,28 @@ struct Impl {
     MeshDev m = mesh(ctx);
     Level& L0 = ctx->lv[0];
     const size_t ms = (size_t)ctx->g.noff * C * C * ctx->g.np;
+    if constexpr (D == 2) {
+      if (ctx->jac_strip && !ctx->jac_columns) {
+        // node-owner strips: every stencil row written once (fp64 + fp32 copy, fixed rows included)
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_jacobian_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JacStrip::smem);
+          attr = true;
+        }
+        const int nxn = ctx->cells[0] + 1, nyn = ctx->cells[1] + 1;
+        const int nstrips = (nxn + JacStrip::WMAX - 1) / JacStrip::WMAX;
+        const int W = (nxn + nstrips - 1) / nstrips;
+        // enough blocks for ~8 waves at 3 CTAs/SM; each chunk recomputes one halo cell row
+        const int base = nstrips * C * S;
+        int nch = std::max(1, std::min((8 * 3 * 148 + base - 1) / base, std::max(1, nyn / 4)));
+        const int H = (nyn + nch - 1) / nch;
+        nch = (nyn + H - 1) / H;
+        pint_launch(ctx, st, k_jacobian_strip, dim3(nstrips * nch, C, S), JacStrip::T, JacStrip::smem, m, ctx->ph,
+                    (const StepScalars*)ctx->d_st, y, yo, L0.A, L0.A32, mask, W, nstrips, H);
+        PINT_LAUNCHED();
+        return PINT_OK;
+      }
+    }
     pint_launch(ctx, st, k_zero_active, vec_grid(ms, S), 256, 0, L0.A, ms, mask);
     constexpr int A = 1 << D;
     if (!ctx->jac_columns) {
@@ -546,7 +570,13 @@ struct Impl {
   static void vc_resid(pint_ctx* ctx, const Level& L, int S, const double* x, const double* b, double* r,
                        const int* mask, cudaStream_t st) {
     const bool w = wide(L.g.nn, S);
-    if (L.A32) {
+    // node-per-thread kernel once the level fills >= 2 waves of 128-thread
+    // CTAs (c3 levels 0-1: +4.6 %); below that the (node, row) threads hide
+    // latency better (c2, L2-resident: -3 % with the node kernel)
+    if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= (size_t)2 * 4 * 148 * 128) {
+      pint_launch(ctx, st, k_spmv_node<D, true, float>, node_grid(L.g.nn, S), 128, 0, L.g, (const float*)L.A32, x, b, r,
+                  mask);
+    } else if (L.A32) {
       if (w) pint_launch(ctx, st, k_spmv<D, true, 3, float>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A32, x, b, r, mask);
       else pint_launch(ctx, st, k_spmv<D, true, 9, float>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, L.A32, x, b, r, mask);
     } else {
@@ -1844,6 +1874,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   }
   ctx->use_fused = std::getenv("PINT_FUSED") && std::getenv("PINT_FUSED")[0] == '1';
   ctx->jac_columns = std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "columns";
+  ctx->jac_strip = !(std::getenv("PINT_JAC") && std::string(std::getenv("PINT_JAC")) == "colour");
   // tiled K1 / K2' in 2-d (c3: residual 0.52 -> 0.45 ms, J w 0.58 -> 0.56 ms); the 3-d tile spills
   // (255 registers) and measured slower (c4 residual 0.23 -> 0.25 ms), so 3-d keeps the per-point kernels
   ctx->elem_old = ctx->D == 3;
@@ -1867,6 +1898,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
   ctx->pdl = !(std::getenv("PINT_PDL") && std::getenv("PINT_PDL")[0] == '0');
+  ctx->spmv32_node = !(std::getenv("PINT_SPMV32") && std::string(std::getenv("PINT_SPMV32")) == "row");
   if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||

@@ -5,6 +5,8 @@ CPU-oracle FSI propagators (oracle/fsi_oracle.py) as C and F.
   python tests/golden/make_parareal_goldens.py c1 classic
   python tests/golden/make_parareal_goldens.py small least_squares
   python tests/golden/make_parareal_goldens.py small classic 2e-2   # tol-based stop
+  python tests/golden/make_parareal_goldens.py c1 classic 1e-30 25  # damped coarse propagator
+                                  # (coarse theta = 1/2 + 25 K = 1: implicit Euler)
 
 Writes tests/golden/parareal_<case>_<variant>.npz with the final boundary
 states, the defect history (correction_norms), theta values and the
@@ -37,25 +39,25 @@ CASES = {
 }
 
 
-def main(case, variant, tol=1e-30):
+def main(case, variant, tol=1e-30, coarse_theta0=1.0):
     P, t_end, kf, kc, L, K = CASES[case]
     F = O.OracleFSIPropagator(P, kf, 1.0, NEWTON)
-    C = O.OracleFSIPropagator(P, kc, 1.0, NEWTON)
+    C = O.OracleFSIPropagator(P, kc, coarse_theta0, NEWTON)
     s0 = O.initial_state(P)
     cfg = PararealConfig(intervals=L, max_iters=K, tol=tol, variant=variant)
     t0 = time.time()
     states, trace = run_parareal(C, F, s0, t_end, cfg)
     dt = time.time() - t0
-    tag = "" if tol == 1e-30 else "_tol"
+    tag = ("" if tol == 1e-30 else "_tol") + ("" if coarse_theta0 == 1.0 else f"_ct{coarse_theta0:g}")
     out = os.path.join(HERE, f"parareal_{case}_{variant}{tag}.npz")
     np.savez_compressed(out, final=np.array([s.values for s in states]), tol=tol, converged=trace.converged,
                         correction_norms=np.array(trace.correction_norms),
                         theta_values=np.array(trace.theta_values), iterations_run=trace.iterations_run,
-                        t_end=t_end, kf=kf, kc=kc, L=L, K=K, seconds=dt,
+                        t_end=t_end, kf=kf, kc=kc, L=L, K=K, seconds=dt, coarse_theta0=coarse_theta0,
                         fine_newton=F.newton_iterations, coarse_newton=C.newton_iterations)
     print(out, f"{dt:.1f} s", trace.iterations_run, np.array(trace.correction_norms)[:, -1])
 
 
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "classic",
-         float(sys.argv[3]) if len(sys.argv) > 3 else 1e-30)
+         float(sys.argv[3]) if len(sys.argv) > 3 else 1e-30, float(sys.argv[4]) if len(sys.argv) > 4 else 1.0)

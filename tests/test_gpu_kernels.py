@@ -198,21 +198,24 @@ def _device_with_env(P, env, S=3):
 
 @pytest.mark.parametrize("name", ["c1", "small3d"])
 def test_jacobian_formulations_agree(cuda, name):
-    """K2 by pointwise linearisation (1 + d dual passes per column component,
-    default) and K2 by one dual pass per Jacobian column (PINT_JAC=columns)
-    assemble the same block-stencil operator up to round-off."""
+    """K2 by pointwise linearisation (1 + d dual passes per column component)
+    in node-owner strips (2-d default; 3-d uses the colour scatter), in the
+    colour-ordered element scatter (PINT_JAC=colour) and K2 by one dual pass
+    per Jacobian column (PINT_JAC=columns) assemble the same block-stencil
+    operator up to round-off."""
     P = PROBLEMS[name]
     S = 3
     Y = random_states(P, S, 51)
     Yo = random_states(P, S, 52)
     k, th, t1 = _step_args(S)
     blocks = []
-    for env in ({}, {"PINT_JAC": "columns"}):
+    for env in ({}, {"PINT_JAC": "colour"}, {"PINT_JAC": "columns"}):
         dev = _device_with_env(P, env)
         dev.assemble(dev.to_device(Y), dev.to_device(Yo), k, th, t1)
         blocks.append(dev.jacobian_blocks(S).cpu().numpy())
-    scale = np.abs(blocks[1]).max()
-    assert np.abs(blocks[0] - blocks[1]).max() <= 1e-13 * scale
+    scale = np.abs(blocks[-1]).max()
+    for b in blocks[:-1]:
+        assert np.abs(b - blocks[-1]).max() <= 1e-13 * scale
 
 
 @pytest.mark.parametrize("name", ["c1", "small3d"])
@@ -252,6 +255,27 @@ def test_vanka_fused_sweep_bitwise(cuda, name, tail_rows):
     outs = []
     for mode in ("fused", "split"):
         dev = _device_with_env(P, {"PINT_VANKA": mode, "PINT_TAIL_ROWS": tail_rows}, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+    assert np.array_equal(outs[0], outs[1]), name
+
+
+@pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("small3d", "300")])
+def test_spmv32_node_bitwise(cuda, name, tail_rows):
+    """The V-cycle residuals with the fp32 operator copy: one thread per node
+    (k_spmv_node, default) and one per (node, row) (PINT_SPMV32=row) sum in
+    the same order, so the V-cycle agrees bit for bit."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 73, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 74, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs = []
+    for mode in ("node", "row"):
+        dev = _device_with_env(P, {"PINT_SPMV32": mode, "PINT_TAIL_ROWS": tail_rows}, S)
         y = dev.to_device(Y)
         dev.assemble(y, y, k, th, t1)
         dev.precond_setup(S, KrylovSettings())

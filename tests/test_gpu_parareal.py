@@ -27,12 +27,12 @@ CASES = {
 }
 
 
-def _props(P, kf, kc, S):
+def _props(P, kf, kc, S, coarse_theta0=1.0):
     from paper_1907_01252_b200.propagator import FSIDevice, NewtonSettings, ThetaSettings, make_propagator
     dev = FSIDevice(P, S)
     nw = NewtonSettings(abs_tol=1e-10, rel_tol=1e-10)
     F = make_propagator(P, ThetaSettings(kf, 1.0, nw), device=dev)
-    C = make_propagator(P, ThetaSettings(kc, 1.0, nw), device=dev)
+    C = make_propagator(P, ThetaSettings(kc, coarse_theta0, nw), device=dev)
     return F, C
 
 
@@ -45,7 +45,7 @@ def _check_against_golden(case, variant, driver, tag=""):
     g = np.load(path)
     tol = float(g["tol"]) if "tol" in g else 1e-30
     P, t_end, kf, kc, L, K = CASES[case]
-    F, C = _props(P, kf, kc, L)
+    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
     s0 = initial_state(P)
     if driver == "device":
         cfg = PararealConfig(intervals=L, max_iters=K, tol=tol, variant=variant)
@@ -100,6 +100,18 @@ def test_c1_classic_matches_reference_driver_on_oracle(cuda):
     assert tr.fine_propagations == 10 * 5
 
 
+def test_c1_damped_coarse_propagator_converges(cuda):
+    """with the shifted-CN coarse propagator (theta_c = 1/2 +
+    K = 0.52, stability function -> -(1 - theta)/theta = -0.92 on stiff modes)
+    the c1 defects stall near 2 %; with a damped coarse propagator (theta_c =
+    1/2 + 25 K = 1, implicit Euler, R(inf) = 0) they fall every iteration.
+    Golden: the reference driver with the oracle propagators."""
+    tr = _check_against_golden("c1", "classic", "device", tag="_ct25")
+    worst = [max(row) for row in tr.correction_norms]
+    assert all(b < a for a, b in zip(worst, worst[1:])), worst
+    assert worst[-1] < 5e-3 * worst[0], worst  # classic coarse: 0.2 (0.123 -> 0.024)
+
+
 def test_exactness_frontier_with_gpu_fine(cuda):
     """Boundaries <= i of iteration i equal the sequential fine solution
     (reference test_parareal.py:217-224): needs a deterministic,
@@ -107,7 +119,7 @@ def test_exactness_frontier_with_gpu_fine(cuda):
     from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
-    F, C = _props(P, kf, kc, L)
+    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
     s0 = initial_state(P)
     grid = [t_end * l / L for l in range(L + 1)]
     seq = [s0]
@@ -134,7 +146,7 @@ def test_device_and_reference_drivers_agree(cuda):
     from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
-    F, C = _props(P, kf, kc, L)
+    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
     s0 = initial_state(P)
     for variant in ("classic", "least_squares", "angle_penalized"):
         a, ta = run_parareal_device(C, F, s0, t_end, PararealConfig(intervals=L, max_iters=2, tol=1e-30,
@@ -217,7 +229,7 @@ def test_pipelined_device_driver_equals_device_driver(cuda):
                                                   make_propagator)
     P, t_end, kf, kc, L, K = CASES["small"]
     nw = NewtonSettings(1e-10, 1e-10)
-    F, C = _props(P, kf, kc, L)
+    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
     s0 = initial_state(P)
     cfg = PararealConfig(intervals=L, max_iters=3, tol=1e-30)
     a, ta = run_parareal_device(C, F, s0, t_end, cfg)

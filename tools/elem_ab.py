@@ -1,7 +1,12 @@
 """A/B timing of the element kernels (K1 residual, K2' J w, K2 assembly) on
-BASELINE meshes with c5-type inputs: the tiled kernels (default) against the
-round-1 per-point kernels (PINT_ELEM=old; the Jacobian kernel has no switch).
-CUDA events, median of repeats, L2 flushed.  One JSON line per (config, variant)."""
+BASELINE meshes with c5-type inputs under environment switches (read at
+pint_create), e.g.
+
+  python tools/elem_ab.py --cases c3 c2 --variants "" PINT_JAC=colour PINT_ELEM=old
+
+CUDA events, median of repeats, L2 flushed.  One JSON line per case: times
+per variant and the max relative difference of r, J w and the assembled
+operator against the first variant."""
 import json
 import os
 import sys
@@ -35,15 +40,24 @@ def timed(fn, flush, reps=7):
 
 def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    for name in sys.argv[1:] or list(CASES):
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", nargs="+", default=list(CASES))
+    ap.add_argument("--variants", nargs="+", default=["", "PINT_ELEM=old"])
+    a = ap.parse_args()
+    for name in a.cases:
         P, S = CASES[name]
         out = {}
-        for var in ("new", "old"):
-            if var == "old":
-                os.environ["PINT_ELEM"] = "old"
-            else:
-                os.environ.pop("PINT_ELEM", None)
+        for var in a.variants:
+            env = dict(kv.split("=", 1) for kv in var.split())
+            saved = {k: os.environ.get(k) for k in env}
+            os.environ.update(env)
             dev = FSIDevice(P, S, restart=1)
+            for k_, v_ in saved.items():
+                if v_ is None:
+                    os.environ.pop(k_, None)
+                else:
+                    os.environ[k_] = v_
             # a small deformation keeps the random meshes admissible on every BASELINE mesh
             y = dev.to_device(0.05 * c5_random_states(P, S, 1))
             yo = dev.to_device(0.05 * c5_random_states(P, S, 2))
@@ -55,11 +69,13 @@ def main():
                    "assembly_ms": timed(lambda: dev.assemble(y, yo, k, th, t1), flush)}
             res["r"] = dev.to_host(r)
             res["jw"] = dev.to_host(jw)
-            out[var] = res
+            res["J"] = dev.jacobian_blocks(S)  # stays on the device
+            out[var or "default"] = res
             del dev
-            torch.cuda.empty_cache()
-        os.environ.pop("PINT_ELEM", None)
-        rel = {f: float(np.abs(out["new"][f] - out["old"][f]).max() / np.abs(out["old"][f]).max()) for f in ("r", "jw")}
+        keys = list(out)
+        ref = out[keys[0]]
+        rel = {v: {**{f: float(np.abs(out[v][f] - ref[f]).max() / np.abs(ref[f]).max()) for f in ("r", "jw")},
+                   "J": float((out[v]["J"] - ref["J"]).abs().max() / ref["J"].abs().max())} for v in keys[1:]}
         print(json.dumps({"case": name, "slices": S, "cells": P.num_cells,
                           **{f"{v}_{k}": out[v][k] for v in out for k in out[v] if k.endswith("_ms")},
                           "max_rel_diff": rel}), flush=True)

@@ -26,7 +26,8 @@ COLS = [
     ("dram_read_MB", "dram__bytes_read.sum"),
     ("dram_write_MB", "dram__bytes_write.sum"),
 ]
-SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3,
+         "us": 1.0, "ns": 1e-3, "ms": 1e3, "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
 
 
 def main():
