@@ -119,7 +119,7 @@ def test_exactness_frontier_with_gpu_fine(cuda):
     from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
-    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
+    F, C = _props(P, kf, kc, L)
     s0 = initial_state(P)
     grid = [t_end * l / L for l in range(L + 1)]
     seq = [s0]
@@ -146,7 +146,7 @@ def test_device_and_reference_drivers_agree(cuda):
     from paper_1907_01252_b200.parareal import PararealConfig, run_parareal_device
     from paper_1907_01252_b200.propagator import initial_state
     P, t_end, kf, kc, L, K = CASES["small"]
-    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
+    F, C = _props(P, kf, kc, L)
     s0 = initial_state(P)
     for variant in ("classic", "least_squares", "angle_penalized"):
         a, ta = run_parareal_device(C, F, s0, t_end, PararealConfig(intervals=L, max_iters=2, tol=1e-30,
@@ -229,7 +229,7 @@ def test_pipelined_device_driver_equals_device_driver(cuda):
                                                   make_propagator)
     P, t_end, kf, kc, L, K = CASES["small"]
     nw = NewtonSettings(1e-10, 1e-10)
-    F, C = _props(P, kf, kc, L, float(g["coarse_theta0"]) if "coarse_theta0" in g else 1.0)
+    F, C = _props(P, kf, kc, L)
     s0 = initial_state(P)
     cfg = PararealConfig(intervals=L, max_iters=3, tol=1e-30)
     a, ta = run_parareal_device(C, F, s0, t_end, cfg)
