@@ -1459,6 +1459,198 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_apply(Grid g, const 
   xout[o] = (FIRST ? 0.0 : xin[o]) + omega * z;
 }
 
+// ---------------------------------------------------------------- Vanka sweep in block-stencil form
+// One additive Vanka sweep is the LINEAR map  x += Sm r  with
+//   Sm = omega * W * sum_c P_c^T A_c^{-1} P_c ,   W = 1 / (cells sharing the node),
+// and Sm couples a node only to the nodes it shares a cell with: it is a
+// block stencil with the footprint of A itself (3^d offsets x C x C per node).
+// Assembled once per hierarchy build it replaces the 2^d C x 2^d C inverse of
+// every cell (2-d: 1600 B per cell) by 3^d C^2 fp32 coefficients per node
+// (2-d: 900 B) -- 0.56x the bytes of the dominant kernel of the fine step in
+// 2-d, 0.42x in 3-d -- and the sweep becomes one fp32 stencil product.
+//
+// k_vanka_stencil_build: thread = (node n, row comp ca).  For offset o = n' - n
+// and column comp cb the entry is the sum, in corner order a, over the cells
+// that hold n as corner a and n' as corner a + o, of A_c^{-1}[(a,ca)][(a+o,cb)]
+// (fp32 storage, summed in fp64), times omega / count(n), rounded once to
+// fp32.  Offsets without a common cell get an explicit zero (the sweep reads
+// every offset with a clamped neighbour index).  Deterministic, no atomics.
+template <int D>
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_build(Grid g, const float* __restrict__ Vinv,
+                                                                         float* __restrict__ Sm, double omega,
+                                                                         const int* __restrict__ active) {
+  pdl_wait();
+  constexpr int C = Cells<D>::C;
+  constexpr int A = Cells<D>::A;
+  constexpr int L = Cells<D>::L;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  if (n >= g.nn) return;
+  const int ca = threadIdx.y;
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+  const int cx = g.n[0] - 1, cy = g.n[1] - 1, cz = D == 3 ? g.n[2] - 1 : 1;
+  const int ncell = cx * cy * cz;
+  const float* Vs = Vinv + (size_t)s * L * L * ncell;
+  int cell_of[A];
+  int cnt = 0;
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+    const int ci = i - (a & 1), cj = j - ((a >> 1) & 1), ck = D == 3 ? k - ((a >> 2) & 1) : 0;
+    const bool ok = ci >= 0 && ci < cx && cj >= 0 && cj < cy && ck >= 0 && ck < cz;
+    cell_of[a] = ok ? (ck * cy + cj) * cx + ci : -1;
+    cnt += ok ? 1 : 0;
+  }
+  const double wgt = omega / cnt;
+  float* So = Sm + (size_t)s * NOFF * C * C * g.np + (size_t)ca * C * g.np + n;
+#pragma unroll 1
+  for (int o = 0; o < NOFF; ++o) {
+    int di, dj, dk;
+    offset_delta(o, D, di, dj, dk);
+    double acc[C];
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) acc[cb] = 0.0;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int bx = (a & 1) + di, by = ((a >> 1) & 1) + dj, bz = D == 3 ? ((a >> 2) & 1) + dk : 0;
+      if (cell_of[a] < 0 || bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+      const int b = bx + 2 * by + 4 * bz;
+      const float* Vr = Vs + ((size_t)(a * C + ca) * L + (size_t)b * C) * ncell + cell_of[a];
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) acc[cb] += (double)__ldg(Vr + (size_t)cb * ncell);
+    }
+#pragma unroll
+    for (int cb = 0; cb < C; ++cb) So[((size_t)o * C * C + cb) * g.np] = (float)(wgt * acc[cb]);
+  }
+}
+
+// x_out = x_in + Sm r  (FIRST: x_out = Sm r), fp32 arithmetic like the cell
+// form (k_vanka_cell / k_vanka_apply): thread = (node, row comp); the block's
+// residual neighbourhood (3^{D-1} node-row ranges of 34 nodes, all components,
+// converted to fp32) is staged in shared memory; the NOFF*C coefficients of
+// the row are loaded coalesced across the 32 nodes of the warp, in batches of
+// one offset plane (2-d: all 45 in flight; 3-d: 63), and accumulated into four
+// partial sums in a fixed order.  wsrc / hn / vout: the deferred basis scaling
+// of k_vanka_apply (v_j = w / h formed here, bitwise k_scale_inv).
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g, const float* __restrict__ Sm,
+                                                                         const double* __restrict__ r,
+                                                                         const double* __restrict__ xin,
+                                                                         double* __restrict__ xout,
+                                                                         const int* __restrict__ active,
+                                                                         unsigned long long* __restrict__ work,
+                                                                         const double* __restrict__ wsrc = nullptr,
+                                                                         const double* __restrict__ hn = nullptr,
+                                                                         double* __restrict__ vout = nullptr) {
+  pdl_wait();
+  constexpr int C = Cells<D>::C;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  double inv = 1.0;
+  if (wsrc) {
+    const double al = hn[blockIdx.y];
+    inv = al != 0.0 ? 1.0 / al : 0.0;
+    r = wsrc;
+  }
+  constexpr int R = D == 2 ? 3 : 9;
+  constexpr int W = 34;
+  __shared__ float rs[C][R][W];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  if (work && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(work, 1ULL);
+  const int n0 = blockIdx.x * 32;
+  const int nx = g.n[0], nxy = g.n[0] * g.n[1];
+  const double* rsl = r + (size_t)s * C * g.np;
+  for (int idx = threadIdx.y * 32 + threadIdx.x; idx < C * R * W; idx += 32 * C) {
+    const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
+    const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
+    const int m = n0 - 1 + w + dj * nx + dk * nxy;
+    rs[cb][q][w] = (m >= 0 && m < g.nn) ? (float)(wsrc ? rsl[(size_t)cb * g.np + m] * inv
+                                                         : __ldg(rsl + (size_t)cb * g.np + m))
+                                        : 0.0f;
+  }
+  __syncthreads();
+  const int n = n0 + threadIdx.x;
+  if (n >= g.nn) return;
+  const int ca = threadIdx.y;
+  const size_t ov = (size_t)s * C * g.np + (size_t)ca * g.np + n;
+  if (wsrc) vout[ov] = wsrc[ov] * inv;
+  const float* Sr = Sm + (size_t)s * NOFF * C * C * g.np + (size_t)ca * C * g.np + n;
+  float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int o0 = 0; o0 < NOFF; o0 += 9) {
+    float v[9][C];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) v[q][cb] = ld_nc(Sr + ((size_t)(o0 + q) * C * C + cb) * g.np);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int o = o0 + q;
+      const int di = o % 3 - 1, row = o / 3;  // row = (dj + 1) + 3 (dk + 1): the staged node-row range
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) p[cb & 3] = fmaf(v[q][cb], rs[cb][row][threadIdx.x + 1 + di], p[cb & 3]);
+    }
+  }
+  const double z = (double)((p[0] + p[1]) + (p[2] + p[3]));
+  xout[ov] = (FIRST ? 0.0 : xin[ov]) + z;
+}
+
+// r = b - A32 x with the neighbourhood of x staged in shared memory (fp64) and
+// thread = (node, row): the same loads per thread as k_vanka_stencil_apply.
+// Association order of stencil_row (offset o into partial o % 3, components in
+// order, (p0 + p1) + p2): bitwise k_spmv<D, true, *, float> and k_spmv_node.
+template <int D>
+__global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, const float* __restrict__ A,
+                                                                    const double* __restrict__ x,
+                                                                    const double* __restrict__ b,
+                                                                    double* __restrict__ y,
+                                                                    const int* __restrict__ active) {
+  pdl_wait();
+  constexpr int C = Cells<D>::C;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  constexpr int R = D == 2 ? 3 : 9;
+  constexpr int W = 34;
+  __shared__ double xs[C][R][W];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int n0 = blockIdx.x * 32;
+  const int nx = g.n[0], nxy = g.n[0] * g.n[1];
+  const double* xsl = x + (size_t)s * C * g.np;
+  for (int idx = threadIdx.y * 32 + threadIdx.x; idx < C * R * W; idx += 32 * C) {
+    const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
+    const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
+    const int m = n0 - 1 + w + dj * nx + dk * nxy;
+    xs[cb][q][w] = (m >= 0 && m < g.nn) ? __ldg(xsl + (size_t)cb * g.np + m) : 0.0;
+  }
+  __syncthreads();
+  const int n = n0 + threadIdx.x;
+  if (n >= g.nn) return;
+  const int ca = threadIdx.y;
+  const size_t ov = (size_t)s * C * g.np + (size_t)ca * g.np + n;
+  const double bv = __ldg(b + ov);
+  const float* Ar = A + (size_t)s * NOFF * C * C * g.np + (size_t)ca * C * g.np + n;
+  double part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int o0 = 0; o0 < NOFF; o0 += 9) {
+    float v[9][C];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) v[q][cb] = ld_nc(Ar + ((size_t)(o0 + q) * C * C + cb) * g.np);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int o = o0 + q;
+      const int di = o % 3 - 1, row = o / 3;
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb)
+        part[o % 3] = fma((double)v[q][cb], xs[cb][row][threadIdx.x + 1 + di], part[o % 3]);
+    }
+  }
+  y[ov] = bv - ((part[0] + part[1]) + part[2]);
+}
+
 }  // namespace pint
 
 // ======================================================================

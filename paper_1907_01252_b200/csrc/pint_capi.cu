@@ -53,6 +53,7 @@ struct Level {
   float* A32 = nullptr;    // fp32 copy of A for the V-cycle's residuals (preconditioner only; level 0 and
                            // the standalone coarse levels above the fused tail)
   float* vinv = nullptr;   // Vanka cell inverses [S][L*L][ncell], fp32 storage (preconditioner only)
+  float* vst = nullptr;    // Vanka sweep in block-stencil form [S][noff][C][C][np] (standalone levels; built from vinv)
   double* ycell = nullptr; // Vanka cell corrections [S][L][ncell]
   int ncell = 0;
 };
@@ -144,6 +145,10 @@ struct pint_ctx {
   bool pdl = true;              // PINT_PDL=0: launch without programmatic stream serialization
   bool jac_strip = true;        // PINT_JAC=colour: 2-d Jacobian by colour-ordered element scatter (k_jacobian_lin)
   bool spmv32_node = true;      // PINT_SPMV32=row: fp32 V-cycle residuals with one thread per (node, row)
+  bool spmv32_staged = true;    // PINT_SPMV32=node|row: without the shared-memory staged residual kernel
+  bool vanka_stencil = true;    // PINT_VANKA=fused|split: cell-inverse sweeps instead of the block-stencil form
+  size_t spmv32_min = (size_t)2 * 4 * 148 * 128;  // PINT_SPMV32_MIN: nodes x slices from which the staged / node
+                                                  // residual kernels replace the (node, row) one
   int tail_rows = 2048;         // PINT_TAIL_ROWS: first level of the fused V-cycle tail has <= this many rows
   int drift_num = 3;            // drift rebuild when 2 its > drift_num base + 4 (PINT_DRIFT; 0 = off)
   int tail_first = -1;   // first level handled by k_vcycle_tail (-1: none)
@@ -573,7 +578,10 @@ struct Impl {
     // node-per-thread kernel once the level fills >= 2 waves of 128-thread
     // CTAs (c3 levels 0-1: +4.6 %); below that the (node, row) threads hide
     // latency better (c2, L2-resident: -3 % with the node kernel)
-    if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= (size_t)2 * 4 * 148 * 128) {
+    if (L.A32 && ctx->spmv32_staged && (size_t)L.g.nn * S >= ctx->spmv32_min) {
+      pint_launch(ctx, st, k_resid32_staged<D>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, (const float*)L.A32, x, b, r,
+                  mask);
+    } else if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= ctx->spmv32_min) {
       pint_launch(ctx, st, k_spmv_node<D, true, float>, node_grid(L.g.nn, S), 128, 0, L.g, (const float*)L.A32, x, b, r,
                   mask);
     } else if (L.A32) {
@@ -657,6 +665,10 @@ struct Impl {
       } else {
         pint_launch(ctx, st, k_block_inverse<D>, node_grid(L.g.nn, S), 128, 0, L.g, L.A, L.Dinv, mask);
       }
+      // block-stencil form of the sweep on the levels that run standalone kernels
+      if (ko->smoother == 1 && !last_dense && ctx->vanka_stencil && L.vst)
+        pint_launch(ctx, st, k_vanka_stencil_build<D>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                    (const float*)L.vinv, L.vst, (double)ko->omega, mask);
     }
     if (ctx->coarse_dense) {
       Level& L = ctx->lv[nl - 1];
@@ -737,6 +749,28 @@ struct Impl {
         e0 = next_event(ctx);
         e1 = next_event(ctx);
         cudaEventRecord(e0, st);
+      }
+      if (ctx->vanka_stencil && L.vst) {
+        // the sweep as one fp32 block-stencil product (k_vanka_stencil_build at the hierarchy build)
+        if (first && ctx->defer_w && &L == &ctx->lv[0]) {
+          pint_launch(ctx, st, k_vanka_stencil_apply<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                      (const float*)L.vst, (const double*)ctx->defer_w, nullptr, xout, mask,
+                      prof ? ctx->d_work : nullptr, (const double*)ctx->defer_w, (const double*)ctx->gm_hnorm,
+                      const_cast<double*>(b));
+          ctx->defer_w = nullptr;
+        } else if (first)
+          pint_launch(ctx, st, k_vanka_stencil_apply<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                      (const float*)L.vst, r, nullptr, xout, mask, prof ? ctx->d_work : nullptr, nullptr, nullptr,
+                      nullptr);
+        else
+          pint_launch(ctx, st, k_vanka_stencil_apply<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                      (const float*)L.vst, r, xin, xout, mask, prof ? ctx->d_work : nullptr, nullptr, nullptr,
+                      nullptr);
+        if (prof) {
+          cudaEventRecord(e1, st);
+          ctx->ev_pairs.emplace_back(e0, e1);
+        }
+        return;
       }
       if (!ctx->vanka_split) {
         // fused cell solves + gather (bitwise the same as the split pair below)
@@ -997,7 +1031,9 @@ struct Impl {
         total += (unsigned long long)ctx->dense_n * ctx->dense_n * 4 + 2 * V;  // fp32 inverse
         continue;
       }
-      const unsigned long long cellb = (unsigned long long)L.ncell * ((unsigned long long)Lc * Lc * 4 + 2 * Lc * 8);
+      const unsigned long long cellb = (ctx->vanka_stencil && L.vst && (ctx->tail_first < 0 || l < ctx->tail_first))
+                                           ? (unsigned long long)L.g.noff * C * C * 4 * L.g.nn
+                                           : (unsigned long long)L.ncell * ((unsigned long long)Lc * Lc * 4 + 2 * Lc * 8);
       // first sweep + (pre-1 + post) full sweeps + restriction residual + transfers
       const int full = ctx->kopt.pre_smooth - 1 + ctx->kopt.post_smooth;
       total += (cellb + 2 * V) + full * (Ab + 2 * V + cellb + 2 * V) + (Ab + 2 * V) + 3 * V;
@@ -1894,11 +1930,19 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->host_beta = !(std::getenv("PINT_HOST_BETA") && std::getenv("PINT_HOST_BETA")[0] == '0');
   ctx->split_norm = std::getenv("PINT_SPLIT_NORM") && std::getenv("PINT_SPLIT_NORM")[0] == '1';
   ctx->vanka_split = ctx->D == 3;
-  if (const char* e = std::getenv("PINT_VANKA")) ctx->vanka_split = std::string(e) == "split";
+  // default since round 2: the sweep in block-stencil form (k_vanka_stencil_apply) on every standalone
+  // level; PINT_VANKA=fused|split select the cell-inverse kernels (the tail always uses cell inverses)
+  ctx->vanka_stencil = true;
+  if (const char* e = std::getenv("PINT_VANKA")) {
+    ctx->vanka_split = std::string(e) == "split";
+    ctx->vanka_stencil = std::string(e) == "stencil";
+  }
   if (const char* e = std::getenv("PINT_DRIFT")) ctx->drift_num = std::atoi(e);
   if (const char* e = std::getenv("PINT_TAIL_ROWS")) ctx->tail_rows = std::atoi(e);
   ctx->pdl = !(std::getenv("PINT_PDL") && std::getenv("PINT_PDL")[0] == '0');
   ctx->spmv32_node = !(std::getenv("PINT_SPMV32") && std::string(std::getenv("PINT_SPMV32")) == "row");
+  ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
+  if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
   if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
@@ -2048,6 +2092,27 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
       }
     }
   }
+  // Vanka sweeps in block-stencil form on the levels above the fused tail (the
+  // tail kernel keeps the cell inverses); without room for it the cell-inverse
+  // sweeps stay (PINT_VANKA=fused|split force them)
+  if (!ctx->matrix_free && ctx->vanka_stencil) {
+    for (size_t l = 0; l < ctx->lv.size(); ++l) {
+      Level& L = ctx->lv[l];
+      if ((l > 0 || ctx->use_tail) && (size_t)L.g.nn * C <= (size_t)ctx->tail_rows) break;
+      const size_t cnt = (size_t)S * L.g.noff * C * C * L.g.np;
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || cnt * sizeof(float) + (size_t(2) << 30) >= free_b)
+        break;
+      if (dalloc(ctx, &L.vst, cnt) != PINT_OK) {
+        L.vst = nullptr;
+        ctx->err.clear();
+        cudaGetLastError();
+        break;
+      }
+    }
+  }
+  if (ctx->lv.empty() || !ctx->lv[0].vst) ctx->vanka_stencil = false;
+  if (ctx->vanka_stencil) ctx->vanka_split = false;
   // device-driven control flow: per-slice loop state
   {
     LoopDev& d = ctx->ld;
@@ -2174,6 +2239,9 @@ const char* pint_profile_kernel(const pint_ctx* ctx) {
   if (ctx->tail_first == 0)
     return ctx->D == 2 ? "k_vcycle_tail_cl<2> (whole V-cycle: mesh fits the cluster tail)"
                        : "k_vcycle_tail_cl<3> (whole V-cycle: mesh fits the cluster tail)";
+  if (ctx->kopt.smoother == 1 && ctx->vanka_stencil)
+    return ctx->D == 2 ? "k_vanka_stencil_apply<2> (level-0 Vanka sweep as one fp32 block-stencil product)"
+                       : "k_vanka_stencil_apply<3> (level-0 Vanka sweep as one fp32 block-stencil product)";
   if (ctx->kopt.smoother == 1 && ctx->vanka_split)
     return ctx->D == 2 ? "k_vanka_cell<2,16> (level-0 cell-patch Vanka solves)"
                        : "k_vanka_cell<3,8> (level-0 cell-patch Vanka solves)";
@@ -2212,7 +2280,11 @@ int pint_profile_read(pint_ctx* ctx, int64_t* launches, int64_t* kernel_launches
   } else if (bytes_per_slice_launch) {
     const Grid& g = ctx->lv[0].g;
     const int64_t C = ctx->C;
-    if (ctx->kopt.smoother == 1 && ctx->vanka_split) {
+    if (ctx->kopt.smoother == 1 && ctx->vanka_stencil) {
+      // k_vanka_stencil_apply: fp32 stencil (noff C^2 per node) + residual in + x out (C per node each);
+      // the x_in read of the non-first sweeps is not counted (lower bound)
+      *bytes_per_slice_launch = (int64_t)g.nn * (4 * (int64_t)g.noff * C * C + 16 * C);
+    } else if (ctx->kopt.smoother == 1 && ctx->vanka_split) {
       // k_vanka_cell: cell inverses (L^2) + cell corrections (L) per cell, residual C per node
       const int64_t Lc = (int64_t)(1 << ctx->D) * C;
       *bytes_per_slice_launch = (int64_t)ctx->lv[0].ncell * (4 * Lc * Lc + 8 * Lc) + (int64_t)g.nn * 8 * C;

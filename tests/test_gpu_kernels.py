@@ -263,10 +263,13 @@ def test_vanka_fused_sweep_bitwise(cuda, name, tail_rows):
 
 
 @pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("small3d", "300")])
-def test_spmv32_node_bitwise(cuda, name, tail_rows):
-    """The V-cycle residuals with the fp32 operator copy: one thread per node
-    (k_spmv_node, default) and one per (node, row) (PINT_SPMV32=row) sum in
-    the same order, so the V-cycle agrees bit for bit."""
+def test_spmv32_variants_bitwise(cuda, name, tail_rows):
+    """The V-cycle residuals with the fp32 operator copy: (node, row) threads
+    over a shared-memory staged neighbourhood (k_resid32_staged, default on
+    wide levels), one thread per node (k_spmv_node) and one per (node, row)
+    with register gathers (k_spmv, PINT_SPMV32=row) sum in the same order, so
+    the V-cycle agrees bit for bit.  PINT_SPMV32_MIN=0 puts the wide-level
+    kernels on these small meshes."""
     from paper_1907_01252_b200.propagator import KrylovSettings
     P = PROBLEMS[name]
     S = 2
@@ -274,13 +277,42 @@ def test_spmv32_node_bitwise(cuda, name, tail_rows):
     B = random_states(P, S, 74, scale_u=1.0)
     k, th, t1 = _step_args(S)
     outs = []
-    for mode in ("node", "row"):
-        dev = _device_with_env(P, {"PINT_SPMV32": mode, "PINT_TAIL_ROWS": tail_rows}, S)
+    for mode in ("staged", "node", "row"):
+        dev = _device_with_env(P, {"PINT_SPMV32": mode, "PINT_SPMV32_MIN": "0", "PINT_TAIL_ROWS": tail_rows}, S)
         y = dev.to_device(Y)
         dev.assemble(y, y, k, th, t1)
         dev.precond_setup(S, KrylovSettings())
         outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
-    assert np.array_equal(outs[0], outs[1]), name
+    assert np.array_equal(outs[0], outs[2]), name
+    assert np.array_equal(outs[1], outs[2]), name
+
+
+@pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("c1", "100"), ("small3d", "300")])
+def test_vanka_stencil_sweep_matches_cell_form(cuda, name, tail_rows):
+    """The Vanka sweep in block-stencil form (k_vanka_stencil_build once per
+    hierarchy build + k_vanka_stencil_apply, default) is the same linear map
+    as the cell-inverse sweep (k_vanka_apply, PINT_VANKA=fused) up to fp32
+    rounding of the summed coefficients: one V-cycle agrees to 1e-5, and a
+    preconditioned solve to rtol 1e-8 takes the same number of iterations up
+    to rounding (within 3; the bench configs' counts are identical)."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 75, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 76, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs, its = [], []
+    for mode in ("stencil", "fused"):
+        dev = _device_with_env(P, {"PINT_VANKA": mode, "PINT_TAIL_ROWS": tail_rows}, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+        x, it, _ = dev.linear_solve(dev.to_device(B), KrylovSettings(rtol=1e-8))
+        its.append(list(it))
+    for s in range(S):
+        assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[1][s]), (name, s)
+    assert max(abs(int(a) - int(b)) for a, b in zip(its[0], its[1])) <= 3, (name, its)
 
 
 @pytest.mark.parametrize("name", ["c1", "small3d"])
