@@ -1924,12 +1924,19 @@ namespace pint {
 #ifndef PINT_TAIL_P3
 #define PINT_TAIL_P3 8  // (3-d)
 #endif
+#ifndef PINT_TAIL_PV2
+#define PINT_TAIL_PV2 2  // lanes per row of the tail's stencil-form Vanka sweep (2-d; measured 1 / 2 / 4: c1 7500 / 8026 / 7804, c2 7714 / 7949 / 8010)
+#endif
+#ifndef PINT_TAIL_PV3
+#define PINT_TAIL_PV3 8  // (3-d; 4 / 8: c4 859 / 875)
+#endif
 constexpr int kMaxLevels = 12;
 
 struct LevelDev {
   Grid g;
   const double* A;
   const float* vinv;
+  const float* vst;  // Vanka sweep in block-stencil form (nullptr: cell inverses)
   double* rhs;
   double* xa;
   double* xb;
@@ -2039,6 +2046,56 @@ __device__ __forceinline__ void tail_vanka_apply(const LevelDev& L, int s, const
     }
     const size_t o = (size_t)s * C * np + (size_t)c * np + n;
     xout[o] = (first ? 0.0 : xin[o]) + omega * (acc / cnt);
+  }
+}
+
+// the same sweep in block-stencil form (L.vst, k_vanka_stencil_build): P lanes
+// per row as in tail_spmv_resid, each with every P-th offset and all its loads
+// in flight, fp32 arithmetic, xor butterfly -- one round of memory latency per
+// row and 3^d C instead of 2^d 2^d C coefficients
+template <int D>
+__device__ __forceinline__ void tail_vanka_stencil(const LevelDev& L, int s, const double* r, const double* xin,
+                                                   double* xout, bool first, int tid, int nth) {
+  constexpr int C = 2 * D + 1;
+  constexpr int NOFF = D == 2 ? 9 : 27;
+  constexpr int P = D == 2 ? PINT_TAIL_PV2 : PINT_TAIL_PV3;
+  constexpr int OPL = (NOFF + P - 1) / P;
+  const int np = L.g.np;
+  const size_t vs = (size_t)C * np;
+  const int total = L.g.nn * C * P;
+  const int part = tid % P;
+  const double* rs = r + s * vs;
+  for (int base = 0; base < total; base += nth) {
+    const int idx = base + tid;
+    const bool ok = idx < total;
+    const int row = ok ? idx / P : 0;
+    const int ca = row / L.g.nn, n = row % L.g.nn;
+    int i, j, k;
+    node_coords(L.g, n, i, j, k);
+    const float* Srow = L.vst + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + n;
+    float a[OPL][C];
+    double rv[OPL][C];
+#pragma unroll
+    for (int q = 0; q < OPL; ++q) {
+      const int off = part + P * q;
+      const int nb = (ok && off < NOFF) ? neighbour(L.g, i, j, k, off) : -1;
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) {
+        a[q][cb] = nb >= 0 ? ld_nc(Srow + ((size_t)off * C * C + cb) * np) : 0.0f;
+        rv[q][cb] = nb >= 0 ? ld_nc(rs + cb * np + nb) : 0.0;
+      }
+    }
+    float acc = 0.0f;
+#pragma unroll
+    for (int q = 0; q < OPL; ++q)
+#pragma unroll
+      for (int cb = 0; cb < C; ++cb) acc = fmaf(a[q][cb], (float)rv[q][cb], acc);
+#pragma unroll
+    for (int o = P / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (ok && part == 0) {
+      const size_t o = s * vs + (size_t)ca * np + n;
+      xout[o] = (first ? 0.0 : xin[o]) + (double)acc;
+    }
   }
 }
 
@@ -2187,7 +2244,8 @@ __device__ __forceinline__ void tail_sweep(const LevelDev& L, int s, const doubl
     tail_sync<CL>();
     r = L.res;
   }
-  tail_vanka_apply<D>(L, s, r, xin, xout, omega, first, tid, nth);
+  if (L.vst) tail_vanka_stencil<D>(L, s, r, xin, xout, first, tid, nth);
+  else tail_vanka_apply<D>(L, s, r, xin, xout, omega, first, tid, nth);
   tail_sync<CL>();
 }
 

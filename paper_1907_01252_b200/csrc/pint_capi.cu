@@ -215,8 +215,11 @@ struct pint_ctx {
 static inline int tail_cluster_size(const pint_ctx* ctx, int S) {
   if (!ctx->tail_cluster) return 1;
   if (ctx->tail_cl_force) return ctx->tail_cl_force;
-  for (int cl = 8; cl >= 2; cl /= 2)
-    if (S * cl <= ctx->num_sms) return cl;
+  // measured (profiles/r02_tail_cluster_ab.jsonl): 4 CTAs per slice beat 8 and 2 on c2 (S = 32), c3 (S = 64,
+  // two CTAs per SM) and c4 (S = 16); 8 for small batches (c1 S = 10: 7720 vs 6750)
+  if (S * 8 <= 96) return 8;  // c1 (S = 10) and the batch-1 coarse sweeps: 8 beats 4 by 14 %
+  if (S * 4 <= 2 * ctx->num_sms) return 4;
+  if (S * 2 <= 2 * ctx->num_sms) return 2;
   return 1;
 }
 
@@ -695,7 +698,7 @@ struct Impl {
         TailArgs& t = ctx->tail;
         for (int l = 0; l < nl; ++l) {
           Level& L = ctx->lv[l];
-          t.lv[l] = LevelDev{L.g, L.A, L.vinv, L.rhs, L.xa, L.xb, L.res, L.sol, L.ycell, L.ncell};
+          t.lv[l] = LevelDev{L.g, L.A, L.vinv, ctx->vanka_stencil ? L.vst : nullptr, L.rhs, L.xa, L.xb, L.res, L.sol, L.ycell, L.ncell};
         }
         t.first = ctx->tail_first;
         t.last = nl - 1;
@@ -2092,13 +2095,12 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
       }
     }
   }
-  // Vanka sweeps in block-stencil form on the levels above the fused tail (the
-  // tail kernel keeps the cell inverses); without room for it the cell-inverse
-  // sweeps stay (PINT_VANKA=fused|split force them)
+  // Vanka sweeps in block-stencil form on every level (standalone kernels and
+  // the fused tail); without room for it the cell-inverse sweeps stay
+  // (PINT_VANKA=fused|split force them)
   if (!ctx->matrix_free && ctx->vanka_stencil) {
     for (size_t l = 0; l < ctx->lv.size(); ++l) {
       Level& L = ctx->lv[l];
-      if ((l > 0 || ctx->use_tail) && (size_t)L.g.nn * C <= (size_t)ctx->tail_rows) break;
       const size_t cnt = (size_t)S * L.g.noff * C * C * L.g.np;
       size_t free_b = 0, total_b = 0;
       if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || cnt * sizeof(float) + (size_t(2) << 30) >= free_b)
