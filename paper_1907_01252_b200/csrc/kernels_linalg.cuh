@@ -96,10 +96,32 @@ __device__ __forceinline__ float ld_nc(const float* p) {
 // all 2*C*NOFF loads of the row are put in flight before any FMA.
 template <int D, int BATCH, typename MT = double>
 __device__ __forceinline__ double stencil_row(const MT* __restrict__ Arow, const double* __restrict__ xs, int np,
-                                              const int (&nbs)[D == 2 ? 9 : 27]) {
+                                              const int (&nbs)[D == 2 ? 9 : 27], int ca) {
   constexpr int C = 2 * D + 1;
   constexpr int NOFF = D == 2 ? 9 : 27;
   double part[3] = {0.0, 0.0, 0.0};
+  if (is_urow(ca, D)) {
+    // deformation row: only the v_i and u_i planes are structurally non-zero (row_couples)
+    const int c0 = ca - D, c1 = ca;
+#pragma unroll
+    for (int o0 = 0; o0 < NOFF; o0 += BATCH) {
+      MT a[BATCH][2];
+      double xv[BATCH][2];
+#pragma unroll
+      for (int q = 0; q < BATCH; ++q) {
+        a[q][0] = ld_nc(Arow + ((size_t)(o0 + q) * C * C + c0) * np);
+        xv[q][0] = ld_nc(xs + c0 * np + nbs[o0 + q]);
+        a[q][1] = ld_nc(Arow + ((size_t)(o0 + q) * C * C + c1) * np);
+        xv[q][1] = ld_nc(xs + c1 * np + nbs[o0 + q]);
+      }
+#pragma unroll
+      for (int q = 0; q < BATCH; ++q) {
+        part[q % 3] = fma((double)a[q][0], xv[q][0], part[q % 3]);
+        part[q % 3] = fma((double)a[q][1], xv[q][1], part[q % 3]);
+      }
+    }
+    return (part[0] + part[1]) + part[2];
+  }
 #pragma unroll
   for (int o0 = 0; o0 < NOFF; o0 += BATCH) {
     MT a[BATCH][C];
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
   const double* xs = x + s * vs;
   int nbs[NOFF];
   stencil_neighbours<D>(g, n, nbs);
-  const double acc = stencil_row<D, BATCH, MT>(As, xs, np, nbs);
+  const double acc = stencil_row<D, BATCH, MT>(As, xs, np, nbs, ca);
   const size_t o = s * vs + (size_t)ca * np + n;
   y[o] = RESID ? b[o] - acc : acc;
 }
@@ -371,11 +393,13 @@ __global__ void __launch_bounds__(128) k_spmv_node(Grid g, const MT* __restrict_
 #pragma unroll
     for (int ca = 0; ca < C; ++ca)
 #pragma unroll
-      for (int cb = 0; cb < C; ++cb) a[ca][cb] = ld_nc(As + ((size_t)(o * C + ca) * C + cb) * np);
+      for (int cb = 0; cb < C; ++cb)
+        if (row_couples(ca, cb, D)) a[ca][cb] = ld_nc(As + ((size_t)(o * C + ca) * C + cb) * np);
 #pragma unroll
     for (int ca = 0; ca < C; ++ca)
 #pragma unroll
-      for (int cb = 0; cb < C; ++cb) part[ca][o % 3] = fma((double)a[ca][cb], xv[cb], part[ca][o % 3]);
+      for (int cb = 0; cb < C; ++cb)
+        if (row_couples(ca, cb, D)) part[ca][o % 3] = fma((double)a[ca][cb], xv[cb], part[ca][o % 3]);
   }
 #pragma unroll
   for (int ca = 0; ca < C; ++ca) {
@@ -456,7 +480,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1), (StencilOcc<D, BATCH>::value
       const double* xs = xin + s * vs;
       int nbs[NOFF];
       stencil_neighbours<D>(g, n, nbs);
-      const double acc = stencil_row<D, BATCH>(As, xs, np, nbs);
+      const double acc = stencil_row<D, BATCH>(As, xs, np, nbs, ca);
       res -= acc;
     }
   }
@@ -1601,17 +1625,26 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g
 // thread = (node, row): the same loads per thread as k_vanka_stencil_apply.
 // Association order of stencil_row (offset o into partial o % 3, components in
 // order, (p0 + p1) + p2): bitwise k_spmv<D, true, *, float> and k_spmv_node.
-template <int D>
+// PROLONG: the coarse-grid correction is added on the way in -- the staged
+// value is x + (P e)(node) with k_prolong_add's arithmetic (prolong_sum, same
+// order), the block's own nodes write it to xnew (out of place: other blocks
+// still read the old x of their halo nodes), and the residual is that of the
+// corrected iterate: bitwise k_prolong_add followed by the plain kernel, one
+// launch and one read + write of x fewer per level and V-cycle.
+template <int D, bool PROLONG>
 __global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, const float* __restrict__ A,
                                                                     const double* __restrict__ x,
                                                                     const double* __restrict__ b,
                                                                     double* __restrict__ y,
-                                                                    const int* __restrict__ active) {
+                                                                    const int* __restrict__ active, Grid gc,
+                                                                    const double* __restrict__ ec,
+                                                                    double* __restrict__ xnew) {
   pdl_wait();
   constexpr int C = Cells<D>::C;
   constexpr int NOFF = D == 2 ? 9 : 27;
   constexpr int R = D == 2 ? 3 : 9;
   constexpr int W = 34;
+  constexpr int RC = D == 2 ? 1 : 4;  // the centre node-row range (dj = dk = 0)
   __shared__ double xs[C][R][W];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
@@ -1622,7 +1655,17 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, con
     const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
     const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
     const int m = n0 - 1 + w + dj * nx + dk * nxy;
-    xs[cb][q][w] = (m >= 0 && m < g.nn) ? __ldg(xsl + (size_t)cb * g.np + m) : 0.0;
+    double v = 0.0;
+    if (m >= 0 && m < g.nn) {
+      v = __ldg(xsl + (size_t)cb * g.np + m);
+      if constexpr (PROLONG) {
+        int fi, fj, fk;
+        node_coords(g, m, fi, fj, fk);
+        v = v + prolong_sum<D>(gc, ec + (size_t)s * C * gc.np + (size_t)cb * gc.np, fi, fj, fk);
+        if (q == RC && w >= 1 && w <= 32) xnew[(size_t)s * C * g.np + (size_t)cb * g.np + m] = v;
+      }
+    }
+    xs[cb][q][w] = v;
   }
   __syncthreads();
   const int n = n0 + threadIdx.x;
@@ -1632,6 +1675,24 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, con
   const double bv = __ldg(b + ov);
   const float* Ar = A + (size_t)s * NOFF * C * C * g.np + (size_t)ca * C * g.np + n;
   double part[3] = {0.0, 0.0, 0.0};
+  if (is_urow(ca, D)) {
+    // deformation row: the v_i and u_i planes only (row_couples), all NOFF offsets in flight
+    const int c0 = ca - D, c1 = ca;
+    float v[NOFF][2];
+#pragma unroll
+    for (int o = 0; o < NOFF; ++o) {
+      v[o][0] = ld_nc(Ar + ((size_t)o * C * C + c0) * g.np);
+      v[o][1] = ld_nc(Ar + ((size_t)o * C * C + c1) * g.np);
+    }
+#pragma unroll
+    for (int o = 0; o < NOFF; ++o) {
+      const int di = o % 3 - 1, row = o / 3;
+      part[o % 3] = fma((double)v[o][0], xs[c0][row][threadIdx.x + 1 + di], part[o % 3]);
+      part[o % 3] = fma((double)v[o][1], xs[c1][row][threadIdx.x + 1 + di], part[o % 3]);
+    }
+    y[ov] = bv - ((part[0] + part[1]) + part[2]);
+    return;
+  }
 #pragma unroll
   for (int o0 = 0; o0 < NOFF; o0 += 9) {
     float v[9][C];
@@ -1988,8 +2049,9 @@ __device__ __forceinline__ void tail_spmv_resid(const LevelDev& L, int s, const 
       const int nb = (ok && off < NOFF) ? neighbour(L.g, i, j, k, off) : -1;
 #pragma unroll
       for (int cb = 0; cb < C; ++cb) {
-        a[q][cb] = nb >= 0 ? ld_nc(Arow + ((size_t)off * C * C + cb) * np) : 0.0;
-        xv[q][cb] = nb >= 0 ? ld_nc(xs + cb * np + nb) : 0.0;
+        const bool use = nb >= 0 && row_couples(ca, cb, D);  // structural zeros are not loaded
+        a[q][cb] = use ? ld_nc(Arow + ((size_t)off * C * C + cb) * np) : 0.0;
+        xv[q][cb] = use ? ld_nc(xs + cb * np + nb) : 0.0;
       }
     }
     double acc = 0.0;
@@ -2419,7 +2481,7 @@ __device__ __forceinline__ void arnoldi_body(const ArnoldiArgs& a) {
       int nbs[NOFF];
       stencil_neighbours<D>(L0.g, nd, nbs);
       const double* Arow = L0.A + (size_t)s * NOFF * C * C * np + (size_t)ca * C * np + nd;
-      a.w[s * n + (size_t)ca * np + nd] = stencil_row<D, 3>(Arow, zj + s * n, np, nbs);
+      a.w[s * n + (size_t)ca * np + nd] = stencil_row<D, 3>(Arow, zj + s * n, np, nbs, ca);
     }
   }
   tail_sync<CL>();

@@ -146,6 +146,8 @@ struct pint_ctx {
   bool jac_strip = true;        // PINT_JAC=colour: 2-d Jacobian by colour-ordered element scatter (k_jacobian_lin)
   bool spmv32_node = true;      // PINT_SPMV32=row: fp32 V-cycle residuals with one thread per (node, row)
   bool spmv32_staged = true;    // PINT_SPMV32=node|row: without the shared-memory staged residual kernel
+  bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
+                                // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
   bool vanka_stencil = true;    // PINT_VANKA=fused|split: cell-inverse sweeps instead of the block-stencil form
   size_t spmv32_min = (size_t)2 * 4 * 148 * 128;  // PINT_SPMV32_MIN: nodes x slices from which the staged / node
                                                   // residual kernels replace the (node, row) one
@@ -574,6 +576,11 @@ struct Impl {
     return PINT_OK;
   }
 
+  // the shared-memory staged fp32 residual kernel runs on this level
+  static bool resid_staged(const pint_ctx* ctx, const Level& L, int S) {
+    return L.A32 && ctx->spmv32_staged && (size_t)L.g.nn * S >= ctx->spmv32_min;
+  }
+
   // V-cycle residual r = b - A x on level L (fp32 operator copy on level 0 when present)
   static void vc_resid(pint_ctx* ctx, const Level& L, int S, const double* x, const double* b, double* r,
                        const int* mask, cudaStream_t st) {
@@ -581,9 +588,9 @@ struct Impl {
     // node-per-thread kernel once the level fills >= 2 waves of 128-thread
     // CTAs (c3 levels 0-1: +4.6 %); below that the (node, row) threads hide
     // latency better (c2, L2-resident: -3 % with the node kernel)
-    if (L.A32 && ctx->spmv32_staged && (size_t)L.g.nn * S >= ctx->spmv32_min) {
-      pint_launch(ctx, st, k_resid32_staged<D>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, (const float*)L.A32, x, b, r,
-                  mask);
+    if (resid_staged(ctx, L, S)) {
+      pint_launch(ctx, st, k_resid32_staged<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                  (const float*)L.A32, x, b, r, mask, L.g, (const double*)nullptr, (double*)nullptr);
     } else if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= ctx->spmv32_min) {
       pint_launch(ctx, st, k_spmv_node<D, true, float>, node_grid(L.g.nn, S), 128, 0, L.g, (const float*)L.A32, x, b, r,
                   mask);
@@ -736,14 +743,15 @@ struct Impl {
     return PINT_OK;
   }
 
+  // resid_done: L.res already holds b - A xin (the fused prolongation + residual kernel)
   static void smooth(pint_ctx* ctx, const Level& L, int S, const double* b, const double* xin, double* xout,
-                     const int* mask, cudaStream_t st, bool first) {
+                     const int* mask, cudaStream_t st, bool first, bool resid_done = false) {
     const double om = ctx->kopt.omega;
     if (ctx->kopt.smoother == 1) {
       constexpr int CELLS = D == 2 ? 16 : 8;
       const double* r = b;
       if (!first) {
-        vc_resid(ctx, L, S, xin, b, L.res, mask, st);
+        if (!resid_done) vc_resid(ctx, L, S, xin, b, L.res, mask, st);
         r = L.res;
       }
       const bool prof = ctx->prof && &L == &ctx->lv[0];
@@ -897,6 +905,14 @@ struct Impl {
     pint_launch(ctx, st, k_restrict<D>, row_grid(Lc.g.nn, S), row_block<D>(), 0, L.g, Lc.g, L.res, Lc.rhs, mask);
     double* xc = Lc.sol;
     vcycle(ctx, l + 1, S, Lc.rhs, xc, mask, st);
+    if (ctx->fuse_prolong && post == 1 && ko.smoother == 1 && resid_staged(ctx, L, S)) {
+      // coarse-grid correction inside the post-smoothing residual: x' = cur + P xc goes to nxt (out of
+      // place), L.res = b - A x' (bitwise k_prolong_add + the plain residual; PINT_FUSE_PROLONG=1, off by default)
+      pint_launch(ctx, st, k_resid32_staged<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+                  (const float*)L.A32, (const double*)cur, b, L.res, mask, Lc.g, (const double*)xc, nxt);
+      smooth(ctx, L, S, b, nxt, x, mask, st, false, true);
+      return;
+    }
     pint_launch(ctx, st, k_prolong_add<D>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g, Lc.g, xc, cur, mask);
     for (int i = 0; i < post; ++i) {
       double* out = (i == post - 1) ? x : nxt;
@@ -1029,7 +1045,8 @@ struct Impl {
       const Level& L = ctx->lv[l];
       const unsigned long long V = (unsigned long long)C * 8 * L.g.nn;
       // the V-cycle residuals read the fp32 copy of level 0 when it exists
-      const unsigned long long Ab = (unsigned long long)L.g.noff * C * C * (L.A32 ? 4 : 8) * L.g.nn;
+      // structurally non-zero coefficient planes only (row_couples: the deformation rows hold 2 of C)
+      const unsigned long long Ab = (unsigned long long)L.g.noff * (C * C - D * (C - 2)) * (L.A32 ? 4 : 8) * L.g.nn;
       if (l == nl - 1 && ctx->coarse_dense) {
         total += (unsigned long long)ctx->dense_n * ctx->dense_n * 4 + 2 * V;  // fp32 inverse
         continue;
@@ -1048,7 +1065,7 @@ struct Impl {
   static unsigned long long arnoldi_bytes(pint_ctx* ctx, int j) {
     unsigned long long total = vcycle_bytes(ctx, 0);
     const unsigned long long V0 = (unsigned long long)C * 8 * ctx->lv[0].g.nn;
-    const unsigned long long A0 = (unsigned long long)ctx->lv[0].g.noff * C * C * 8 * ctx->lv[0].g.nn;
+    const unsigned long long A0 = (unsigned long long)ctx->lv[0].g.noff * (C * C - D * (C - 2)) * 8 * ctx->lv[0].g.nn;
     total += A0 + 2 * V0;                          // w = J z
     total += 2 * (2ULL * (j + 1) * V0 + 2 * V0);   // CGS2: two dot passes + two updates
     total += 3 * V0;                               // norm + scale
@@ -1946,6 +1963,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_node = !(std::getenv("PINT_SPMV32") && std::string(std::getenv("PINT_SPMV32")) == "row");
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
+  ctx->fuse_prolong = std::getenv("PINT_FUSE_PROLONG") && std::getenv("PINT_FUSE_PROLONG")[0] == '1';
   if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||

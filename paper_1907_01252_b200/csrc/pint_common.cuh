@@ -58,6 +58,23 @@ PINT_HD void offset_delta(int off, int dim, int& di, int& dj, int& dk) {
 
 PINT_HD int center_offset(int dim) { return dim == 2 ? 4 : 13; }
 
+// Structural zeros of the block-stencil operators.  A deformation row u_i --
+// harmonic extension k (theta grad u_i^n + (1 - theta) grad u_i^{n-1}, grad psi) on
+// fluid nodes, kinematic condition (u_i^n - u_i^{n-1}) - k (theta v_i^n + ...) on
+// solid nodes, identity on fixed dofs (fsi_qfunc.cuh: uvec / uten) -- couples
+// only to u_i and v_i, at every stencil offset; the Galerkin products keep the
+// pattern (the transfers act per component).  The C - 2 other coefficient planes
+// of such a row are exact zeros, which the product kernels neither load nor
+// multiply (24 % of the operator in 2-d, 31 % in 3-d; a skipped term would add
+// fma(0, x, acc) = acc, so the results are bitwise those of the full loops).
+// tests/test_gpu_kernels.py::test_deformation_rows_structural_zeros checks
+// the assembled planes.  -DPINT_PATTERN=0 restores the full loops.
+#ifndef PINT_PATTERN
+#define PINT_PATTERN 1
+#endif
+PINT_HD constexpr bool is_urow(int ca, int dim) { return PINT_PATTERN && ca >= dim && ca < 2 * dim; }
+PINT_HD constexpr bool row_couples(int ca, int cb, int dim) { return !is_urow(ca, dim) || cb == ca || cb == ca - dim; }
+
 // neighbour index or -1 when outside the grid
 PINT_HD int neighbour(const Grid& g, int i, int j, int k, int off) {
   int di, dj, dk;

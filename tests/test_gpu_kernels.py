@@ -240,6 +240,37 @@ def test_vanka_setup_variants_agree(cuda, name):
         assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[1][s]), (name, s)
 
 
+@pytest.mark.parametrize("name", ["small2d", "c1", "small3d"])
+def test_deformation_rows_structural_zeros(devices, name):
+    """The product kernels skip the coefficient planes (u_i row, column other
+    than v_i / u_i) as structural zeros (pint_common.cuh row_couples): the
+    assembled Jacobian must hold exact zeros there at every stencil offset,
+    for fluid, solid and interface nodes, and the oracle's sparse Jacobian has
+    no entry there either."""
+    P, dev = PROBLEMS[name], devices[name]
+    S = 2
+    Y = random_states(P, S, 81)
+    Yo = random_states(P, S, 82)
+    k, th, t1 = _step_args(S)
+    dev.assemble(dev.to_device(Y), dev.to_device(Yo), k, th, t1)
+    blocks = dev.jacobian_blocks(S).cpu().numpy()  # [S][noff][ca][cb][np]
+    d, C = P.dim, P.dofs_per_node
+    assert np.abs(blocks).max() > 0.0
+    for i in range(d):
+        for cb in range(C):
+            if cb in (i, d + i):
+                assert np.abs(blocks[:, :, d + i, cb, :]).max() > 0.0
+            else:
+                assert not blocks[:, :, d + i, cb, :].any(), (name, i, cb)
+    J = O.jacobian(P, Y[0], Yo[0], k[0], th[0], t1[0]).tocoo()
+    n = P.num_nodes
+    rows_c, cols_c = J.row // n, J.col // n
+    nz = J.data != 0.0
+    for i in range(d):
+        bad = nz & (rows_c == d + i) & (cols_c != i) & (cols_c != d + i)
+        assert not bad.any(), (name, i)
+
+
 @pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("small3d", "300")])
 def test_vanka_fused_sweep_bitwise(cuda, name, tail_rows):
     """The fused level-0 Vanka sweep (k_vanka_apply: cell solves + gather in
@@ -285,6 +316,28 @@ def test_spmv32_variants_bitwise(cuda, name, tail_rows):
         outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
     assert np.array_equal(outs[0], outs[2]), name
     assert np.array_equal(outs[1], outs[2]), name
+
+
+@pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("c1", "100"), ("small3d", "300")])
+def test_fused_prolongation_bitwise(cuda, name, tail_rows):
+    """The coarse-grid correction added inside the post-smoothing residual
+    kernel (k_resid32_staged<PROLONG>, PINT_FUSE_PROLONG=1; measured slower, off) equals
+    k_prolong_add followed by the plain residual (default) bit for
+    bit: same prolongation sum, same residual order."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 77, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 78, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs = []
+    for fuse in ("1", "0"):
+        dev = _device_with_env(P, {"PINT_FUSE_PROLONG": fuse, "PINT_SPMV32_MIN": "0", "PINT_TAIL_ROWS": tail_rows}, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+    assert np.array_equal(outs[0], outs[1]), name
 
 
 @pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("c1", "100"), ("small3d", "300")])
