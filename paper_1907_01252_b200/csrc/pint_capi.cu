@@ -146,6 +146,7 @@ struct pint_ctx {
   bool jac_strip = true;        // PINT_JAC=colour: 2-d Jacobian by colour-ordered element scatter (k_jacobian_lin)
   bool spmv32_node = true;      // PINT_SPMV32=row: fp32 V-cycle residuals with one thread per (node, row)
   bool spmv32_staged = true;    // PINT_SPMV32=node|row: without the shared-memory staged residual kernel
+  int strip_w = 25;             // PINT_STRIP_W: owned node columns per Jacobian strip (<= 31)
   bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
                                 // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
   bool vanka_stencil = true;    // PINT_VANKA=fused|split: cell-inverse sweeps instead of the block-stencil form
@@ -534,7 +535,10 @@ struct Impl {
           attr = true;
         }
         const int nxn = ctx->cells[0] + 1, nyn = ctx->cells[1] + 1;
-        const int nstrips = (nxn + JacStrip::WMAX - 1) / JacStrip::WMAX;
+        // owned node columns per strip: <= 25 keeps the W * C phase-2 items of a row within one round of the
+        // 128 threads (31 needs two, the second nearly empty); PINT_STRIP_W overrides
+        const int wmax = std::max(1, std::min(ctx->strip_w, (int)JacStrip::WMAX));
+        const int nstrips = (nxn + wmax - 1) / wmax;
         const int W = (nxn + nstrips - 1) / nstrips;
         // enough blocks for ~8 waves at 3 CTAs/SM; each chunk recomputes one halo cell row
         const int base = nstrips * C * S;
@@ -1963,6 +1967,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_node = !(std::getenv("PINT_SPMV32") && std::string(std::getenv("PINT_SPMV32")) == "row");
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
+  if (const char* e = std::getenv("PINT_STRIP_W")) ctx->strip_w = std::atoi(e);
   ctx->fuse_prolong = std::getenv("PINT_FUSE_PROLONG") && std::getenv("PINT_FUSE_PROLONG")[0] == '1';
   if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
