@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=4)
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--variant", default="classic")
+    ap.add_argument("--coarse-theta0", type=float, default=None,
+                    help="theta0 of the coarse propagator (theta = 1/2 + theta0 K; 0.5 / K = implicit Euler)")
     ap.add_argument("--stab-k", type=float, default=None, help="fixed stabilization time scale (h/U if 0)")
     a = ap.parse_args()
     rc = CONFIGS[a.config]
@@ -38,10 +40,11 @@ def main():
     nw = NewtonSettings(1e-10, 1e-10)
     dev = FSIDevice(P, rc.intervals)
     F = make_propagator(P, ThetaSettings(rc.fine_step, rc.theta0, nw), device=dev)
+    ct0 = rc.theta0 if a.coarse_theta0 is None else a.coarse_theta0
     if a.driver == "pipelined":
-        C = make_propagator(P, ThetaSettings(rc.coarse_step, rc.theta0, nw), device=FSIDevice(P, 1))
+        C = make_propagator(P, ThetaSettings(rc.coarse_step, ct0, nw), device=FSIDevice(P, 1))
     else:
-        C = make_propagator(P, ThetaSettings(rc.coarse_step, rc.theta0, nw), device=dev)
+        C = make_propagator(P, ThetaSettings(rc.coarse_step, ct0, nw), device=dev)
     cfg = PararealConfig(intervals=rc.intervals, max_iters=a.iters or rc.iterations, tol=1e-30, variant=a.variant)
     t0 = time.perf_counter()
     if a.driver == "pipelined":
@@ -49,7 +52,8 @@ def main():
     else:
         _, tr = run_parareal_device(C, F, initial_state(P), rc.t_end, cfg)
     wall = time.perf_counter() - t0
-    print(json.dumps({"config": a.config, "driver": a.driver, "variant": a.variant, "stab_k": P.stab_k, "wall_s": wall, "init_s": tr.init_seconds,
+    print(json.dumps({"config": a.config, "driver": a.driver + (f"[{a.chunks}]" if a.driver == "pipelined" else ""),
+                      "coarse_theta0": ct0, "variant": a.variant, "stab_k": P.stab_k, "wall_s": wall, "init_s": tr.init_seconds,
                       "fine_s": tr.fine_seconds, "sweep_s": tr.sweep_seconds, "iterations": tr.iterations_run,
                       "fine_steps_x_slices": rc.intervals * rc.fine_steps_per_window * tr.iterations_run,
                       "defects_last_boundary": [row[-1] for row in tr.correction_norms],
