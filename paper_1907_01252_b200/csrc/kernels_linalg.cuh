@@ -987,10 +987,25 @@ __device__ __forceinline__ void dense_apply_warps(const Grid& g, const float* __
   const float* Ms = M + (size_t)s * n * ld;
   const double* bs = b + (size_t)s * C * g.np;
   const int lane = tid & 31;
+  // the lane's right-hand-side entries are the same for every row: loaded once
+  // (dense levels hold <= 448 dofs after the cluster inversion, 1024 at most)
+  constexpr int Q = 14;  // columns per lane and round: 14 * 32 = 448
   for (int row = tid >> 5; row < n; row += nth >> 5) {
     const float* Mr = Ms + (size_t)row * ld;
     double acc = 0.0;
-    for (int c = lane; c < n; c += 32) acc = fma((double)Mr[c], bs[(c / g.nn) * g.np + (c % g.nn)], acc);
+    for (int c0 = 0; c0 < n; c0 += 32 * Q) {
+      float mv[Q];
+      double bv[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {  // all loads of the round in flight before the first FMA
+        const int c = c0 + lane + 32 * q;
+        mv[q] = c < n ? __ldg(Mr + c) : 0.0f;
+        bv[q] = c < n ? bs[(c / g.nn) * g.np + (c % g.nn)] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (c0 + lane + 32 * q < n) acc = fma((double)mv[q], bv[q], acc);  // same order as the rolled loop
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) x[(size_t)s * C * g.np + (row / g.nn) * g.np + (row % g.nn)] = acc;

@@ -146,6 +146,7 @@ struct pint_ctx {
   bool jac_strip = true;        // PINT_JAC=colour: 2-d Jacobian by colour-ordered element scatter (k_jacobian_lin)
   bool spmv32_node = true;      // PINT_SPMV32=row: fp32 V-cycle residuals with one thread per (node, row)
   bool spmv32_staged = true;    // PINT_SPMV32=node|row: without the shared-memory staged residual kernel
+  int tail_stage = 1;           // PINT_TAIL_STAGE=0: coarsest inverse read from L2 instead of staged in shared memory
   int strip_w = 25;             // PINT_STRIP_W: owned node columns per Jacobian strip (<= 31)
   bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
                                 // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
@@ -862,7 +863,10 @@ struct Impl {
       }
       const int cl = tail_cluster_size(ctx, S);
       const size_t tsm = ctx->coarse_dense ? tail_dense_smem(ctx->dense_n, ctx->dense_ld, cl) : 0;
-      const bool stage = ctx->coarse_dense && tsm <= kTailSmemMax;
+      // the coarsest inverse is staged in shared memory whenever a CTA's rows fit, even when that runs the
+      // S * cl CTAs in two waves (c3, S = 64, cl = 4: 929 staged vs 887 from L2; c2 8438 vs 6341);
+      // PINT_TAIL_STAGE=0 reads it from L2
+      const bool stage = ctx->coarse_dense && tsm <= kTailSmemMax && ctx->tail_stage != 0;
       const TailArgs& ta = stage ? ctx->tail_cl : ctx->tail;
       const size_t sm = stage ? tsm : 0;
       if (cl == 8)
@@ -1968,6 +1972,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
   if (const char* e = std::getenv("PINT_STRIP_W")) ctx->strip_w = std::atoi(e);
+  if (const char* e = std::getenv("PINT_TAIL_STAGE")) ctx->tail_stage = std::atoi(e);
   ctx->fuse_prolong = std::getenv("PINT_FUSE_PROLONG") && std::getenv("PINT_FUSE_PROLONG")[0] == '1';
   if (const char* e = std::getenv("PINT_POLL")) ctx->poll_every = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
