@@ -58,6 +58,16 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return out;
 }
 
+// sum of n doubles in index order (the serial tail of the reduction kernels).
+// Batching the loads sixteen at a time, and the Givens coefficients eight at
+// a time, measured SLOWER on every config (c2 8 195 vs 8 453, c3 924 vs 937
+// together with the re-balanced residual warps): kept rolled.
+__device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int n) {
+  double t = 0.0;
+  for (int b = 0; b < n; ++b) t += __ldcg(p + b);
+  return t;
+}
+
 // Neighbour node of every stencil offset; offsets that leave the grid are
 // clamped to the node itself.  Their coefficients are exactly zero (assembly,
 // fix-up and RAP never write a non-zero there), so the products vanish and
@@ -242,8 +252,7 @@ __global__ void k_dot_final(const double* __restrict__ partial, int nblk, double
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   if (active && !active[s]) return;
-  double acc = 0.0;
-  for (int b = 0; b < nblk; ++b) acc += partial[(size_t)s * nblk + b];
+  double acc = ordered_sum(partial + (size_t)s * nblk, nblk);
   if (take_sqrt) acc = sqrt(acc);
   if (degen && degen[s]) acc = __longlong_as_double(0x7ff0000000000000LL);
   out[s] = acc;
@@ -280,8 +289,7 @@ __global__ void k_mdot_final(const double* __restrict__ partial, int nblk, int n
   if (s >= S) return;
   if (active && !active[s]) return;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += partial[((size_t)s * maxv + v) * nblk + b];
+    double acc = ordered_sum(partial + ((size_t)s * maxv + v) * nblk, nblk);
     if (accumulate) h[(size_t)s * hstride + v] += acc;
     else h[(size_t)s * hstride + v] = acc;
   }
@@ -1646,27 +1654,34 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g
 // still read the old x of their halo nodes), and the residual is that of the
 // corrected iterate: bitwise k_prolong_add followed by the plain kernel, one
 // launch and one read + write of x fewer per level and V-cycle.
+// Warp roles (block = 32 nodes x (D + 2) warps): one warp per velocity row, one
+// for the pressure row, and ONE for all D deformation rows -- those read 2 of
+// the C coefficient planes (row_couples), so D of them weigh about as much as
+// one full row (2-d: 36 vs 45 loads, 3-d: 162 vs 189).  With a warp per row the
+// deformation warps finished early and idled their slots (ncu: 52 % of the
+// warp slots active, 0.77 of HBM peak on c3 level 0).
 template <int D, bool PROLONG>
-__global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, const float* __restrict__ A,
-                                                                    const double* __restrict__ x,
-                                                                    const double* __restrict__ b,
-                                                                    double* __restrict__ y,
-                                                                    const int* __restrict__ active, Grid gc,
-                                                                    const double* __restrict__ ec,
-                                                                    double* __restrict__ xnew) {
+__global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const float* __restrict__ A,
+                                                               const double* __restrict__ x,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ y,
+                                                               const int* __restrict__ active, Grid gc,
+                                                               const double* __restrict__ ec,
+                                                               double* __restrict__ xnew) {
   pdl_wait();
   constexpr int C = Cells<D>::C;
   constexpr int NOFF = D == 2 ? 9 : 27;
   constexpr int R = D == 2 ? 3 : 9;
   constexpr int W = 34;
   constexpr int RC = D == 2 ? 1 : 4;  // the centre node-row range (dj = dk = 0)
+  constexpr int NW = D + 2;           // warps per block
   __shared__ double xs[C][R][W];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const int n0 = blockIdx.x * 32;
   const int nx = g.n[0], nxy = g.n[0] * g.n[1];
   const double* xsl = x + (size_t)s * C * g.np;
-  for (int idx = threadIdx.y * 32 + threadIdx.x; idx < C * R * W; idx += 32 * C) {
+  for (int idx = threadIdx.y * 32 + threadIdx.x; idx < C * R * W; idx += 32 * NW) {
     const int w = idx % W, q = (idx / W) % R, cb = idx / (W * R);
     const int dj = q % 3 - 1, dk = D == 3 ? q / 3 - 1 : 0;
     const int m = n0 - 1 + w + dj * nx + dk * nxy;
@@ -1685,46 +1700,59 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_resid32_staged(Grid g, con
   __syncthreads();
   const int n = n0 + threadIdx.x;
   if (n >= g.nn) return;
-  const int ca = threadIdx.y;
-  const size_t ov = (size_t)s * C * g.np + (size_t)ca * g.np + n;
-  const double bv = __ldg(b + ov);
-  const float* Ar = A + (size_t)s * NOFF * C * C * g.np + (size_t)ca * C * g.np + n;
-  double part[3] = {0.0, 0.0, 0.0};
-  if (is_urow(ca, D)) {
-    // deformation row: the v_i and u_i planes only (row_couples), all NOFF offsets in flight
-    const int c0 = ca - D, c1 = ca;
-    float v[NOFF][2];
+  const float* As = A + (size_t)s * NOFF * C * C * g.np + n;
+  const size_t vbase = (size_t)s * C * g.np + n;
+  if (PINT_PATTERN && threadIdx.y == D + 1) {
+    // the D deformation rows: planes v_i and u_i only, all NOFF offsets of a row in flight
+#pragma unroll 1
+    for (int i = 0; i < D; ++i) {
+      const int ca = D + i, c0 = i, c1 = D + i;
+      const float* Ar = As + (size_t)ca * C * g.np;
+      const double bv = __ldg(b + vbase + (size_t)ca * g.np);
+      double part[3] = {0.0, 0.0, 0.0};
+      float v[NOFF][2];
 #pragma unroll
-    for (int o = 0; o < NOFF; ++o) {
-      v[o][0] = ld_nc(Ar + ((size_t)o * C * C + c0) * g.np);
-      v[o][1] = ld_nc(Ar + ((size_t)o * C * C + c1) * g.np);
-    }
+      for (int o = 0; o < NOFF; ++o) {
+        v[o][0] = ld_nc(Ar + ((size_t)o * C * C + c0) * g.np);
+        v[o][1] = ld_nc(Ar + ((size_t)o * C * C + c1) * g.np);
+      }
 #pragma unroll
-    for (int o = 0; o < NOFF; ++o) {
-      const int di = o % 3 - 1, row = o / 3;
-      part[o % 3] = fma((double)v[o][0], xs[c0][row][threadIdx.x + 1 + di], part[o % 3]);
-      part[o % 3] = fma((double)v[o][1], xs[c1][row][threadIdx.x + 1 + di], part[o % 3]);
+      for (int o = 0; o < NOFF; ++o) {
+        const int di = o % 3 - 1, row = o / 3;
+        part[o % 3] = fma((double)v[o][0], xs[c0][row][threadIdx.x + 1 + di], part[o % 3]);
+        part[o % 3] = fma((double)v[o][1], xs[c1][row][threadIdx.x + 1 + di], part[o % 3]);
+      }
+      y[vbase + (size_t)ca * g.np] = bv - ((part[0] + part[1]) + part[2]);
     }
-    y[ov] = bv - ((part[0] + part[1]) + part[2]);
     return;
   }
+  // full rows: warp y < D -> velocity row y, warp D -> the pressure row; without the
+  // pattern (-DPINT_PATTERN=0) the last warp runs the deformation rows as full rows too
+  const int nrows = (!PINT_PATTERN && threadIdx.y == D + 1) ? D : 1;
+#pragma unroll 1
+  for (int i = 0; i < nrows; ++i) {
+    const int ca = threadIdx.y < D ? threadIdx.y : (threadIdx.y == D ? 2 * D : D + i);
+    const float* Ar = As + (size_t)ca * C * g.np;
+    const double bv = __ldg(b + vbase + (size_t)ca * g.np);
+    double part[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-  for (int o0 = 0; o0 < NOFF; o0 += 9) {
-    float v[9][C];
+    for (int o0 = 0; o0 < NOFF; o0 += 9) {
+      float v[9][C];
 #pragma unroll
-    for (int q = 0; q < 9; ++q)
+      for (int q = 0; q < 9; ++q)
 #pragma unroll
-      for (int cb = 0; cb < C; ++cb) v[q][cb] = ld_nc(Ar + ((size_t)(o0 + q) * C * C + cb) * g.np);
+        for (int cb = 0; cb < C; ++cb) v[q][cb] = ld_nc(Ar + ((size_t)(o0 + q) * C * C + cb) * g.np);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      const int o = o0 + q;
-      const int di = o % 3 - 1, row = o / 3;
+      for (int q = 0; q < 9; ++q) {
+        const int o = o0 + q;
+        const int di = o % 3 - 1, row = o / 3;
 #pragma unroll
-      for (int cb = 0; cb < C; ++cb)
-        part[o % 3] = fma((double)v[q][cb], xs[cb][row][threadIdx.x + 1 + di], part[o % 3]);
+        for (int cb = 0; cb < C; ++cb)
+          part[o % 3] = fma((double)v[q][cb], xs[cb][row][threadIdx.x + 1 + di], part[o % 3]);
+      }
     }
+    y[vbase + (size_t)ca * g.np] = bv - ((part[0] + part[1]) + part[2]);
   }
-  y[ov] = bv - ((part[0] + part[1]) + part[2]);
 }
 
 }  // namespace pint
@@ -1832,8 +1860,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused(const double* __rest
   }
   if (!last_block_of_slice(counters + s, (unsigned)nblk)) return;
   for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) {
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + ((size_t)s * maxv + vv) * nblk + b);
+    const double t = ordered_sum(partial + ((size_t)s * maxv + vv) * nblk, nblk);
     if (mode == 0) {
       h[(size_t)s * hstride + vv] = t;
     } else {
@@ -1864,8 +1891,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mdot_fused_v(const double* __re
   if (threadIdx.x == 0) partial[((size_t)s * maxv + v) * nblk + blockIdx.x] = acc;
   if (!last_block_of_slice(counters + s, (unsigned)(nblk * nv))) return;
   for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) {
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + ((size_t)s * maxv + vv) * nblk + b);
+    const double t = ordered_sum(partial + ((size_t)s * maxv + vv) * nblk, nblk);
     if (mode == 0) {
       h[(size_t)s * hstride + vv] = t;
     } else {
@@ -1901,8 +1927,7 @@ __global__ void __launch_bounds__(kRedThreads) k_norm_givens(const double* __res
   if (threadIdx.x == 0) partial[(size_t)s * nblk + blockIdx.x] = acc;
   if (!last_block_of_slice(counters + s, (unsigned)nblk)) return;
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + (size_t)s * nblk + b);
+    const double t = ordered_sum(partial + (size_t)s * nblk, nblk);
     H[(size_t)s * (m + 1) * m + (size_t)j * (m + 1) + j + 1] = sqrt(t);
     hnorm[s] = sqrt(t);  // kept for v_{j+1} = w / h_{j+1,j}: the rotation zeroes H[j+1][j]
     counters[s] = 0u;
@@ -1964,8 +1989,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mupdate_norm_givens(
   if (threadIdx.x == 0) partial[(size_t)s * nblk + blockIdx.x] = acc;
   if (!last_block_of_slice(counters + s, (unsigned)nblk)) return;
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += __ldcg(partial + (size_t)s * nblk + b);
+    const double t = ordered_sum(partial + (size_t)s * nblk, nblk);
     H[(size_t)s * (m + 1) * m + (size_t)j * (m + 1) + j + 1] = sqrt(t);
     hnorm[s] = sqrt(t);
     counters[s] = 0u;

@@ -594,7 +594,7 @@ struct Impl {
     // CTAs (c3 levels 0-1: +4.6 %); below that the (node, row) threads hide
     // latency better (c2, L2-resident: -3 % with the node kernel)
     if (resid_staged(ctx, L, S)) {
-      pint_launch(ctx, st, k_resid32_staged<D, false>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+      pint_launch(ctx, st, k_resid32_staged<D, false>, row_grid(L.g.nn, S), dim3(32, D + 2), 0, L.g,
                   (const float*)L.A32, x, b, r, mask, L.g, (const double*)nullptr, (double*)nullptr);
     } else if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= ctx->spmv32_min) {
       pint_launch(ctx, st, k_spmv_node<D, true, float>, node_grid(L.g.nn, S), 128, 0, L.g, (const float*)L.A32, x, b, r,
@@ -916,7 +916,7 @@ struct Impl {
     if (ctx->fuse_prolong && post == 1 && ko.smoother == 1 && resid_staged(ctx, L, S)) {
       // coarse-grid correction inside the post-smoothing residual: x' = cur + P xc goes to nxt (out of
       // place), L.res = b - A x' (bitwise k_prolong_add + the plain residual; PINT_FUSE_PROLONG=1, off by default)
-      pint_launch(ctx, st, k_resid32_staged<D, true>, row_grid(L.g.nn, S), row_block<D>(), 0, L.g,
+      pint_launch(ctx, st, k_resid32_staged<D, true>, row_grid(L.g.nn, S), dim3(32, D + 2), 0, L.g,
                   (const float*)L.A32, (const double*)cur, b, L.res, mask, Lc.g, (const double*)xc, nxt);
       smooth(ctx, L, S, b, nxt, x, mask, st, false, true);
       return;
