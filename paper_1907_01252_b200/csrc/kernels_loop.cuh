@@ -28,6 +28,7 @@ struct LoopScalars {
   int cgs_force;                // 0: Gram-Schmidt passes by tolerance, 1 / 2 forced
   double abs_tol, rel_tol, damping_min;
   double lin_rtol, lin_rtol_first, lin_atol;
+  double forcing;               // later Newton iterations solve to max(lin_atol, forcing * target) (0.1; PINT_FORCING)
   const StepScalars* sts;       // [nmax][S] step scalars (host-computed: same arithmetic as the host path)
   const double* t1tab;          // [nmax][S] step end times
   const int* nsteps;            // [S]
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kLoopThreads) k_gmres_init(LoopDev d, cudaGrap
   for (int s = threadIdx.x; s < ls->S; s += blockDim.x) {
     // inexact-Newton forcing: first Newton iteration of the step at rtol_first
     const double rt = (d.its[s] == 0 && ls->lin_rtol_first > 0.0) ? fmax(ls->lin_rtol, ls->lin_rtol_first) : ls->lin_rtol;
-    const double at = fmax(ls->lin_atol, 0.1 * d.target[s]);
+    const double at = fmax(ls->lin_atol, ls->forcing * d.target[s]);
     const double beta = d.running[s] ? d.rnorm[s] : 0.0;  // ||b|| = ||-r|| = ||r||, bitwise
     const double tol = fmax(rt * beta, at);
     d.gm_tol[s] = tol;

@@ -100,6 +100,15 @@ def test_c1_classic_matches_reference_driver_on_oracle(cuda):
     assert tr.fine_propagations == 10 * 5
 
 
+@pytest.mark.parametrize("variant", ["least_squares", "angle_penalized"])
+def test_c1_weighted_variants_match_reference_driver_on_oracle(cuda, variant):
+    """BASELINE config c1 with the theta-weighted corrections (parareal.py:166-197):
+    same iteration count, defect history, theta values and endpoints as the
+    reference driver on the oracle."""
+    tr = _check_against_golden("c1", variant, "device")
+    assert all(0.0 <= th <= 1.0 for row in tr.theta_values for th in row)
+
+
 def test_c1_damped_coarse_propagator_converges(cuda):
     """with the shifted-CN coarse propagator (theta_c = 1/2 +
     K = 0.52, stability function -> -(1 - theta)/theta = -0.92 on stiff modes)
