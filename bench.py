@@ -450,7 +450,7 @@ def main():
     ap.add_argument("--post", type=int, default=1, help="multigrid post-smoothing sweeps")
     ap.add_argument("--omega", type=float, default=0.9, help="smoother damping")
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
-    ap.add_argument("--reuse", type=int, default=32,
+    ap.add_argument("--reuse", type=int, default=64,
                     help="rebuild the multigrid hierarchy every k steps (or on Krylov-count drift)")
     ap.add_argument("--max-levels", type=int, default=0, help="multigrid levels used (0: all)")
     ap.add_argument("--rtol-first", type=float, default=3e-5, help="GMRES rtol of the first Newton iteration")

@@ -80,7 +80,8 @@ typedef struct pint_krylov_opts {
                             grew past 1.5x (+2) the count right after its last build; 0: every
                             Newton iteration */
   double rtol_first;     /* inexact-Newton forcing of the first Newton iteration of a step (0: use rtol);
-                            later iterations use rtol, never below a tenth of the Newton target */
+                            later iterations use rtol, never below half the Newton target
+                            (PINT_FORCING) */
 } pint_krylov_opts;
 
 /* ---- lifetime -------------------------------------------------------- */

@@ -83,7 +83,7 @@ class KrylovSettings:
     max_levels: int = 0
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
-    precond_reuse: int = 32     # rebuild a slice's multigrid hierarchy every k steps, or when its Krylov
+    precond_reuse: int = 64     # rebuild a slice's multigrid hierarchy every k steps, or when its Krylov
                                 # count drifts past 1.5x (+2) the post-build count (0: every Newton iteration)
     rtol_first: float = 3e-5    # inexact-Newton forcing of the first Newton iteration (0: rtol)
 
