@@ -861,6 +861,259 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
   }
 }
 
+// ---------------------------------------------------------------- K1 residual, node-owner strips (2-d default)
+// The same ownership as k_jacobian_strip for the residual vector: a block owns
+// the rows of W node columns x a chunk of node rows and sweeps the strip's
+// cell rows bottom to top (3-row ring of staged node values, next row
+// prefetched during phase 1):
+//   phase 1  thread = (cell of the row, Gauss point): fields from the ring,
+//            qflux<double>, the NF flux values (and the outflow face terms) to
+//            shared memory;
+//   phase 2  thread = (node column, row component): tests the fluxes of the
+//            cells left / right of the node with its shape functions; the
+//            bottom-corner terms complete node row cj on top of the
+//            top-corner terms kept from cell row cj - 1, and the row is
+//            written ONCE, Dirichlet / identity rows (r = y - g) included.
+// One launch instead of a zeroing pass, 2^d colour launches with a
+// read-modify-write scatter (the long-scoreboard stall of k_elem_tile, ncu
+// r02d) and k_fix_residual.  Fixed summation order (cell row j-1 left, right,
+// row j left, right; points in order, then face points): deterministic and
+// independent of the batch.
+struct ResStrip {
+  static constexpr int A = 4, C = 5, NS = 3, D = 2;
+  static constexpr int T = 128;
+  static constexpr int WMAX = T / A - 1;
+  static constexpr int NF = 3 * D + 2 * D * D + 1;  // vec, ten, uvec, uten, pv, pt
+  static constexpr int RW = WMAX + 3;
+  static constexpr int ITEMS = 160;
+  static constexpr size_t smem = sizeof(double) * ((size_t)(NF + D) * T + A * A * NS + (A / 2) * A * NS +
+                                                   (size_t)3 * 2 * C * RW + (size_t)ITEMS);
+  // flux slots (the layout of ElemTile<2>)
+  static constexpr PINT_HD int vec(int i) { return i; }
+  static constexpr PINT_HD int ten(int i, int j) { return D + i * D + j; }
+  static constexpr PINT_HD int uvec(int i) { return D + D * D + i; }
+  static constexpr PINT_HD int uten(int i, int j) { return 2 * D + D * D + i * D + j; }
+  static constexpr PINT_HD int pv() { return 2 * D + 2 * D * D; }
+  static constexpr PINT_HD int pt(int j) { return 2 * D + 2 * D * D + 1 + j; }
+};
+
+__global__ void __launch_bounds__(ResStrip::T, 3) k_residual_strip(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
+                                                                  const double* __restrict__ y, const double* __restrict__ yo,
+                                                                  double* __restrict__ r, int* __restrict__ degen,
+                                                                  const int* __restrict__ active, int W, int nstrips, int H) {
+  pdl_wait();
+  using L = ResStrip;
+  using ET = ResStrip;
+  constexpr int A = L::A, C = L::C, NS = L::NS, T = L::T, D = 2, RW = L::RW, NF = L::NF;
+  extern __shared__ double sm[];
+  double* sf = sm;                                   // flux [NF][T]
+  double* sb = sf + (size_t)NF * T;                  // outflow face terms [D][T]
+  double* tv = sb + (size_t)D * T;                   // [q][b][NS]
+  double* tf = tv + A * A * NS;                      // [face q][b][NS]
+  double* ring = tf + (A / 2) * A * NS;              // [slot 3][lvl 2][c][RW]
+  double* part = ring + 3 * 2 * C * RW;              // top-corner partials [ITEMS]
+  __shared__ int sdeg;
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;  // uniform per block
+  const int lane = threadIdx.x;
+  const int nx = m.cells[0], ny = m.cells[1];
+  const int strip = blockIdx.x % nstrips, chunk = blockIdx.x / nstrips;
+  const int i0 = strip * W;
+  const int nown = min(W, nx + 1 - i0);
+  const int j0 = chunk * H, j1 = min(j0 + H, ny + 1);
+  if (nown <= 0 || j0 >= j1) return;
+  const int c_lo = max(i0 - 1, 0), c_hi = min(i0 + nown - 1, nx - 1);
+  const int ncell = c_hi - c_lo + 1;
+  const int ncol = ncell + 1;
+  const int cj_lo = max(j0 - 1, 0), cj_hi = min(j1 - 1, ny - 1);
+  const int np = m.g.np;
+  const size_t vs = (size_t)C * np;
+  const double* ys = y + s * vs;
+  const double* yos = yo + s * vs;
+  if (lane == 0) sdeg = 0;
+  if (lane < A + (A >> 1)) {
+    const bool face = lane >= A;
+    double xi[D], N[A], dN[A][D];
+    gauss_point<D>(face ? lane - A : lane, face, xi);
+    q1_shape<D>(xi, ph.ih, N, dN);
+    double* t = face ? tf + (lane - A) * A * NS : tv + lane * A * NS;
+#pragma unroll
+    for (int b = 0; b < A; ++b) {
+      t[b * NS] = N[b];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[b * NS + 1 + k] = dN[b][k];
+    }
+  }
+  constexpr int PER = (2 * C * RW + T - 1) / T;
+  auto load_row = [&](int rr, double (&v)[PER]) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;
+      const int col = idx % RW, c = (idx / RW) % C, lvl = idx / (RW * C);
+      v[k] = (lvl < 2 && col < ncol) ? __ldg((lvl == 0 ? ys : yos) + (size_t)c * np + node_index(m.g, c_lo + col, rr, 0))
+                                     : 0.0;
+    }
+  };
+  auto store_row = [&](int rr, const double (&v)[PER]) {
+    double* dst = ring + (rr % 3) * 2 * C * RW;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = lane + k * T;
+      if (idx < 2 * C * RW) dst[idx] = v[k];
+    }
+  };
+  {
+    double v[PER];
+    load_row(cj_lo, v);
+    store_row(cj_lo, v);
+    load_row(cj_lo + 1, v);
+    store_row(cj_lo + 1, v);
+  }
+  const int lc = lane % 32, q = lane / 32;
+  const int nitems = nown * C;
+  const double ramp = st[s].ramp;
+  __syncthreads();
+  for (int cj = cj_lo; cj <= cj_hi; ++cj) {
+    double pre[PER];
+    const bool more = cj + 2 <= min(cj_hi + 1, ny);
+    if (more) load_row(cj + 2, pre);
+    // ---- phase 1: pointwise flux of (cell c_lo + lc, row cj) at point q
+    if (lc < ncell) {
+      const int ci = c_lo + lc;
+      const uint8_t cf = m.cell_flags[cj * nx + ci];
+      const bool solid = cf & kCellSolid;
+      const double* r0 = ring + (cj % 3) * 2 * C * RW;
+      const double* r1 = ring + ((cj + 1) % 3) * 2 * C * RW;
+      auto getter = [&](int lvl) {
+        return [=](int a, int c) {
+          const double* rr = (a >> 1) ? r1 : r0;
+          return rr[(lvl * C + c) * RW + lc + (a & 1)];
+        };
+      };
+      auto shape = [&](const double* t, double (&N)[A], double (&dN)[A][D]) {
+#pragma unroll
+        for (int b = 0; b < A; ++b) {
+          N[b] = t[b * NS];
+#pragma unroll
+          for (int k = 0; k < D; ++k) dN[b][k] = t[b * NS + 1 + k];
+        }
+      };
+      double* fo = sf + lane;
+      {
+        double N[A], dN[A][D];
+        shape(tv + q * A * NS, N, dN);
+        QFields<D, double> fn, fold;
+        interp<D>(N, dN, getter(0), fn);
+        interp<D>(N, dN, getter(1), fold);
+        QFlux<D, double> fx;
+        bool dg = false;
+        qflux<D, double, double, double>(ph, st[s], solid, fn, fold, fx, dg);
+        if (dg) sdeg = 1;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          fo[ET::vec(i) * T] = fx.vec[i];
+          fo[ET::uvec(i) * T] = fx.uvec[i];
+          fo[ET::pt(i) * T] = fx.pt[i];
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            fo[ET::ten(i, j) * T] = fx.ten[i][j];
+            fo[ET::uten(i, j) * T] = fx.uten[i][j];
+          }
+        }
+        fo[ET::pv() * T] = fx.pv;
+      }
+      if ((cf & kCellOutflow) && q < (A >> 1)) {
+        double N[A], dN[A][D];
+        shape(tf + q * A * NS, N, dN);
+        QFields<D, double> gn, gold;
+        interp<D>(N, dN, getter(0), gn);
+        interp<D>(N, dN, getter(1), gold);
+        double B[D];
+        qflux_outflow<D, double, double, double>(ph, st[s], gn, gold, B);
+#pragma unroll
+        for (int i = 0; i < D; ++i) sb[i * T + lane] = B[i];
+      }
+    }
+    if (more) store_row(cj + 2, pre);
+    __syncthreads();
+    // ---- phase 2: rows (node (i, cj), ca) and (node (i, cj + 1), ca)
+    for (int it = lane; it < nitems; it += T) {
+      const int ca = it / nown, li = it % nown;
+      const int i = i0 + li;
+      const bool own_bottom = cj >= j0;
+      const bool own_top = cj + 1 < j1;
+      const bool top_final = own_top && cj + 1 == ny;
+      // contribution of cell (ci, cj) to row (corner a, ca)
+      auto cell_term = [&](int ci, int a) -> double {
+        if (ci < 0 || ci >= nx) return 0.0;
+        const int lcell = ci - c_lo;
+        const uint8_t cf = m.cell_flags[cj * nx + ci];
+        const bool solid = cf & kCellSolid;
+        if (ca == 2 * D && solid) return 0.0;               // solid cells own no p rows
+        const int nj = cj + (a >> 1);
+        const uint8_t nf = m.node_flags[node_index(m.g, i, nj, 0)];
+        const bool ext = solid || !(nf & kSolidTouch);
+        double acc = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < A; ++qq) {
+          const double* f = sf + qq * 32 + lcell;
+          const double* ta = tv + (qq * A + a) * NS;
+          double v;
+          if (ca < D) {
+            v = f[ET::vec(ca) * T] * ta[0];
+#pragma unroll
+            for (int j = 0; j < D; ++j) v += f[ET::ten(ca, j) * T] * ta[1 + j];
+          } else if (ca < 2 * D) {
+            const int iu = ca - D;
+            v = f[ET::uvec(iu) * T] * ta[0];
+            if (ext) {
+              double ex = 0.0;
+#pragma unroll
+              for (int j = 0; j < D; ++j) ex += f[ET::uten(iu, j) * T] * ta[1 + j];
+              v = v + ex;
+            }
+          } else {
+            v = f[ET::pv() * T] * ta[0];
+#pragma unroll
+            for (int j = 0; j < D; ++j) v += f[ET::pt(j) * T] * ta[1 + j];
+          }
+          acc += ph.wq * v;
+        }
+        if ((cf & kCellOutflow) && ca < D) {
+#pragma unroll
+          for (int qq = 0; qq < (A >> 1); ++qq)
+            acc += (-ph.wf) * (sb[ca * T + qq * 32 + lcell] * tf[(qq * A + a) * NS]);
+        }
+        return acc;
+      };
+      auto write_row = [&](int j, double R) {
+        const int n = node_index(m.g, i, j, 0);
+        const uint8_t nf = m.node_flags[n];
+        double out = R;
+        if (row_fixed(nf, ca, D)) {
+          const double g = (ca == 0) ? ramp * m.profile[n] : 0.0;
+          out = ring[(j % 3) * 2 * C * RW + ca * RW + (i - c_lo)] - g;  // y - g from the staged node row
+        }
+        r[s * vs + (size_t)ca * np + n] = out;
+      };
+      if (own_bottom) {
+        double R = cj > cj_lo ? part[it] : 0.0;
+        R += cell_term(i - 1, 1);  // node is the bottom-right corner of the left cell
+        R += cell_term(i, 0);      // bottom-left corner of the right cell
+        write_row(cj, R);
+      }
+      if (own_top) {
+        double P = cell_term(i - 1, 3);  // top-right corner of the left cell
+        P += cell_term(i, 2);            // top-left corner of the right cell
+        if (top_final) write_row(cj + 1, P);
+        else part[it] = P;
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0 && sdeg) degen[s] = 1;  // benign: every writer stores 1
+}
+
 // ---------------------------------------------------------------- Jacobian-vector product (matrix-free)
 template <int D>
 __global__ void __launch_bounds__(128, ElemOcc<D>::value) k_jvp_colour(MeshDev m, Phys ph, const StepScalars* __restrict__ st,

@@ -149,6 +149,9 @@ struct pint_ctx {
   int tail_stage = 1;           // PINT_TAIL_STAGE=0: coarsest inverse read from L2 instead of staged in shared memory
   double forcing = 0.5;         // PINT_FORCING: absolute Krylov tolerance of the later Newton iterations / Newton target
                                 // (round 1: 0.1; 0.5 keeps Newton at 2.0000 its per step on c2-c4 with 4-7 % fewer Krylov its)
+  bool res_strip = false;       // PINT_RES=strip: K1 in node-owner strips (one launch, no zeroing / colour scatter / fix-up;
+                                // measured slower: c3 0.64 vs 0.45 ms -- the per-row barriers outweigh the saved passes)
+  int res_waves = 4;            // PINT_RES_WAVES: target waves of strip-residual blocks (more chunks, shorter sweeps)
   int strip_w = 25;             // PINT_STRIP_W: owned node columns per Jacobian strip (<= 31)
   bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
                                 // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
@@ -490,6 +493,30 @@ struct Impl {
   static int residual(pint_ctx* ctx, int S, const double* y, const double* yo, double* r, const int* mask,
                       double* h_norms, cudaStream_t st) {
     MeshDev m = mesh(ctx);
+    if constexpr (D == 2) {
+      if (ctx->res_strip) {
+        // node-owner strips: every residual row written once (fixed rows included), one launch
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_residual_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ResStrip::smem);
+          attr = true;
+        }
+        cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
+        if (ctx->capturing) ctx->nopdl.insert(st);  // memset node: no programmatic edge out of it
+        const int nxn = ctx->cells[0] + 1, nyn = ctx->cells[1] + 1;
+        const int wmax = std::max(1, std::min(ctx->strip_w, (int)ResStrip::WMAX));
+        const int nstrips = (nxn + wmax - 1) / wmax;
+        const int W = (nxn + nstrips - 1) / nstrips;
+        const int base = nstrips * S;
+        int nch = std::max(1, std::min((ctx->res_waves * 3 * 148 + base - 1) / base, std::max(1, nyn / 2)));
+        const int H = (nyn + nch - 1) / nch;
+        nch = (nyn + H - 1) / H;
+        pint_launch(ctx, st, k_residual_strip, dim3(nstrips * nch, S), ResStrip::T, ResStrip::smem, m, ctx->ph,
+                    (const StepScalars*)ctx->d_st, y, yo, r, ctx->d_degen, mask, W, nstrips, H);
+        PINT_LAUNCHED();
+        return norms(ctx, S, r, r, mask, true, ctx->d_degen, h_norms, st);
+      }
+    }
     pint_launch(ctx, st, k_zero_active, vec_grid(vs(ctx), S), 256, 0, r, vs(ctx), mask);
     cudaMemsetAsync(ctx->d_degen, 0, sizeof(int) * S, st);
     if (ctx->capturing) ctx->nopdl.insert(st);  // memset node: no programmatic edge out of it
@@ -1975,6 +2002,8 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
   if (const char* e = std::getenv("PINT_STRIP_W")) ctx->strip_w = std::atoi(e);
+  if (const char* e = std::getenv("PINT_RES")) ctx->res_strip = std::string(e) == "strip";
+  if (const char* e = std::getenv("PINT_RES_WAVES")) ctx->res_waves = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PINT_FORCING")) ctx->forcing = std::atof(e);
   if (const char* e = std::getenv("PINT_TAIL_STAGE")) ctx->tail_stage = std::atoi(e);
   ctx->fuse_prolong = std::getenv("PINT_FUSE_PROLONG") && std::getenv("PINT_FUSE_PROLONG")[0] == '1';

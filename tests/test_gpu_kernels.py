@@ -240,6 +240,30 @@ def test_vanka_setup_variants_agree(cuda, name):
         assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[1][s]), (name, s)
 
 
+@pytest.mark.parametrize("name", ["small2d", "c1"])
+def test_residual_strip_variant_agrees(cuda, name):
+    """K1 in node-owner strips (k_residual_strip, PINT_RES=strip: one launch
+    writing every row once, fixed rows included; measured slower than the tiled
+    colour kernels, off by default) gives the same residual up to round-off,
+    flags the same degenerate slices, and matches the oracle."""
+    P = PROBLEMS[name]
+    S = 3
+    Y = random_states(P, S, 91)
+    Yo = random_states(P, S, 92)
+    k, th, t1 = _step_args(S)
+    outs, norms = [], []
+    for env in ({}, {"PINT_RES": "strip"}):
+        dev = _device_with_env(P, env)
+        r, nrm = dev.residual(dev.to_device(Y), dev.to_device(Yo), k, th, t1)
+        outs.append(dev.to_host(r))
+        norms.append(nrm)
+    scale = np.abs(outs[0]).max()
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-13 * scale
+    assert np.allclose(norms[0], norms[1], rtol=1e-13)
+    ref = O.residual(P, Y[0], Yo[0], k[0], th[0], t1[0])
+    assert np.linalg.norm(outs[1][0] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("name", ["small2d", "c1", "small3d"])
 def test_deformation_rows_structural_zeros(devices, name):
     """The product kernels skip the coefficient planes (u_i row, column other
