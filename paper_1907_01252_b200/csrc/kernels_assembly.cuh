@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
       // contribution of cell (ci, cj) to row (a, ca): K[off(a, b)] += ...
       auto cell_terms = [&](int ci, int a, double (&Kx)[9]) {
         if (ci < 0 || ci >= nx) return;
+        if (!row_couples(ca, cp, D)) return;                // structural zero plane (u_i row, column not v_i / u_i)
         const int lcell = ci - c_lo;
         const uint8_t cf = m.cell_flags[cj * nx + ci];
         const bool solid = cf & kCellSolid;
