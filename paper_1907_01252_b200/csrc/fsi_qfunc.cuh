@@ -54,6 +54,43 @@ PINT_HD double value_of(const Dual& a) { return a.v; }
 PINT_HD double deriv_of(double) { return 0.0; }
 PINT_HD double deriv_of(const Dual& a) { return a.d; }
 
+// value + N tangents: one pass of the flux carries N derivative directions, so
+// the primal part (and every division) is computed once for all of them and
+// the N tangent chains are independent instructions (ILP for the FP64 pipe)
+template <int N>
+struct DualV {
+  double v, d[N];
+  PINT_HD DualV() : v(0.0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) d[k] = 0.0;
+  }
+  PINT_HD DualV(double a) : v(a) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) d[k] = 0.0;
+  }
+};
+#define PINT_DV_LOOP _Pragma("unroll") for (int k = 0; k < N; ++k)
+template <int N> PINT_HD DualV<N> operator+(DualV<N> a, DualV<N> b) { DualV<N> r; r.v = a.v + b.v; PINT_DV_LOOP r.d[k] = a.d[k] + b.d[k]; return r; }
+template <int N> PINT_HD DualV<N> operator-(DualV<N> a, DualV<N> b) { DualV<N> r; r.v = a.v - b.v; PINT_DV_LOOP r.d[k] = a.d[k] - b.d[k]; return r; }
+template <int N> PINT_HD DualV<N> operator*(DualV<N> a, DualV<N> b) { DualV<N> r; r.v = a.v * b.v; PINT_DV_LOOP r.d[k] = a.d[k] * b.v + a.v * b.d[k]; return r; }
+template <int N> PINT_HD DualV<N> operator/(DualV<N> a, DualV<N> b) {
+  const double ib = 1.0 / b.v;  // one division for the value and all tangents
+  DualV<N> r; r.v = a.v * ib; PINT_DV_LOOP r.d[k] = (a.d[k] - r.v * b.d[k]) * ib; return r;
+}
+template <int N> PINT_HD DualV<N> operator-(DualV<N> a) { DualV<N> r; r.v = -a.v; PINT_DV_LOOP r.d[k] = -a.d[k]; return r; }
+template <int N> PINT_HD DualV<N> operator+(DualV<N> a, double b) { a.v += b; return a; }
+template <int N> PINT_HD DualV<N> operator+(double a, DualV<N> b) { b.v += a; return b; }
+template <int N> PINT_HD DualV<N> operator-(DualV<N> a, double b) { a.v -= b; return a; }
+template <int N> PINT_HD DualV<N> operator-(double a, DualV<N> b) { DualV<N> r; r.v = a - b.v; PINT_DV_LOOP r.d[k] = -b.d[k]; return r; }
+template <int N> PINT_HD DualV<N> operator*(DualV<N> a, double b) { a.v *= b; PINT_DV_LOOP a.d[k] *= b; return a; }
+template <int N> PINT_HD DualV<N> operator*(double a, DualV<N> b) { b.v *= a; PINT_DV_LOOP b.d[k] *= a; return b; }
+template <int N> PINT_HD DualV<N> operator/(DualV<N> a, double b) { const double ib = 1.0 / b; a.v *= ib; PINT_DV_LOOP a.d[k] *= ib; return a; }
+template <int N> PINT_HD DualV<N> operator/(double a, DualV<N> b) {
+  const double ib = 1.0 / b.v;
+  DualV<N> r; r.v = a * ib; PINT_DV_LOOP r.d[k] = -r.v * b.d[k] * ib; return r;
+}
+template <int N> PINT_HD double value_of(const DualV<N>& a) { return a.v; }
+
 // ---------------------------------------------------------------- small matrices
 template <int D, typename T>
 PINT_HD T det_inv(const T (&F)[D][D], T (&Fi)[D][D]) {
@@ -126,11 +163,11 @@ PINT_HD void gauss_point(int q, bool face, double (&xi)[D]) {
 // Scalar promotion: double op double -> double, anything with a Dual -> Dual.
 template <class A, class B>
 struct PromoteT {
-  using type = Dual;
+  using type = A;  // A is a dual type (Dual or DualV<N>); B is double or the same dual type
 };
-template <>
-struct PromoteT<double, double> {
-  using type = double;
+template <class B>
+struct PromoteT<double, B> {
+  using type = B;
 };
 template <class A, class B>
 using P2 = typename PromoteT<A, B>::type;
@@ -352,11 +389,11 @@ __device__ __forceinline__ void qflux_outflow(const Phys& ph, const StepScalars&
 
 // fields with dual parts in ONE group only: the trial function (N_b, dN_b)
 // of component cb (G = 0 velocity, 1 deformation, 2 pressure group)
-template <int D, int G>
+template <int D, int G, typename DT = Dual>
 struct SeedTypes {
-  using TV = std::conditional_t<G == 0, Dual, double>;
-  using TU = std::conditional_t<G == 1, Dual, double>;
-  using TP = std::conditional_t<G == 2, Dual, double>;
+  using TV = std::conditional_t<G == 0, DT, double>;
+  using TU = std::conditional_t<G == 1, DT, double>;
+  using TP = std::conditional_t<G == 2, DT, double>;
   using F = QFields<D, TV, TU, TP>;
 };
 
@@ -447,6 +484,35 @@ __device__ __forceinline__ void seed_dir(const QFields<D, double>& f, int cb, in
   } else {
     n.p = f.p;
   }
+}
+
+// all 1 + D unit directions of component cb at once: tangent 0 seeds the value
+// of cb, tangent 1 + k its derivative along x_k (seed_dir for dir = 0 .. D in
+// one DualV<1 + D> pass)
+template <int D, int G>
+__device__ __forceinline__ void seed_all(const QFields<D, double>& f, int cb,
+                                         typename SeedTypes<D, G, DualV<1 + D>>::F& n) {
+  using DT = DualV<1 + D>;
+  auto mk = [](double v, int dir, bool on) {
+    DT r(v);
+    if (on) {
+#pragma unroll
+      for (int k = 0; k < 1 + D; ++k) r.d[k] = (k == dir) ? 1.0 : 0.0;
+    }
+    return r;
+  };
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    if constexpr (G == 0) n.v[i] = mk(f.v[i], 0, cb == i); else n.v[i] = f.v[i];
+    if constexpr (G == 1) n.u[i] = mk(f.u[i], 0, cb == D + i); else n.u[i] = f.u[i];
+    if constexpr (G == 2) n.gp[i] = mk(f.gp[i], 1 + i, true); else n.gp[i] = f.gp[i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if constexpr (G == 0) n.Gv[i][j] = mk(f.Gv[i][j], 1 + j, cb == i); else n.Gv[i][j] = f.Gv[i][j];
+      if constexpr (G == 1) n.Gu[i][j] = mk(f.Gu[i][j], 1 + j, cb == D + i); else n.Gu[i][j] = f.Gu[i][j];
+    }
+  }
+  if constexpr (G == 2) n.p = mk(f.p, 0, true); else n.p = f.p;
 }
 
 // dual fields: values from f, derivatives from the interpolated direction w

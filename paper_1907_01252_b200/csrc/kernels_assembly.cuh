@@ -630,6 +630,58 @@ __device__ __forceinline__ void strip_point(const Phys& ph, const StepScalars& s
   }
 }
 
+// the same table from ONE flux pass carrying all 1 + d directions as tangents
+// (DualV<1 + d>): the primal part and the divisions are computed once per
+// column component instead of once per direction, and the tangent chains are
+// independent instructions.  Same derivative values up to the association of
+// the products (the Jacobians agree to round-off, test_jacobian_formulations_agree).
+template <int G>
+__device__ __forceinline__ void strip_point_mt(const Phys& ph, const StepScalars& st, bool solid, bool face_pt, int cp,
+                                               const QFields<2, double>& fn, const QFields<2, double>& fo,
+                                               const QFields<2, double>& gn, const QFields<2, double>& go,
+                                               double* __restrict__ sg) {
+  using J = JacStrip;
+  constexpr int D = 2, NS = J::NS, T = J::T;
+  using DT = DualV<NS>;
+  using ST = SeedTypes<D, G, DT>;
+  {
+    typename ST::F fd;
+    seed_all<D, G>(fn, cp, fd);
+    QFlux<D, DT> fx;
+    bool dg = false;
+    qflux<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, solid, fd, fo, fx, dg);
+#pragma unroll
+    for (int dir = 0; dir < NS; ++dir) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        sg[((i * NS + 0) * NS + dir) * T] = fx.vec[i].d[dir];
+        sg[(((D + i) * NS + 0) * NS + dir) * T] = fx.uvec[i].d[dir];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          sg[((i * NS + 1 + j) * NS + dir) * T] = fx.ten[i][j].d[dir];
+          sg[(((D + i) * NS + 1 + j) * NS + dir) * T] = fx.uten[i][j].d[dir];
+        }
+      }
+      sg[((2 * D * NS + 0) * NS + dir) * T] = fx.pv.d[dir];
+#pragma unroll
+      for (int j = 0; j < D; ++j) sg[((2 * D * NS + 1 + j) * NS + dir) * T] = fx.pt[j].d[dir];
+    }
+  }
+  if constexpr (G != 2) {
+    if (face_pt) {
+      typename ST::F fd;
+      seed_all<D, G>(gn, cp, fd);
+      P2<typename ST::TV, typename ST::TU> B[D];
+      qflux_outflow<D, typename ST::TV, typename ST::TU, typename ST::TP>(ph, st, fd, go, B);
+#pragma unroll
+      for (int dir = 0; dir < NS; ++dir)
+#pragma unroll
+        for (int i = 0; i < D; ++i) sg[(J::GSZ + i * NS + dir) * T] = B[i].d[dir];
+    }
+  }
+}
+
+template <bool MT>
 __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Phys ph, const StepScalars* __restrict__ st,
                                                                   const double* __restrict__ y, const double* __restrict__ yo,
                                                                   double* __restrict__ J, float* __restrict__ J32,
@@ -749,12 +801,21 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
         interp<D>(N, dN, getter(0), gn);
         interp<D>(N, dN, getter(1), go);
       }
-      if (cp < D)
-        strip_point<0>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
-      else if (cp < 2 * D)
-        strip_point<1>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
-      else
-        strip_point<2>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+      if constexpr (MT) {
+        if (cp < D)
+          strip_point_mt<0>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+        else if (cp < 2 * D)
+          strip_point_mt<1>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+        else
+          strip_point_mt<2>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+      } else {
+        if (cp < D)
+          strip_point<0>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+        else if (cp < 2 * D)
+          strip_point<1>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+        else
+          strip_point<2>(ph, st[s], solid, face_pt, cp, fn, fo, gn, go, sg + lane);
+      }
     }
     if (more) store_row(cj + 2, pre);  // slot (cj + 2) % 3 = (cj - 1) % 3: not read in this row
     __syncthreads();

@@ -152,6 +152,7 @@ struct pint_ctx {
   bool res_strip = false;       // PINT_RES=strip: K1 in node-owner strips (one launch, no zeroing / colour scatter / fix-up;
                                 // measured slower: c3 0.64 vs 0.45 ms -- the per-row barriers outweigh the saved passes)
   int res_waves = 4;            // PINT_RES_WAVES: target waves of strip-residual blocks (more chunks, shorter sweeps)
+  bool jac_mt = true;           // PINT_JAC_MT=0: one dual pass per direction in the strip Jacobian (round-2 first form)
   int strip_w = 25;             // PINT_STRIP_W: owned node columns per Jacobian strip (<= 31)
   bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
                                 // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
@@ -561,7 +562,8 @@ struct Impl {
         // node-owner strips: every stencil row written once (fp64 + fp32 copy, fixed rows included)
         static bool attr = false;
         if (!attr) {
-          cudaFuncSetAttribute(k_jacobian_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JacStrip::smem);
+          cudaFuncSetAttribute(k_jacobian_strip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JacStrip::smem);
+          cudaFuncSetAttribute(k_jacobian_strip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JacStrip::smem);
           attr = true;
         }
         const int nxn = ctx->cells[0] + 1, nyn = ctx->cells[1] + 1;
@@ -575,8 +577,12 @@ struct Impl {
         int nch = std::max(1, std::min((8 * 3 * 148 + base - 1) / base, std::max(1, nyn / 4)));
         const int H = (nyn + nch - 1) / nch;
         nch = (nyn + H - 1) / H;
-        pint_launch(ctx, st, k_jacobian_strip, dim3(nstrips * nch, C, S), JacStrip::T, JacStrip::smem, m, ctx->ph,
-                    (const StepScalars*)ctx->d_st, y, yo, L0.A, L0.A32, mask, W, nstrips, H);
+        if (ctx->jac_mt)  // all 1 + d directions of a column component in one multi-tangent flux pass (PINT_JAC_MT=0: one pass each)
+          pint_launch(ctx, st, k_jacobian_strip<true>, dim3(nstrips * nch, C, S), JacStrip::T, JacStrip::smem, m, ctx->ph,
+                      (const StepScalars*)ctx->d_st, y, yo, L0.A, L0.A32, mask, W, nstrips, H);
+        else
+          pint_launch(ctx, st, k_jacobian_strip<false>, dim3(nstrips * nch, C, S), JacStrip::T, JacStrip::smem, m, ctx->ph,
+                      (const StepScalars*)ctx->d_st, y, yo, L0.A, L0.A32, mask, W, nstrips, H);
         PINT_LAUNCHED();
         return PINT_OK;
       }
@@ -2002,6 +2008,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
   if (const char* e = std::getenv("PINT_STRIP_W")) ctx->strip_w = std::atoi(e);
+  if (const char* e = std::getenv("PINT_JAC_MT")) ctx->jac_mt = e[0] == '1';
   if (const char* e = std::getenv("PINT_RES")) ctx->res_strip = std::string(e) == "strip";
   if (const char* e = std::getenv("PINT_RES_WAVES")) ctx->res_waves = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PINT_FORCING")) ctx->forcing = std::atof(e);

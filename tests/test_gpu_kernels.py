@@ -199,7 +199,9 @@ def _device_with_env(P, env, S=3):
 @pytest.mark.parametrize("name", ["c1", "small3d"])
 def test_jacobian_formulations_agree(cuda, name):
     """K2 by pointwise linearisation (1 + d dual passes per column component)
-    in node-owner strips (2-d default; 3-d uses the colour scatter), in the
+    in node-owner strips (2-d default, all directions of a column component in
+    one multi-tangent flux pass; PINT_JAC_MT=0: one dual pass per direction;
+    3-d uses the colour scatter), in the
     colour-ordered element scatter (PINT_JAC=colour) and K2 by one dual pass
     per Jacobian column (PINT_JAC=columns) assemble the same block-stencil
     operator up to round-off."""
@@ -209,7 +211,7 @@ def test_jacobian_formulations_agree(cuda, name):
     Yo = random_states(P, S, 52)
     k, th, t1 = _step_args(S)
     blocks = []
-    for env in ({}, {"PINT_JAC": "colour"}, {"PINT_JAC": "columns"}):
+    for env in ({}, {"PINT_JAC_MT": "0"}, {"PINT_JAC": "colour"}, {"PINT_JAC": "columns"}):
         dev = _device_with_env(P, env)
         dev.assemble(dev.to_device(Y), dev.to_device(Yo), k, th, t1)
         blocks.append(dev.jacobian_blocks(S).cpu().numpy())
