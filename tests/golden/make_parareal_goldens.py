@@ -36,6 +36,9 @@ CASES = {
     "c1": (CONFIGS["c1"].problem, 1.0, 0.002, 0.02, 10, 5),
     "small": (small_problem(8, 2), 0.8, 0.01, 0.05, 8, 4),
     "small3d": (channel_3d(10, 2, 2, name="small3d"), 0.2, 0.01, 0.05, 4, 3),
+    # BASELINE c2 (32 slices, fine 2^-10, coarse 2^-6), first 3 of its 8 iterations (the oracle needs ~50 min
+    # for them on one core; the full 8-iteration run is tests/golden/make_parareal_c2.py)
+    "c2k3": (CONFIGS["c2"].problem, CONFIGS["c2"].t_end, CONFIGS["c2"].fine_step, CONFIGS["c2"].coarse_step, 32, 3),
 }
 
 

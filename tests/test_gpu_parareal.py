@@ -24,6 +24,7 @@ CASES = {
     "small": (small_problem(8, 2), 0.8, 0.01, 0.05, 8, 4),
     "c1": (CONFIGS["c1"].problem, 1.0, 0.002, 0.02, 10, 5),
     "small3d": (channel_3d(10, 2, 2, name="small3d"), 0.2, 0.01, 0.05, 4, 3),
+    "c2k3": (CONFIGS["c2"].problem, CONFIGS["c2"].t_end, CONFIGS["c2"].fine_step, CONFIGS["c2"].coarse_step, 32, 3),
 }
 
 
@@ -107,6 +108,15 @@ def test_c1_weighted_variants_match_reference_driver_on_oracle(cuda, variant):
     reference driver on the oracle."""
     tr = _check_against_golden("c1", variant, "device")
     assert all(0.0 <= th <= 1.0 for row in tr.theta_values for th in row)
+
+
+def test_c2_first_iterations_match_reference_driver_on_oracle(cuda):
+    """BASELINE config c2 (64x16 mesh, 32 slices): the first 3 Parareal
+    iterations against the reference driver on the oracle -- same defect
+    history and endpoints (skipped until the golden exists: ~50 min of oracle
+    time, tests/golden/make_parareal_goldens.py c2k3)."""
+    tr = _check_against_golden("c2k3", "classic", "device")
+    assert tr.fine_propagations == 32 * 3
 
 
 def test_c1_damped_coarse_propagator_converges(cuda):
