@@ -515,6 +515,34 @@ __device__ __forceinline__ void seed_all(const QFields<D, double>& f, int cb,
   if constexpr (G == 2) n.p = mk(f.p, 0, true); else n.p = f.p;
 }
 
+// NT consecutive unit directions dir0 .. dir0 + NT - 1 of component cb as the
+// tangents of one DualV<NT> pass (seed_all is dir0 = 0, NT = 1 + D)
+template <int D, int G, int NT>
+__device__ __forceinline__ void seed_dirs(const QFields<D, double>& f, int cb, int dir0,
+                                          typename SeedTypes<D, G, DualV<NT>>::F& n) {
+  using DT = DualV<NT>;
+  auto mk = [dir0](double v, int dir, bool on) {
+    DT r(v);
+    if (on) {
+#pragma unroll
+      for (int k = 0; k < NT; ++k) r.d[k] = (dir0 + k == dir) ? 1.0 : 0.0;
+    }
+    return r;
+  };
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    if constexpr (G == 0) n.v[i] = mk(f.v[i], 0, cb == i); else n.v[i] = f.v[i];
+    if constexpr (G == 1) n.u[i] = mk(f.u[i], 0, cb == D + i); else n.u[i] = f.u[i];
+    if constexpr (G == 2) n.gp[i] = mk(f.gp[i], 1 + i, true); else n.gp[i] = f.gp[i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if constexpr (G == 0) n.Gv[i][j] = mk(f.Gv[i][j], 1 + j, cb == i); else n.Gv[i][j] = f.Gv[i][j];
+      if constexpr (G == 1) n.Gu[i][j] = mk(f.Gu[i][j], 1 + j, cb == D + i); else n.Gu[i][j] = f.Gu[i][j];
+    }
+  }
+  if constexpr (G == 2) n.p = mk(f.p, 0, true); else n.p = f.p;
+}
+
 // dual fields: values from f, derivatives from the interpolated direction w
 template <int D>
 __device__ __forceinline__ void seed_fields(const QFields<D, double>& f, const QFields<D, double>& w,

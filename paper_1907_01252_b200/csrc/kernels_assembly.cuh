@@ -312,6 +312,9 @@ struct JacLin {
   static_assert((2 * C * A * EPB) % T == 0, "staging loads per thread");
 };
 
+#ifndef PINT_JACLIN_NT
+#define PINT_JACLIN_NT 1  // tangents per flux pass of the 3-d colour-path Jacobian (2: two DualV<2> passes)
+#endif
 template <int D, int G>
 __device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& st, const ElemIndex<D>& e, int q,
                                              const double* __restrict__ y, const double* __restrict__ yo, int np,
@@ -332,7 +335,38 @@ __device__ __forceinline__ void jaclin_point(const Phys& ph, const StepScalars& 
   const bool solid = e.cflag & kCellSolid;
   auto gy = [&](int a, int c) { return __ldg(y + c * np + e.node[a]); };
   auto go = [&](int a, int c) { return __ldg(yo + c * np + e.node[a]); };
-  {
+  if constexpr (D == 3 && PINT_JACLIN_NT > 1) {
+    // volume point, 3-d: the 1 + d directions in passes of PINT_JACLIN_NT tangents (DualV): the primal part
+    // of the flux and its divisions are shared by the tangents of a pass
+    constexpr int NT = PINT_JACLIN_NT;
+    using DT = DualV<NT>;
+    using SV = SeedTypes<D, G, DT>;
+#pragma unroll 1
+    for (int dir0 = 0; dir0 < NS; dir0 += NT) {
+      typename SV::F fd;
+      seed_dirs<D, G, NT>(fn, cp, dir0, fd);
+      QFlux<D, DT> fx;
+      bool dg = false;
+      qflux<D, typename SV::TV, typename SV::TU, typename SV::TP>(ph, st, solid, fd, fo, fx, dg);
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const int dir = dir0 + k;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          sg[((i * NS + 0) * NS + dir) * T] = fx.vec[i].d[k];
+          sg[(((D + i) * NS + 0) * NS + dir) * T] = fx.uvec[i].d[k];
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            sg[((i * NS + 1 + j) * NS + dir) * T] = fx.ten[i][j].d[k];
+            sg[(((D + i) * NS + 1 + j) * NS + dir) * T] = fx.uten[i][j].d[k];
+          }
+        }
+        sg[((2 * D * NS + 0) * NS + dir) * T] = fx.pv.d[k];
+#pragma unroll
+        for (int j = 0; j < D; ++j) sg[((2 * D * NS + 1 + j) * NS + dir) * T] = fx.pt[j].d[k];
+      }
+    }
+  } else {
     // volume point: fields interpolated by the caller from the staged node values
 #pragma unroll 1
     for (int dir = 0; dir < NS; ++dir) {
@@ -480,6 +514,7 @@ __global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(M
     for (int o = 0; o < NS; ++o) ta_r[o] = ta[o];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
+      if (!row_couples(c, cp, D)) continue;  // structural zero plane: never computed, never scattered
       // u rows of a node without the extension row: value-tested part only
       const bool full = !(c >= D && c < 2 * D) || ext;
       double h[NS];
@@ -538,12 +573,12 @@ __global__ void __launch_bounds__(JacLin<D>::T, JacLin<D>::OCC) k_jacobian_lin(M
   for (int b = 0; b < A; ++b)
 #pragma unroll
     for (int c = 0; c < C; ++c)
-      if (!(c == 2 * D && solid)) K[c][b] += o[idx(b, c)];
+      if (!(c == 2 * D && solid) && row_couples(c, cp, D)) K[c][b] += o[idx(b, c)];
 #pragma unroll
   for (int b = 0; b < A; ++b)
 #pragma unroll
     for (int c = 0; c < C; ++c)
-      if (!(c == 2 * D && solid)) o[idx(b, c)] = K[c][b];
+      if (!(c == 2 * D && solid) && row_couples(c, cp, D)) o[idx(b, c)] = K[c][b];
 }
 
 // ---------------------------------------------------------------- K2 Jacobian, node-owner strips (2-d default)
