@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
     for (int k = 0; k < PER; ++k) {
       const int idx = lane + k * T;
       const int col = idx % RW, c = (idx / RW) % C, lvl = idx / (RW * C);
+      PINT_CHECK_IDX(!(lvl < 2 && col < ncol) || (c_lo + col <= nx && r >= 0 && r <= ny));
       v[k] = (lvl < 2 && col < ncol) ? __ldg((lvl == 0 ? ys : yos) + (size_t)c * np + node_index(m.g, c_lo + col, r, 0))
                                      : 0.0;
     }
@@ -873,6 +874,7 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
         if (ci < 0 || ci >= nx) return;
         if (!row_couples(ca, cp, D)) return;                // structural zero plane (u_i row, column not v_i / u_i)
         const int lcell = ci - c_lo;
+        PINT_CHECK_IDX(lcell >= 0 && lcell < 32 && lcell < ncell && it < L::ITEMS && cj >= 0 && cj < ny);
         const uint8_t cf = m.cell_flags[cj * nx + ci];
         const bool solid = cf & kCellSolid;
         if (ca == 2 * D && solid) return;                   // solid cells own no p rows
@@ -924,6 +926,7 @@ __global__ void __launch_bounds__(JacStrip::T, 3) k_jacobian_strip(MeshDev m, Ph
       };
       auto write_row = [&](int j, const double (&Kx)[9]) {
         const int n = node_index(m.g, i, j, 0);
+        PINT_CHECK_IDX(n >= 0 && n < m.g.nn && i <= nx && j <= ny);
         const uint8_t nf = m.node_flags[n];
         const bool fixed = row_fixed(nf, ca, D);
         const int ctr = center_offset(D);
@@ -1047,6 +1050,7 @@ __global__ void __launch_bounds__(ResStrip::T, 3) k_residual_strip(MeshDev m, Ph
     for (int k = 0; k < PER; ++k) {
       const int idx = lane + k * T;
       const int col = idx % RW, c = (idx / RW) % C, lvl = idx / (RW * C);
+      PINT_CHECK_IDX(!(lvl < 2 && col < ncol) || (c_lo + col <= nx && rr >= 0 && rr <= ny));
       v[k] = (lvl < 2 && col < ncol) ? __ldg((lvl == 0 ? ys : yos) + (size_t)c * np + node_index(m.g, c_lo + col, rr, 0))
                                      : 0.0;
     }
@@ -1144,6 +1148,7 @@ __global__ void __launch_bounds__(ResStrip::T, 3) k_residual_strip(MeshDev m, Ph
       auto cell_term = [&](int ci, int a) -> double {
         if (ci < 0 || ci >= nx) return 0.0;
         const int lcell = ci - c_lo;
+        PINT_CHECK_IDX(lcell >= 0 && lcell < 32 && lcell < ncell && it < L::ITEMS);
         const uint8_t cf = m.cell_flags[cj * nx + ci];
         const bool solid = cf & kCellSolid;
         if (ca == 2 * D && solid) return 0.0;               // solid cells own no p rows
@@ -1185,6 +1190,7 @@ __global__ void __launch_bounds__(ResStrip::T, 3) k_residual_strip(MeshDev m, Ph
       };
       auto write_row = [&](int j, double R) {
         const int n = node_index(m.g, i, j, 0);
+        PINT_CHECK_IDX(n >= 0 && n < m.g.nn && (i - c_lo) >= 0 && (i - c_lo) < RW);
         const uint8_t nf = m.node_flags[n];
         double out = R;
         if (row_fixed(nf, ca, D)) {

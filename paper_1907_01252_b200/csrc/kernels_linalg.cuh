@@ -1564,6 +1564,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_build(Grid g
       const int bx = (a & 1) + di, by = ((a >> 1) & 1) + dj, bz = D == 3 ? ((a >> 2) & 1) + dk : 0;
       if (cell_of[a] < 0 || bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
       const int b = bx + 2 * by + 4 * bz;
+      PINT_CHECK_IDX(b >= 0 && b < A && cell_of[a] < ncell && o < NOFF);
       const float* Vr = Vs + ((size_t)(a * C + ca) * L + (size_t)b * C) * ncell + cell_of[a];
 #pragma unroll
       for (int cb = 0; cb < C; ++cb) acc[cb] += (double)__ldg(Vr + (size_t)cb * ncell);
@@ -1636,6 +1637,7 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g
     for (int q = 0; q < 9; ++q) {
       const int o = o0 + q;
       const int di = o % 3 - 1, row = o / 3;  // row = (dj + 1) + 3 (dk + 1): the staged node-row range
+      PINT_CHECK_IDX(row >= 0 && row < R && (int)threadIdx.x + 1 + di >= 0 && (int)threadIdx.x + 1 + di < W);
 #pragma unroll
       for (int cb = 0; cb < C; ++cb) p[cb & 3] = fmaf(v[q][cb], rs[cb][row][threadIdx.x + 1 + di], p[cb & 3]);
     }
@@ -1692,6 +1694,7 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
         int fi, fj, fk;
         node_coords(g, m, fi, fj, fk);
         v = v + prolong_sum<D>(gc, ec + (size_t)s * C * gc.np + (size_t)cb * gc.np, fi, fj, fk);
+        PINT_CHECK_IDX(m < g.np);
         if (q == RC && w >= 1 && w <= 32) xnew[(size_t)s * C * g.np + (size_t)cb * g.np + m] = v;
       }
     }
@@ -1700,6 +1703,7 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
   __syncthreads();
   const int n = n0 + threadIdx.x;
   if (n >= g.nn) return;
+  PINT_CHECK_IDX(n >= 0 && n < g.nn && g.nn <= g.np && (int)blockDim.y == NW);
   const float* As = A + (size_t)s * NOFF * C * C * g.np + n;
   const size_t vbase = (size_t)s * C * g.np + n;
   if (PINT_PATTERN && threadIdx.y == D + 1) {
@@ -2180,6 +2184,7 @@ __device__ __forceinline__ void tail_vanka_stencil(const LevelDev& L, int s, con
     for (int q = 0; q < OPL; ++q) {
       const int off = part + P * q;
       const int nb = (ok && off < NOFF) ? neighbour(L.g, i, j, k, off) : -1;
+      PINT_CHECK_IDX(nb < L.g.nn && (!ok || (n < L.g.nn && ca < C)));
 #pragma unroll
       for (int cb = 0; cb < C; ++cb) {
         a[q][cb] = nb >= 0 ? ld_nc(Srow + ((size_t)off * C * C + cb) * np) : 0.0f;

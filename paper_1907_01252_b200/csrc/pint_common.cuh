@@ -7,6 +7,8 @@
 // per node reads every coefficient with unit stride across the warp.
 #pragma once
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,6 +20,23 @@ namespace pint {
 // the grid it depends on (a no-op when launched without the PDL attribute),
 // so the host may launch it while its predecessor drains (pint_launch).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// -DPINT_BOUNDS=1: device-side index checks in the round-2 kernels (the pool's
+// compute-sanitizer is closed; tools/jobs/r02_bounds.sh runs the GPU tests on
+// such a build).  A failed check prints its location and traps, which surfaces
+// as a CUDA error in the next API call.
+#if defined(PINT_BOUNDS) && PINT_BOUNDS
+#define PINT_CHECK_IDX(cond)                                                                      \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("PINT_BOUNDS violated: %s at %s:%d (block %d,%d,%d thread %d,%d)\n", #cond, __FILE__, __LINE__, \
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, threadIdx.y);                       \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define PINT_CHECK_IDX(cond) ((void)0)
+#endif
 
 constexpr int kMaxDim = 3;
 
