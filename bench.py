@@ -448,7 +448,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pre", type=int, default=1, help="multigrid pre-smoothing sweeps")
     ap.add_argument("--post", type=int, default=1, help="multigrid post-smoothing sweeps")
-    ap.add_argument("--omega", type=float, default=0.9, help="smoother damping")
+    ap.add_argument("--omega", type=float, default=0.0, help="smoother damping (0: the library default, 0.9)")
     ap.add_argument("--smoother", default="vanka", choices=("vanka", "jacobi"))
     ap.add_argument("--reuse", type=int, default=64,
                     help="rebuild the multigrid hierarchy every k steps (or on Krylov-count drift)")

@@ -79,7 +79,7 @@ class KrylovSettings:
     max_iters: int = 300
     pre_smooth: int = 1
     post_smooth: int = 1
-    omega: float = 0.9
+    omega: float = 0.0          # smoother damping; 0 = default (Vanka 0.9, node-block Jacobi 0.5)
     max_levels: int = 0
     coarse_sweeps: int = 20
     smoother: str = "vanka"    # "vanka" (cell patches) or "jacobi" (node blocks, omega ~0.5)
@@ -94,14 +94,24 @@ class KrylovSettings:
             raise ValueError("restart and max_iters must be positive")
         if self.pre_smooth < 1 or self.post_smooth < 1:
             raise ValueError("need at least one pre- and post-smoothing sweep")
-        if not 0.0 < self.omega <= 1.0:
-            raise ValueError("omega must lie in (0, 1]")
+        if not 0.0 <= self.omega <= 1.0:
+            raise ValueError("omega must lie in (0, 1] (0 selects the default of the mesh dimension)")
         if self.smoother not in ("vanka", "jacobi"):
             raise ValueError("smoother must be 'vanka' or 'jacobi'")
 
-    def c_struct(self) -> _lib.KrylovOpts:
+    def resolved_omega(self, dim: int) -> float:
+        """Additive Vanka damping.  0.9 in both dimensions: in 2-d 1.0 is 1-4 %
+        faster on the FINE steps of c1/c2/c3 (profiles/r02_omega_2d.jsonl) but
+        2-3x slower on the coarse implicit-Euler steps of c3 and 15 % slower on
+        its shifted-CN coarse steps, and 5 % slower on c4 -- the robust value
+        stays the default; pass omega explicitly to tune one propagator."""
+        if self.omega > 0.0:
+            return self.omega
+        return 0.5 if self.smoother == "jacobi" else 0.9
+
+    def c_struct(self, dim: int = 3) -> _lib.KrylovOpts:
         return _lib.KrylovOpts(self.rtol, self.atol, self.restart, self.max_iters, self.pre_smooth,
-                               self.post_smooth, self.omega, self.max_levels, self.coarse_sweeps,
+                               self.post_smooth, self.resolved_omega(dim), self.max_levels, self.coarse_sweeps,
                                1 if self.smoother == "vanka" else 0, int(self.precond_reuse),
                                float(self.rtol_first))
 
@@ -283,7 +293,7 @@ class FSIDevice:
         return out
 
     def precond_setup(self, S, krylov: KrylovSettings):
-        ko = krylov.c_struct()
+        ko = krylov.c_struct(self.problem.dim)
         self.check(self.lib.pint_precond_setup(self.handle, S, ctypes.byref(ko), _stream()), "pint_precond_setup")
 
     def precond_apply(self, b, out=None):
@@ -295,7 +305,7 @@ class FSIDevice:
     def linear_solve(self, b, krylov: KrylovSettings, out=None):
         S = b.shape[0]
         out = out if out is not None else self.empty(S)
-        ko = krylov.c_struct()
+        ko = krylov.c_struct(self.problem.dim)
         its = (ctypes.c_int32 * S)()
         res = (ctypes.c_double * S)()
         self.check(self.lib.pint_linear_solve(self.handle, S, _ptr(b), _ptr(out), ctypes.byref(ko), its, res,
@@ -306,7 +316,7 @@ class FSIDevice:
         """Unpreconditioned GMRES on J(y) x = b with the matrix-free K2' operator."""
         S = b.shape[0]
         out = out if out is not None else self.empty(S)
-        ko = krylov.c_struct()
+        ko = krylov.c_struct(self.problem.dim)
         its = (ctypes.c_int32 * S)()
         res = (ctypes.c_double * S)()
         self.check(self.lib.pint_linear_solve_mf(self.handle, S, _ptr(y), _ptr(y_old), _darr(k), _darr(theta),
@@ -342,7 +352,7 @@ class FSIDevice:
         host arrays (theta, corr, newton its, krylov its, status, fail t)."""
         L = len(nsteps)
         no = _lib.NewtonOpts(newton.abs_tol, newton.rel_tol, newton.max_iters, newton.damping_min)
-        ko = krylov.c_struct()
+        ko = krylov.c_struct(self.problem.dim)
         th, cr, ft = (ctypes.c_double * L)(), (ctypes.c_double * L)(), (ctypes.c_double * L)()
         nit, kit, status = (ctypes.c_int32 * L)(), (ctypes.c_int32 * L)(), (ctypes.c_int32 * L)()
         ns = (ctypes.c_int32 * L)(*[int(n) for n in nsteps])
@@ -371,7 +381,7 @@ class FSIDevice:
         S = y_in.shape[0]
         y_out = y_out if y_out is not None else self.empty(S)
         no = _lib.NewtonOpts(newton.abs_tol, newton.rel_tol, newton.max_iters, newton.damping_min)
-        ko = krylov.c_struct()
+        ko = krylov.c_struct(self.problem.dim)
         nit = (ctypes.c_int32 * S)()
         kit = (ctypes.c_int32 * S)()
         status = (ctypes.c_int32 * S)()
