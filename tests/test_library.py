@@ -61,3 +61,20 @@ def test_missing_library_raises(tmp_path):
             _lib.load(str(tmp_path / "nope.so"))
     finally:
         _lib._lib = saved
+
+
+def test_krylov_settings_defaults_reach_the_c_struct():
+    """Host-side solver settings: omega = 0 selects the library default of the
+    smoother (Vanka 0.9 in both dimensions, node-block Jacobi 0.5), an explicit
+    omega is passed through, and the C struct carries the reuse period and the
+    first-iteration forcing."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    ks = KrylovSettings()
+    assert ks.resolved_omega(2) == 0.9 and ks.resolved_omega(3) == 0.9
+    assert KrylovSettings(smoother="jacobi").resolved_omega(2) == 0.5
+    assert KrylovSettings(omega=0.8).resolved_omega(3) == 0.8
+    c = ks.c_struct(2)
+    assert c.omega == 0.9 and c.smoother == 1 and c.precond_reuse == 64 and c.restart == 30
+    assert abs(c.rtol_first - 3e-5) < 1e-20
+    with pytest.raises(ValueError):
+        KrylovSettings(omega=1.5)
