@@ -1662,11 +1662,10 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g
 // one full row (2-d: 36 vs 45 loads, 3-d: 162 vs 189).  With a warp per row the
 // deformation warps finished early and idled their slots (ncu: 52 % of the
 // warp slots active, 0.77 of HBM peak on c3 level 0).
-#ifndef PINT_RESID_MINB3
-#define PINT_RESID_MINB3 1  // resident blocks per SM the 3-d staged residual is compiled for (register cap)
-#endif
+// (no minimum-blocks launch bound: ptxas settles at 56 registers in 2-d on its own; an explicit bound of 1
+// lets it take 116 and costs 10 % of the c3 step, caps of 40-96 registers were measured slower or equal)
 template <int D, bool PROLONG>
-__global__ void __launch_bounds__(32 * (D + 2), (D == 3 ? PINT_RESID_MINB3 : 1)) k_resid32_staged(Grid g, const float* __restrict__ A,
+__global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const float* __restrict__ A,
                                                                const double* __restrict__ x,
                                                                const double* __restrict__ b,
                                                                double* __restrict__ y,
