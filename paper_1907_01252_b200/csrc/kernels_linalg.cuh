@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "pint_common.cuh"
 
@@ -1664,7 +1665,10 @@ __global__ void __launch_bounds__(32 * (2 * D + 1)) k_vanka_stencil_apply(Grid g
 // warp slots active, 0.77 of HBM peak on c3 level 0).
 // (no minimum-blocks launch bound: ptxas settles at 56 registers in 2-d on its own; an explicit bound of 1
 // lets it take 116 and costs 10 % of the c3 step, caps of 40-96 registers were measured slower or equal)
-template <int D, bool PROLONG>
+// ACC32: fp32 products and partial sums (as the Vanka sweep), the staged x converted once -- no fp32 -> fp64
+// conversions and fp64 FMAs in the inner loop; the result differs from the fp64 accumulation by fp32 round-off
+// of a preconditioner-side residual (PINT_RESID_ACC=f32, off by default)
+template <int D, bool PROLONG, bool ACC32 = false>
 __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const float* __restrict__ A,
                                                                const double* __restrict__ x,
                                                                const double* __restrict__ b,
@@ -1679,7 +1683,8 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
   constexpr int W = 34;
   constexpr int RC = D == 2 ? 1 : 4;  // the centre node-row range (dj = dk = 0)
   constexpr int NW = D + 2;           // warps per block
-  __shared__ double xs[C][R][W];
+  using XT = std::conditional_t<ACC32, float, double>;
+  __shared__ XT xs[C][R][W];
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const int n0 = blockIdx.x * 32;
@@ -1700,7 +1705,7 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
         if (q == RC && w >= 1 && w <= 32) xnew[(size_t)s * C * g.np + (size_t)cb * g.np + m] = v;
       }
     }
-    xs[cb][q][w] = v;
+    xs[cb][q][w] = (XT)v;
   }
   __syncthreads();
   const int n = n0 + threadIdx.x;
@@ -1715,7 +1720,7 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
       const int ca = D + i, c0 = i, c1 = D + i;
       const float* Ar = As + (size_t)ca * C * g.np;
       const double bv = __ldg(b + vbase + (size_t)ca * g.np);
-      double part[3] = {0.0, 0.0, 0.0};
+      XT part[3] = {0, 0, 0};
       float v[NOFF][2];
 #pragma unroll
       for (int o = 0; o < NOFF; ++o) {
@@ -1725,10 +1730,10 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
 #pragma unroll
       for (int o = 0; o < NOFF; ++o) {
         const int di = o % 3 - 1, row = o / 3;
-        part[o % 3] = fma((double)v[o][0], xs[c0][row][threadIdx.x + 1 + di], part[o % 3]);
-        part[o % 3] = fma((double)v[o][1], xs[c1][row][threadIdx.x + 1 + di], part[o % 3]);
+        part[o % 3] = fma((XT)v[o][0], xs[c0][row][threadIdx.x + 1 + di], part[o % 3]);
+        part[o % 3] = fma((XT)v[o][1], xs[c1][row][threadIdx.x + 1 + di], part[o % 3]);
       }
-      y[vbase + (size_t)ca * g.np] = bv - ((part[0] + part[1]) + part[2]);
+      y[vbase + (size_t)ca * g.np] = bv - (double)((part[0] + part[1]) + part[2]);
     }
     return;
   }
@@ -1740,7 +1745,7 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
     const int ca = threadIdx.y < D ? threadIdx.y : (threadIdx.y == D ? 2 * D : D + i);
     const float* Ar = As + (size_t)ca * C * g.np;
     const double bv = __ldg(b + vbase + (size_t)ca * g.np);
-    double part[3] = {0.0, 0.0, 0.0};
+    XT part[3] = {0, 0, 0};
 #pragma unroll
     for (int o0 = 0; o0 < NOFF; o0 += 9) {
       float v[9][C];
@@ -1754,10 +1759,10 @@ __global__ void __launch_bounds__(32 * (D + 2)) k_resid32_staged(Grid g, const f
         const int di = o % 3 - 1, row = o / 3;
 #pragma unroll
         for (int cb = 0; cb < C; ++cb)
-          part[o % 3] = fma((double)v[q][cb], xs[cb][row][threadIdx.x + 1 + di], part[o % 3]);
+          part[o % 3] = fma((XT)v[q][cb], xs[cb][row][threadIdx.x + 1 + di], part[o % 3]);
       }
     }
-    y[vbase + (size_t)ca * g.np] = bv - ((part[0] + part[1]) + part[2]);
+    y[vbase + (size_t)ca * g.np] = bv - (double)((part[0] + part[1]) + part[2]);
   }
 }
 

@@ -153,6 +153,7 @@ struct pint_ctx {
                                 // measured slower: c3 0.64 vs 0.45 ms -- the per-row barriers outweigh the saved passes)
   int res_waves = 4;            // PINT_RES_WAVES: target waves of strip-residual blocks (more chunks, shorter sweeps)
   bool jac_mt = true;           // PINT_JAC_MT=0: one dual pass per direction in the strip Jacobian (round-2 first form)
+  bool resid_acc32 = false;     // PINT_RESID_ACC=f32: fp32 accumulation in the staged V-cycle residual
   int strip_w = 25;             // PINT_STRIP_W: owned node columns per Jacobian strip (<= 31)
   bool fuse_prolong = false;    // PINT_FUSE_PROLONG=1: coarse-grid correction inside the post-smoothing residual kernel
                                 // (bitwise k_prolong_add + residual; measured slower: c3 863 vs 881, c4 874 vs 879)
@@ -629,8 +630,12 @@ struct Impl {
     // CTAs (c3 levels 0-1: +4.6 %); below that the (node, row) threads hide
     // latency better (c2, L2-resident: -3 % with the node kernel)
     if (resid_staged(ctx, L, S)) {
-      pint_launch(ctx, st, k_resid32_staged<D, false>, row_grid(L.g.nn, S), dim3(32, D + 2), 0, L.g,
-                  (const float*)L.A32, x, b, r, mask, L.g, (const double*)nullptr, (double*)nullptr);
+      if (ctx->resid_acc32)
+        pint_launch(ctx, st, k_resid32_staged<D, false, true>, row_grid(L.g.nn, S), dim3(32, D + 2), 0, L.g,
+                    (const float*)L.A32, x, b, r, mask, L.g, (const double*)nullptr, (double*)nullptr);
+      else
+        pint_launch(ctx, st, k_resid32_staged<D, false>, row_grid(L.g.nn, S), dim3(32, D + 2), 0, L.g,
+                    (const float*)L.A32, x, b, r, mask, L.g, (const double*)nullptr, (double*)nullptr);
     } else if (L.A32 && ctx->spmv32_node && (size_t)L.g.nn * S >= ctx->spmv32_min) {
       pint_launch(ctx, st, k_spmv_node<D, true, float>, node_grid(L.g.nn, S), 128, 0, L.g, (const float*)L.A32, x, b, r,
                   mask);
@@ -2008,6 +2013,7 @@ int pint_create_ex(const pint_problem_desc* desc, int32_t max_slices, int32_t re
   ctx->spmv32_staged = !std::getenv("PINT_SPMV32") || std::string(std::getenv("PINT_SPMV32")) == "staged";
   if (const char* e = std::getenv("PINT_SPMV32_MIN")) ctx->spmv32_min = (size_t)std::atoll(e);
   if (const char* e = std::getenv("PINT_STRIP_W")) ctx->strip_w = std::atoi(e);
+  if (const char* e = std::getenv("PINT_RESID_ACC")) ctx->resid_acc32 = std::string(e) == "f32";
   if (const char* e = std::getenv("PINT_JAC_MT")) ctx->jac_mt = e[0] == '1';
   if (const char* e = std::getenv("PINT_RES")) ctx->res_strip = std::string(e) == "strip";
   if (const char* e = std::getenv("PINT_RES_WAVES")) ctx->res_waves = std::max(1, std::atoi(e));

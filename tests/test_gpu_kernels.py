@@ -344,6 +344,30 @@ def test_spmv32_variants_bitwise(cuda, name, tail_rows):
     assert np.array_equal(outs[1], outs[2]), name
 
 
+@pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("small3d", "300")])
+def test_resid32_fp32_accumulation_variant(cuda, name, tail_rows):
+    """PINT_RESID_ACC=f32 (opt-in): the staged V-cycle residual with fp32
+    products and partial sums.  It is off by default because it would make a
+    slice's bits depend on whether its batch crosses the staged-kernel
+    threshold; one V-cycle agrees with the fp64 accumulation to 1e-5."""
+    from paper_1907_01252_b200.propagator import KrylovSettings
+    P = PROBLEMS[name]
+    S = 2
+    Y = random_states(P, S, 79, scale_u=1e-4) * 0.1
+    B = random_states(P, S, 80, scale_u=1.0)
+    k, th, t1 = _step_args(S)
+    outs = []
+    for acc in ("f64", "f32"):
+        dev = _device_with_env(P, {"PINT_RESID_ACC": acc, "PINT_SPMV32_MIN": "0", "PINT_TAIL_ROWS": tail_rows}, S)
+        y = dev.to_device(Y)
+        dev.assemble(y, y, k, th, t1)
+        dev.precond_setup(S, KrylovSettings())
+        outs.append(dev.to_host(dev.precond_apply(dev.to_device(B))))
+    for s in range(S):
+        assert np.linalg.norm(outs[0][s] - outs[1][s]) <= 1e-5 * np.linalg.norm(outs[0][s]), (name, s)
+    assert not np.array_equal(outs[0], outs[1])  # the variant really ran
+
+
 @pytest.mark.parametrize("name,tail_rows", [("c1", "1000"), ("c1", "100"), ("small3d", "300")])
 def test_fused_prolongation_bitwise(cuda, name, tail_rows):
     """The coarse-grid correction added inside the post-smoothing residual
